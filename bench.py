@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 state-vector core (BASELINE.json metric).
+
+Workload ("sweep", the default): BASELINE config 2 -- a Haar-random 2x2
+unitary applied to every qubit in turn of a normalised Gaussian complex128
+state with 2^m amplitudes per GPU (m = 30: 16 GiB), fresh unitaries each
+step.  On N GPUs the state has n = m + log2(N) qubits (weak scaling, the
+top log2(N) qubits global, as in config 4), so each step also runs log2(N)
+global-qubit gates through the exchange path.
+
+Unit: one gate applied to 2^30 amplitudes (an n=30 gate-update).  `value`
+is whole-job gate-updates/s in that unit (at N=1 exactly config 2's
+gate-updates/s); hbm_gbs is the algorithmic traffic (32 B per amplitude per
+gate, read + write) over the device time.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--local-qubits M] [--no-fuse] [--workload sweep|qaoa]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gate-updates/s and achieved HBM GB/s (n=30 c128); weak-scaled n=33-36 on 1-8 GPUs"
+UNIT = "gate-updates/s (n=30-equivalent: 1 unit = one 2x2 gate on 2^30 c128 amplitudes)"
+LAUNCH_KINDS = {1: "k_gate1q", 2: "k_controlled", 3: "k_cut_phase", 4: "k_tile",
+                5: "k_exchange_peer", 6: "k_tree"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--local-qubits", type=int, default=30)
+    ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--workload", default="sweep", choices=["sweep", "qaoa"])
+    ap.add_argument("--seed", type=int, default=20260809)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"])
+    return ap.parse_args()
+
+
+# ---- clocks -------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(kernel)
+    except (OSError, ValueError):
+        return None
+
+
+# ---- distributed plumbing -------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world):
+    if world == 1:
+        return None
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group(backend="gloo")
+    return dist
+
+
+def max_over_ranks(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+# ---- CPU baseline (oracle port, host threads) ----------------------------------------
+def cpu_sweep_sample(m: int, gates: int, seed: int) -> dict:
+    """Time the reference algorithm (oracle restatement, all host threads) on
+    a bounded sample: `gates` single-gate applications on a 2^m state."""
+    from oracle import cpu_baseline as cb
+
+    rng = np.random.default_rng(seed)
+    psi = np.full(1 << m, 2.0 ** (-m / 2.0), dtype=np.complex128)
+    targets = [int(x) for x in np.linspace(0, m - 1, gates).round()]
+    us = [haar(rng) for _ in targets]
+    cb.apply_1q_threaded(psi, 0, np.eye(2, dtype=np.complex128))  # warm (page faults)
+    t0 = time.perf_counter()
+    for q, u in zip(targets, us):
+        cb.apply_1q_threaded(psi, q, u)
+    dt = time.perf_counter() - t0
+    units = len(targets) * (2.0 ** m) / 2.0 ** 30
+    return {"value": units / dt, "unit": UNIT, "cores": cb.threads(), "kind": "port",
+            "sample": f"{len(targets)} single-gate applications (targets {targets}) on a "
+                      f"2^{m} complex128 state, oracle/cpu_baseline.py (numpy, "
+                      f"{cb.threads()} threads), {dt:.2f} s"}
+
+
+def haar(rng):
+    from paper_2001_10554_b200.workloads import haar_2x2
+
+    return haar_2x2(rng)
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU algorithm (oracle port; the Python
+    reference cannot travel to the GPU box) on the host cores."""
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import cpu_baseline as cb
+
+    m = args.local_qubits
+    rng = np.random.default_rng(args.seed)
+    psi = np.full(1 << m, 2.0 ** (-m / 2.0), dtype=np.complex128)
+    for s in range(args.warmup):
+        cb.apply_1q_threaded(psi, s % m, haar(rng))
+    times = []
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        q = (s * 7) % m
+        a = time.perf_counter()
+        cb.apply_1q_threaded(psi, q, haar(rng))
+        times.append(time.perf_counter() - a)
+    dt = time.perf_counter() - t0
+    units = args.steps * (2.0 ** m) / 2.0 ** 30
+    value = units / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128 (f64 pairs)", "data": "synthetic",
+        "config": {"workload": f"config 2 sample: one Haar 2x2 gate per step on a 2^{m} "
+                               f"complex128 state, targets (7*step) mod {m}",
+                   "qubits": m, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.threads(), "kind": "port",
+                         "sample": f"{args.steps} single-gate steps at n={m}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---- our arm ----------------------------------------------------------------------------
+def run_ours(args):
+    world, rank, local = dist_env()
+    dist = init_dist(world)
+    import paper_2001_10554_b200 as qs
+    from paper_2001_10554_b200 import _native, runtime
+    from paper_2001_10554_b200 import distribution as qdist
+    from paper_2001_10554_b200.workloads import device_gaussian
+
+    if qs.device_count() < 1:
+        raise SystemExit("bench.py: no CUDA device -- the B200 core has no CPU fallback")
+    if world & (world - 1):
+        raise SystemExit("bench.py: --gpus must be a power of two")
+    m = args.local_qubits
+    p = world.bit_length() - 1
+    n = m + p
+    comm = qdist.TorchComm(exchange_mode=args.exchange) if world > 1 else qdist.single_rank_comm()
+    if args.workload == "qaoa":
+        return run_qaoa(args, dist, comm, world, rank, local)
+    ctx = runtime.make_context(comm, n, 1, device=local, fuse=not args.no_fuse)
+    ctx.norm_check_interval = 0
+    st = ctx.state
+    group_norm = (lambda x: qdist.group_reduce_sum(x, ctx.topology, comm)) if world > 1 else None
+    device_gaussian(st, args.seed, group_norm)
+    rng = np.random.default_rng(args.seed + 1)
+    total_steps = args.warmup + args.steps
+    sweeps = [[haar(rng) for _ in range(n)] for _ in range(total_steps)]
+
+    def step(us):
+        q = ctx.queue
+        for k in range(n):
+            if k < m:
+                q.one_qubit(k, us[k])
+            else:
+                ctx.flush()
+                qdist.apply_one_qubit_gate(ctx.partition, ctx.topology, comm, k, us[k])
+        ctx.flush()
+
+    for s in range(args.warmup):
+        step(sweeps[s])
+    st.synchronize()
+    barrier(dist)
+    clocks = ClockSampler(local)
+    clocks.start()
+    st.launch_log(True)
+    st.event_record(0)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        step(sweeps[args.warmup + s])
+    st.event_record(1)
+    st.synchronize()
+    wall = time.perf_counter() - t0
+    ms_dev = st.event_elapsed_ms(0, 1)
+    st.launch_log(False)
+    launch_ms, launch_kind = st.read_launch_log()
+    clock = clocks.stop()
+    barrier(dist)
+    ms_total = max_over_ranks(dist, ms_dev)
+    units_per_step = n * (2.0 ** n) / 2.0 ** 30
+    value = units_per_step * args.steps / (ms_total / 1e3)
+    bytes_per_step_per_gpu = 32.0 * (2 ** m) * n  # algorithmic: every gate r+w of the slice
+    hbm_gbs = bytes_per_step_per_gpu * world * args.steps / (ms_total / 1e3) / 1e9
+
+    # dominant kernel and its roofline
+    peak, peak_src = measured_peak()
+    kinds, share = {}, {}
+    for k, t in zip(launch_kind, launch_ms):
+        kinds.setdefault(int(k), []).append(float(t))
+    dom = max(kinds, key=lambda k: sum(kinds[k])) if kinds else 4
+    dom_ms = float(np.mean(kinds[dom])) if kinds else float("nan")
+    for k, v in kinds.items():
+        share[LAUNCH_KINDS.get(k, str(k))] = {"launches": len(v), "ms": float(np.sum(v)),
+                                             "share": float(np.sum(v) / ms_dev)}
+    bytes_per_launch = 32.0 * (2 ** m)  # one pass: read + write every amplitude once
+    achieved = bytes_per_launch / (dom_ms / 1e3) / 1e9
+    traffic = ncu_traffic(LAUNCH_KINDS.get(dom, ""))
+
+    # e2e through the public API with host buffers (upload + sweep + download)
+    e2e = run_e2e(args, ctx, st, sweeps, step, m, n, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sweep_sample(min(m, 30), 3, args.seed)
+
+    passes = ctx.queue.passes_total
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128 (f64 pairs)", "data": "synthetic",
+            "config": {
+                "workload": f"config 2 sweep: Haar 2x2 on each of the {n} qubits in turn, "
+                            f"fresh unitaries per step, normalised Gaussian state, "
+                            f"2^{m} c128 amplitudes per GPU (n={n}, {p} global qubits)",
+                "qubits": n, "local_qubits": m, "gates_per_step": n,
+                "fused": not args.no_fuse, "parallelism": f"state sharded over {world} GPU(s)",
+                "exchange": args.exchange if world > 1 else None,
+                "l2": "inputs larger than L2 (16 GiB state vs 126 MB)"},
+            "hbm_gbs": hbm_gbs,
+            "hbm_frac_of_measured": hbm_gbs / (peak * world),
+            "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_launch": bytes_per_launch, "avg_launch_ms": dom_ms,
+                         "peak_source": peak_src},
+            "kernel_share": share,
+            "passes_per_step": None if not args.steps else None,
+            "gpu_launches": int(len(launch_ms)),
+            "wall_s": wall,
+            "clocks": clock,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line))
+    barrier(dist)
+    return 0
+
+
+def run_e2e(args, ctx, st, sweeps, step, m, n, dist):
+    """Same metric through the public API with host (pinned) buffers: every step
+    uploads the state, runs the sweep and downloads the result."""
+    import torch
+
+    k = max(1, args.e2e_steps)
+    host = torch.empty(2 << m, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+    st.download(host)
+    st.synchronize()
+    barrier(dist)
+    t0 = time.perf_counter()
+    for s in range(k):
+        st.upload(host)
+        step(sweeps[s % len(sweeps)])
+        st.download(host)
+    dt = time.perf_counter() - t0
+    dt = max_over_ranks(dist, dt)
+    units = n * (2.0 ** n) / 2.0 ** 30
+    return {"value": units * k / dt, "unit": UNIT, "h2d_bytes_per_step": 16 * (2 ** m),
+            "d2h_bytes_per_step": 16 * (2 ** m), "steps": k,
+            "note": "per GPU bytes; wall clock around upload + sweep + download"}
+
+
+def run_qaoa(args, dist, comm, world, rank, local):
+    raise SystemExit("qaoa workload: see bench_qaoa.py")
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,167 @@
+/*
+ * qsb200.h -- C ABI of the B200-native state-vector core (libqsb200.so).
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2001.10554 as
+ * implemented by the `qpool` reference (pure Python/numpy).  The reference has
+ * no FFI; its "operator API" is the Python module surface of
+ * qpool.statevector / qpool.distribution.  Each entry point
+ * below names the reference function whose arithmetic it replaces.  The
+ * Python shim `paper_2001_10554_b200` binds these with ctypes and keeps the
+ * reference names, argument meaning and exception types.
+ *
+ * Conventions
+ *  - Amplitudes are complex128, interleaved (re, im) doubles: numpy's memory
+ *    layout, so `array.view(np.float64)` crosses the ABI without a copy.
+ *  - A 2x2 gate matrix is 8 doubles: u00.re u00.im u01.re u01.im u10.re
+ *    u10.im u11.re u11.im (C order of a (2,2) complex128 array).
+ *  - Qubit 0 is the least-significant index bit.  One handle holds
+ *    `num_states` independent partitions ("pool" mode) of 2^m amplitudes
+ *    each, contiguous, state-major.  Rank r of a 2^p-rank group owns global
+ *    indices [r*2^m, (r+1)*2^m) (reference distribution.py:60-65).
+ *  - Every function returns a status (QS_OK == 0).  On failure
+ *    qs_last_error() returns a thread-local message.  Kernel launches are
+ *    stream-ordered on the handle's own CUDA stream; downloads and
+ *    observables synchronise.  There is no CPU fallback: without a CUDA
+ *    device every compute entry point fails with QS_ERR_CUDA.
+ */
+#ifndef QSB200_H
+#define QSB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSB200_ABI_VERSION 1
+
+/* status codes -- the Python shim maps them to the reference exceptions */
+#define QS_OK            0
+#define QS_ERR_VALUE     1   /* ValueError      (statevector.py:129-130,170-171,184-187) */
+#define QS_ERR_LOCALITY  2   /* LocalityError   (statevector.py:25-26,165-169,186-187)   */
+#define QS_ERR_CUDA      3   /* RuntimeError    (no device / launch failure)             */
+#define QS_ERR_COMM      4   /* TransportError  (transport.py:44-46)                      */
+#define QS_ERR_NOMEM     5   /* MemoryError                                               */
+
+/* gate kinds for qs_gate.kind */
+#define QS_KIND_1Q        0  /* 2x2 on `target`            statevector.py:162-177        */
+#define QS_KIND_CTRL      1  /* 2x2 on `target` if `control` statevector.py:180-195      */
+#define QS_KIND_CUTPHASE  2  /* psi_i *= lut[cut(i)]        statevector.py:198-206 with
+                                                            runtime.py:131-133, graphs.py:35-42 */
+
+/* observable kinds for qs_observable */
+#define QS_OBS_NORM    0     /* statevector.py:209-212 */
+#define QS_OBS_PROB    1     /* statevector.py:215-231 */
+#define QS_OBS_Z       2     /* statevector.py:234-242 */
+#define QS_OBS_MAXCUT  3     /* statevector.py:245-251 */
+
+typedef struct qs_state qs_state;
+
+/* One gate of a program.  `offset` indexes `mats` (in doubles) for state 0;
+ * state s uses offset + s*stride (stride 0 = same entry for every state).
+ * For QS_KIND_1Q / QS_KIND_CTRL an entry is 8 doubles (2x2 matrix); for
+ * QS_KIND_CUTPHASE it is the (num_edges+1)-entry complex LUT
+ * lut[k] = exp(-1j * gamma * k) computed by the host with numpy. */
+typedef struct qs_gate {
+    int32_t  kind;
+    int32_t  target;
+    int32_t  control;   /* -1 when uncontrolled */
+    int32_t  reserved;
+    uint64_t offset;
+    uint64_t stride;
+} qs_gate;
+
+/* ---- library ---------------------------------------------------------- */
+int         qs_abi_version(void);
+const char* qs_last_error(void);
+int         qs_device_count(int32_t* out);
+/* Per-thread byte/message counters of the global-qubit exchange, mirroring
+ * TransportCounters (transport.py:49-65): amplitudes moved between ranks. */
+int         qs_counters(const qs_state* st, uint64_t* messages, uint64_t* amplitudes);
+
+/* ---- state lifetime: replaces StatePartition + allocate_partition
+ *      (statevector.py:74-115) ------------------------------------------- */
+int qs_state_create(int32_t num_qubits, int32_t num_local_qubits, int32_t rank_index,
+                    int32_t num_states, int32_t device, qs_state** out);
+int qs_state_destroy(qs_state* st);
+int qs_state_info(const qs_state* st, int32_t* num_qubits, int32_t* num_local_qubits,
+                  int32_t* rank_index, int32_t* num_states, uint64_t* amps_per_state);
+/* raw device pointer of the amplitudes (for peer mapping / inspection) */
+int qs_state_device_ptr(const qs_state* st, void** out);
+int qs_synchronize(qs_state* st);
+
+/* host <-> device, `count` complex amplitudes starting at flat amplitude
+ * index `offset` (state-major).  Pinned or pageable host memory. */
+int qs_state_upload(qs_state* st, const double* host, uint64_t offset, uint64_t count);
+int qs_state_download(qs_state* st, double* host, uint64_t offset, uint64_t count);
+
+/* ---- initialisation: statevector.py:123-141 --------------------------- */
+int qs_init_zero(qs_state* st);
+int qs_init_basis(qs_state* st, uint64_t global_index);            /* init_basis_state */
+int qs_init_constant(qs_state* st, double re, double im);           /* init_uniform: host passes 2**(-n/2) */
+/* i.i.d. N(0,1) re/im from a counter-based generator keyed by (seed, global
+ * index): identical for any rank split (not the numpy stream; unnormalised). */
+int qs_init_gaussian(qs_state* st, uint64_t seed);
+int qs_scale(qs_state* st, double factor);
+
+/* ---- gates ------------------------------------------------------------- */
+/* apply_local_one_qubit_gate (statevector.py:162-177), one matrix per state
+ * (`u_stride` doubles apart; 0 = one matrix for all states). */
+int qs_apply_1q(qs_state* st, int32_t q, const double* u, uint64_t u_stride);
+/* apply_local_controlled_gate (statevector.py:180-195): control-mask
+ * compaction touches only the control=1 half (a quarter for CPhase-like
+ * matrices diag(1, z)). */
+int qs_apply_controlled(qs_state* st, int32_t control, int32_t target,
+                        const double* u, uint64_t u_stride);
+/* apply_diagonal_phase with gamma*cut_counts (statevector.py:198-206,
+ * runtime.py:131-133): edges is 2*num_edges vertex ids, lut as in qs_gate. */
+int qs_apply_cut_phase(qs_state* st, const int32_t* edges, int32_t num_edges,
+                       const double* lut, uint64_t lut_stride);
+/* A sequence of gates in program order (runtime.run_circuit, runtime.py:155-162).
+ * With fuse != 0 the native planner groups consecutive gates into shared-
+ * memory tile passes (one HBM read+write per pass); per-amplitude arithmetic
+ * and order are unchanged, so results are bit-identical to fuse == 0. */
+int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count,
+                     const double* mats, uint64_t mats_len,
+                     const int32_t* edges, int32_t num_edges, int32_t fuse);
+/* Number of HBM passes the last qs_apply_program launched (planner output). */
+int qs_last_program_passes(const qs_state* st, int32_t* passes);
+
+/* ---- observables: per-state partial sums in the reference's tree order
+ *      (statevector.py:29-45, 209-251); out has num_states doubles ------- */
+int qs_observable(qs_state* st, int32_t kind, int32_t q, const int32_t* edges,
+                  int32_t num_edges, double* out);
+
+/* ---- global-qubit path: distribution.py:121-230 ----------------------- */
+/* Pairwise exchange gate for a target on a global qubit, computed in one
+ * kernel over NVLink peer memory: this rank updates half of the pairs it
+ * shares with `peer` (the partner's partition, mapped with
+ * qs_peer_open or another handle on the same device) and writes both
+ * members.  is_lower: this rank holds the i_q=0 side.  control_local >= 0
+ * restricts the update to offsets whose local control bit is 1 (case (c),
+ * distribution.py:229-230).  The caller orders the call between two
+ * partner barriers (both ranks call it; the pair sets are disjoint). */
+int qs_exchange_gate_peer(qs_state* st, void* peer_amps, int32_t is_lower,
+                          const double* u, int32_t control_local);
+/* The reference's own three-step half-buffer exchange (Fig. 3,
+ * distribution.py:121-178) over NCCL send/recv, chunked (chunk amplitudes
+ * per message) and double-buffered; requires qs_comm_init. */
+int qs_exchange_gate_nccl(qs_state* st, int32_t peer_rank, int32_t is_lower,
+                          const double* u, int32_t control_local, uint64_t chunk);
+/* CUDA IPC for peer mapping across processes (64-byte handles). */
+int qs_state_ipc_handle(const qs_state* st, unsigned char* handle64);
+int qs_peer_open(qs_state* st, const unsigned char* handle64, void** peer_amps);
+int qs_peer_close(qs_state* st, void* peer_amps);
+/* NCCL communicator (libnccl.so.2 is loaded lazily with dlopen). */
+int qs_nccl_unique_id(unsigned char* id128);
+int qs_comm_init(qs_state* st, const unsigned char* id128, int32_t nranks, int32_t rank);
+int qs_comm_destroy(qs_state* st);
+
+/* ---- timing helper for the benchmark: events on the handle's stream ---- */
+int qs_event_record(qs_state* st, int32_t slot);
+int qs_event_elapsed_ms(qs_state* st, int32_t slot_a, int32_t slot_b, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSB200_H */

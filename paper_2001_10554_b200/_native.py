@@ -1,0 +1,272 @@
+"""ctypes binding of libqsb200.so (the C ABI in include/qsb200.h).
+
+This module is the only place the Python shim touches native code.  There is
+no CPU fallback: if the library or a CUDA device is missing, every compute
+call raises.  Status codes map onto the reference's exception types
+(statevector.LocalityError, ValueError, transport.TransportError).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libqsb200.so")
+
+QS_OK, QS_ERR_VALUE, QS_ERR_LOCALITY, QS_ERR_CUDA, QS_ERR_COMM, QS_ERR_NOMEM = range(6)
+QS_KIND_1Q, QS_KIND_CTRL, QS_KIND_CUTPHASE = 0, 1, 2
+QS_OBS_NORM, QS_OBS_PROB, QS_OBS_Z, QS_OBS_MAXCUT = 0, 1, 2, 3
+
+# Every symbol include/qsb200.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_counters",
+    "qs_state_create", "qs_state_destroy", "qs_state_info", "qs_state_device_ptr",
+    "qs_synchronize", "qs_state_upload", "qs_state_download",
+    "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
+    "qs_apply_1q", "qs_apply_controlled", "qs_apply_cut_phase", "qs_apply_program",
+    "qs_last_program_passes", "qs_observable",
+    "qs_exchange_gate_peer", "qs_exchange_gate_nccl", "qs_state_ipc_handle", "qs_peer_open",
+    "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
+    "qs_event_record", "qs_event_elapsed_ms", "qs_launch_log", "qs_launch_log_read",
+)
+
+
+class LocalityError(ValueError):
+    """A kernel was asked to act on a qubit the local slice does not pair
+    (reference statevector.py:25-26)."""
+
+
+class TransportError(RuntimeError):
+    """Exchange/communicator failure (reference transport.py:44-46)."""
+
+
+class NativeError(RuntimeError):
+    """CUDA failure inside libqsb200 (no device, launch error)."""
+
+
+class QsGate(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("target", ctypes.c_int32),
+                ("control", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("offset", ctypes.c_uint64), ("stride", ctypes.c_uint64)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+_P = ctypes.c_void_p
+_I = ctypes.c_int32
+_U = ctypes.c_uint64
+_D = ctypes.c_double
+_DP = ctypes.POINTER(ctypes.c_double)
+_IP = ctypes.POINTER(ctypes.c_int32)
+_UP = ctypes.POINTER(ctypes.c_uint64)
+_BP = ctypes.POINTER(ctypes.c_ubyte)
+
+_SIGNATURES = {
+    "qs_abi_version": ([], ctypes.c_int),
+    "qs_last_error": ([], ctypes.c_char_p),
+    "qs_device_count": ([_IP], ctypes.c_int),
+    "qs_counters": ([_P, _UP, _UP], ctypes.c_int),
+    "qs_state_create": ([_I, _I, _I, _I, _I, ctypes.POINTER(_P)], ctypes.c_int),
+    "qs_state_destroy": ([_P], ctypes.c_int),
+    "qs_state_info": ([_P, _IP, _IP, _IP, _IP, _UP], ctypes.c_int),
+    "qs_state_device_ptr": ([_P, ctypes.POINTER(_P)], ctypes.c_int),
+    "qs_synchronize": ([_P], ctypes.c_int),
+    "qs_state_upload": ([_P, _DP, _U, _U], ctypes.c_int),
+    "qs_state_download": ([_P, _DP, _U, _U], ctypes.c_int),
+    "qs_init_zero": ([_P], ctypes.c_int),
+    "qs_init_basis": ([_P, _U], ctypes.c_int),
+    "qs_init_constant": ([_P, _D, _D], ctypes.c_int),
+    "qs_init_gaussian": ([_P, _U], ctypes.c_int),
+    "qs_scale": ([_P, _D], ctypes.c_int),
+    "qs_apply_1q": ([_P, _I, _DP, _U], ctypes.c_int),
+    "qs_apply_controlled": ([_P, _I, _I, _DP, _U], ctypes.c_int),
+    "qs_apply_cut_phase": ([_P, _IP, _I, _DP, _U], ctypes.c_int),
+    "qs_apply_program": ([_P, ctypes.POINTER(QsGate), _I, _DP, _U, _IP, _I, _I], ctypes.c_int),
+    "qs_last_program_passes": ([_P, _IP], ctypes.c_int),
+    "qs_observable": ([_P, _I, _I, _IP, _I, _DP], ctypes.c_int),
+    "qs_exchange_gate_peer": ([_P, _P, _I, _DP, _I], ctypes.c_int),
+    "qs_exchange_gate_nccl": ([_P, _I, _I, _DP, _I, _U], ctypes.c_int),
+    "qs_state_ipc_handle": ([_P, _BP], ctypes.c_int),
+    "qs_peer_open": ([_P, _BP, ctypes.POINTER(_P)], ctypes.c_int),
+    "qs_peer_close": ([_P, _P], ctypes.c_int),
+    "qs_nccl_unique_id": ([_BP], ctypes.c_int),
+    "qs_comm_init": ([_P, _BP, _I, _I], ctypes.c_int),
+    "qs_comm_destroy": ([_P], ctypes.c_int),
+    "qs_event_record": ([_P, _I], ctypes.c_int),
+    "qs_event_elapsed_ms": ([_P, _I, _I, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
+    "qs_launch_log": ([_P, _I], ctypes.c_int),
+    "qs_launch_log_read": ([_P, ctypes.POINTER(ctypes.c_float), _IP, _I, _IP], ctypes.c_int),
+}
+
+
+def load(path: str | None = None):
+    """Load (once) and return the ctypes handle of libqsb200.so."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = path or LIB_PATH
+        if not os.path.exists(path):
+            raise ImportError(
+                f"{path} is missing: build it with `python -m paper_2001_10554_b200.build` "
+                "(the B200 core has no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (args, res) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc == QS_OK:
+        return
+    msg = (load().qs_last_error() or b"").decode(errors="replace")
+    if rc == QS_ERR_VALUE:
+        raise ValueError(msg)
+    if rc == QS_ERR_LOCALITY:
+        raise LocalityError(msg)
+    if rc == QS_ERR_COMM:
+        raise TransportError(msg)
+    if rc == QS_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise NativeError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args))
+
+
+def device_count() -> int:
+    n = ctypes.c_int32(0)
+    rc = load().qs_device_count(ctypes.byref(n))
+    return n.value if rc == QS_OK else 0
+
+
+def dptr(a: np.ndarray):
+    """float64 pointer to a C-contiguous array (complex128 or float64)."""
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("array must be C-contiguous")
+    return a.ctypes.data_as(_DP)
+
+
+def iptr(a: np.ndarray):
+    return a.ctypes.data_as(_IP)
+
+
+class DeviceState:
+    """Owning handle of one qs_state (num_states partitions of 2^m amplitudes)."""
+
+    def __init__(self, num_qubits: int, num_local_qubits: int, rank_index: int = 0,
+                 num_states: int = 1, device: int = 0):
+        lib = load()
+        h = _P()
+        check(lib.qs_state_create(num_qubits, num_local_qubits, rank_index, num_states, device,
+                                  ctypes.byref(h)))
+        self._h = h
+        self.num_qubits = num_qubits
+        self.num_local_qubits = num_local_qubits
+        self.rank_index = rank_index
+        self.num_states = num_states
+        self.device = device
+        self.amps_per_state = 1 << num_local_qubits
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise ValueError("state was destroyed")
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None:
+            load().qs_state_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- data movement --------------------------------------------------------
+    def upload(self, amps: np.ndarray, offset: int = 0) -> None:
+        a = np.ascontiguousarray(amps, dtype=np.complex128).ravel()
+        call("qs_state_upload", self.handle, dptr(a), offset, a.size)
+
+    def download(self, out: np.ndarray | None = None, offset: int = 0,
+                 count: int | None = None) -> np.ndarray:
+        total = self.amps_per_state * self.num_states
+        if count is None:
+            count = total - offset
+        if out is None:
+            out = np.empty(count, dtype=np.complex128)
+        call("qs_state_download", self.handle, dptr(out), offset, count)
+        return out
+
+    def synchronize(self) -> None:
+        call("qs_synchronize", self.handle)
+
+    def device_ptr(self) -> int:
+        p = _P()
+        call("qs_state_device_ptr", self.handle, ctypes.byref(p))
+        return p.value
+
+    def counters(self) -> tuple[int, int]:
+        msgs, amps = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        call("qs_counters", self.handle, ctypes.byref(msgs), ctypes.byref(amps))
+        return msgs.value, amps.value
+
+    # ---- kernels ----------------------------------------------------------------
+    def apply_program(self, gates: list[QsGate] | ctypes.Array, mats: np.ndarray,
+                      edges: np.ndarray | None = None, fuse: bool = True) -> int:
+        n = len(gates)
+        arr = gates if isinstance(gates, ctypes.Array) else (QsGate * n)(*gates)
+        mats = np.ascontiguousarray(mats, dtype=np.float64)
+        if edges is None:
+            e = np.zeros(2, dtype=np.int32)
+            ne = 0
+        else:
+            e = np.ascontiguousarray(edges, dtype=np.int32).reshape(-1)
+            ne = e.size // 2
+            if ne == 0:
+                e = np.zeros(2, dtype=np.int32)
+        call("qs_apply_program", self.handle, arr, n, dptr(mats), mats.size, iptr(e), ne,
+             1 if fuse else 0)
+        passes = ctypes.c_int32(0)
+        call("qs_last_program_passes", self.handle, ctypes.byref(passes))
+        return passes.value
+
+    def observable(self, kind: int, q: int = 0, edges: np.ndarray | None = None) -> np.ndarray:
+        out = np.empty(self.num_states, dtype=np.float64)
+        e = np.zeros(2, dtype=np.int32) if edges is None else \
+            np.ascontiguousarray(edges, dtype=np.int32).reshape(-1)
+        ne = 0 if edges is None else e.size // 2
+        if e.size == 0:
+            e = np.zeros(2, dtype=np.int32)
+        call("qs_observable", self.handle, kind, q, iptr(e), ne, dptr(out))
+        return out
+
+    def launch_log(self, enable: bool) -> None:
+        call("qs_launch_log", self.handle, 1 if enable else 0)
+
+    def read_launch_log(self, cap: int = 1 << 16) -> tuple[np.ndarray, np.ndarray]:
+        ms = (ctypes.c_float * cap)()
+        kinds = (ctypes.c_int32 * cap)()
+        count = ctypes.c_int32(0)
+        call("qs_launch_log_read", self.handle, ms, kinds, cap, ctypes.byref(count))
+        k = min(count.value, cap)
+        return np.frombuffer(ms, dtype=np.float32, count=k).copy(), \
+            np.frombuffer(kinds, dtype=np.int32, count=k).copy()
+
+    def event_record(self, slot: int) -> None:
+        call("qs_event_record", self.handle, slot)
+
+    def event_elapsed_ms(self, a: int, b: int) -> float:
+        ms = ctypes.c_float(0)
+        call("qs_event_elapsed_ms", self.handle, a, b, ctypes.byref(ms))
+        return float(ms.value)

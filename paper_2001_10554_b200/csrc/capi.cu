@@ -1,0 +1,928 @@
+// C ABI of libqsb200.so: state lifetime, the fusion planner, observables and
+// the global-qubit exchange (declarations and reference citations in
+// include/qsb200.h).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace qsb;
+
+namespace qsb {
+size_t tile_smem_bytes();
+}
+
+// ---------------------------------------------------------------------------
+// errors
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+    do {                                                                                  \
+        cudaError_t _e = (expr);                                                          \
+        if (_e != cudaSuccess)                                                            \
+            return fail(_e == cudaErrorMemoryAllocation ? QS_ERR_NOMEM : QS_ERR_CUDA,    \
+                        "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+    } while (0)
+
+#define CHECK_LAUNCH()                                                                    \
+    do {                                                                                  \
+        cudaError_t _e = cudaGetLastError();                                              \
+        if (_e != cudaSuccess)                                                            \
+            return fail(QS_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(_e), \
+                        __FILE__, __LINE__);                                              \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily so the library has no link-time dependency on a
+// particular libnccl (torch ships its own).
+typedef int ncclResult_t_;
+typedef void* ncclComm_t_;
+struct NcclId {
+    char internal[128];
+};
+enum { kNcclFloat64 = 8 };  // ncclDataType_t: ncclFloat64 == ncclDouble == 8
+
+struct NcclApi {
+    bool loaded = false;
+    void* handle = nullptr;
+    ncclResult_t_ (*GetUniqueId)(NcclId*) = nullptr;
+    ncclResult_t_ (*CommInitRank)(ncclComm_t_*, int, NcclId, int) = nullptr;
+    ncclResult_t_ (*CommDestroy)(ncclComm_t_) = nullptr;
+    ncclResult_t_ (*Send)(const void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+    ncclResult_t_ (*Recv)(void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+    ncclResult_t_ (*GroupStart)() = nullptr;
+    ncclResult_t_ (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t_) = nullptr;
+};
+NcclApi g_nccl;
+
+int nccl_load() {
+    if (g_nccl.loaded) return QS_OK;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+        g_nccl.handle = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+        if (g_nccl.handle) break;
+    }
+    if (!g_nccl.handle) return fail(QS_ERR_COMM, "cannot dlopen libnccl.so.2: %s", dlerror());
+#define NCCL_SYM(field, name)                                                          \
+    g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(g_nccl.handle, name)); \
+    if (!g_nccl.field) return fail(QS_ERR_COMM, "libnccl lacks %s", name);
+    NCCL_SYM(GetUniqueId, "ncclGetUniqueId");
+    NCCL_SYM(CommInitRank, "ncclCommInitRank");
+    NCCL_SYM(CommDestroy, "ncclCommDestroy");
+    NCCL_SYM(Send, "ncclSend");
+    NCCL_SYM(Recv, "ncclRecv");
+    NCCL_SYM(GroupStart, "ncclGroupStart");
+    NCCL_SYM(GroupEnd, "ncclGroupEnd");
+    NCCL_SYM(GetErrorString, "ncclGetErrorString");
+#undef NCCL_SYM
+    g_nccl.loaded = true;
+    return QS_OK;
+}
+
+#define NCCL_TRY(expr)                                                                     \
+    do {                                                                                   \
+        ncclResult_t_ _r = (expr);                                                         \
+        if (_r != 0)                                                                       \
+            return fail(QS_ERR_COMM, "%s: %s", #expr, g_nccl.GetErrorString(_r));          \
+    } while (0)
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// state
+struct LaunchRec {
+    int32_t kind;
+    cudaEvent_t start, stop;
+};
+
+struct qs_state {
+    int n = 0, m = 0, rank = 0, num_states = 1, device = 0;
+    uint64_t amps_per_state = 0;
+    double2* psi = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t comm_stream = nullptr;
+    // device scratch
+    double* d_mats = nullptr;
+    size_t mats_cap = 0;  // doubles
+    DevGate* d_gates = nullptr;
+    size_t gates_cap = 0;
+    double* d_scratch = nullptr;
+    size_t scratch_cap = 0;
+    double* d_u = nullptr;  // 8 doubles for exchange gates
+    double* h_out = nullptr;  // pinned observable results
+    size_t h_out_cap = 0;
+    // NCCL exchange staging
+    ncclComm_t_ comm = nullptr;
+    double2* d_stage[2] = {nullptr, nullptr};
+    size_t stage_cap = 0;  // amplitudes per buffer
+    // accounting (TransportCounters analogue)
+    uint64_t messages = 0, amplitudes = 0;
+    int32_t last_passes = 0;
+    // timing
+    cudaEvent_t ev[8] = {};
+    bool launch_log = false;
+    std::vector<LaunchRec> recs;
+};
+
+namespace {
+
+int ensure_device(qs_state* st) {
+    CUDA_TRY(cudaSetDevice(st->device));
+    return QS_OK;
+}
+
+template <typename T>
+int grow(T** p, size_t* cap, size_t need) {
+    if (*cap >= need) return QS_OK;
+    if (*p) {
+        cudaDeviceSynchronize();  // queued kernels may still read the old buffer
+        cudaError_t e = cudaFree(*p);
+        if (e != cudaSuccess) return fail(QS_ERR_CUDA, "cudaFree: %s", cudaGetErrorString(e));
+    }
+    size_t n = std::max(need, *cap * 2);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        *cap = 0;
+        return fail(QS_ERR_NOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
+    }
+    *cap = n;
+    return QS_OK;
+}
+
+int build_cut_terms(const int32_t* edges, int32_t num_edges, int n, CutTerms* ct) {
+    memset(ct, 0, sizeof(*ct));
+    if (num_edges < 0) return fail(QS_ERR_VALUE, "negative edge count");
+    if (num_edges > 0 && !edges) return fail(QS_ERR_VALUE, "edges is NULL");
+    for (int e = 0; e < num_edges; ++e) {
+        int u = edges[2 * e], v = edges[2 * e + 1];
+        if (u == v) return fail(QS_ERR_VALUE, "self-loop at vertex %d", u);
+        if (u < 0 || v < 0 || u >= n || v >= n || u > 63 || v > 63)
+            return fail(QS_ERR_VALUE, "edge (%d, %d) endpoint out of range for %d qubits", u, v, n);
+        int lo = std::min(u, v), d = std::abs(u - v);
+        int k = 0;
+        while (k < ct->count && ct->shift[k] != d) ++k;
+        if (k == ct->count) {
+            if (ct->count == kMaxCutTerms) return fail(QS_ERR_VALUE, "too many edge distances");
+            ct->shift[k] = d;
+            ct->mask[k] = 0;
+            ct->count++;
+        }
+        if (ct->mask[k] & (uint64_t(1) << lo))
+            return fail(QS_ERR_VALUE, "duplicate edge (%d, %d)", u, v);
+        ct->mask[k] |= uint64_t(1) << lo;
+    }
+    return QS_OK;
+}
+
+// launch bracketing for the optional per-launch timing log
+struct LaunchScope {
+    qs_state* st;
+    LaunchRec rec{};
+    LaunchScope(qs_state* s, int kind) : st(s) {
+        if (!st->launch_log) return;
+        rec.kind = kind;
+        cudaEventCreate(&rec.start);
+        cudaEventCreate(&rec.stop);
+        cudaEventRecord(rec.start, st->stream);
+    }
+    ~LaunchScope() {
+        if (!st->launch_log) return;
+        cudaEventRecord(rec.stop, st->stream);
+        st->recs.push_back(rec);
+    }
+};
+
+enum { kLaunchGate1q = 1, kLaunchControlled = 2, kLaunchPhase = 3, kLaunchTile = 4,
+       kLaunchExchange = 5, kLaunchReduce = 6 };
+
+bool is_diag_one(const double* e) {
+    return e[0] == 1.0 && e[1] == 0.0 && e[2] == 0.0 && e[3] == 0.0 && e[4] == 0.0 && e[5] == 0.0;
+}
+
+// ---- the fusion planner ----------------------------------------------------
+struct PlannedPass {
+    int first, count;  // range in the program
+};
+
+int launch_single(qs_state* st, const qs_gate& g, const CutTerms& ct, const double* mats_host) {
+    const int ns = st->num_states;
+    if (g.kind == QS_KIND_1Q) {
+        LaunchScope ls(st, kLaunchGate1q);
+        launch_gate1q(st->psi, st->m, ns, g.target, st->d_mats, g.offset, g.stride, st->stream);
+    } else if (g.kind == QS_KIND_CTRL) {
+        bool diag = true;
+        for (int s = 0; s < ns && diag; ++s) diag = is_diag_one(mats_host + g.offset + s * g.stride);
+        LaunchScope ls(st, kLaunchControlled);
+        launch_controlled(st->psi, st->m, ns, g.control, g.target, st->d_mats, g.offset, g.stride,
+                          diag, st->stream);
+    } else {
+        LaunchScope ls(st, kLaunchPhase);
+        launch_cut_phase(st->psi, st->m, ns, uint64_t(st->rank) << st->m, ct, st->d_mats, g.offset,
+                         g.stride, st->stream);
+    }
+    CHECK_LAUNCH();
+    return QS_OK;
+}
+
+
+
+// Build the TilePass + device gate list for program[first, first+count).
+int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const CutTerms& ct,
+                std::vector<DevGate>& dev_gates_host) {
+    // tile bits: the targets, plus qubits 0..2 for 128-byte rows, filled upward
+    uint64_t need = 0x7;
+    for (int i = 0; i < count; ++i)
+        if (prog[first + i].kind != QS_KIND_CUTPHASE) need |= uint64_t(1) << prog[first + i].target;
+    for (int b = 0; __builtin_popcountll(need) < kTileLog2 && b < st->m; ++b) need |= uint64_t(1) << b;
+    TilePass P;
+    memset(&P, 0, sizeof(P));
+    P.m = st->m;
+    int k = 0;
+    for (int b = 0; b < st->m; ++b)
+        if (need & (uint64_t(1) << b)) P.tile_bits[k++] = b;
+    P.low_run = 0;
+    while (P.low_run < kTileLog2 && P.tile_bits[P.low_run] == P.low_run) ++P.low_run;
+    P.tiles_per_state = uint64_t(1) << (st->m - kTileLog2);
+    P.num_tiles = P.tiles_per_state * uint64_t(st->num_states);
+    P.rank_offset = uint64_t(st->rank) << st->m;
+    auto pos_of = [&](int qubit) {
+        for (int p = 0; p < kTileLog2; ++p)
+            if (P.tile_bits[p] == qubit) return p;
+        return -1;
+    };
+    // rounds: consecutive gates whose targets fit in kRegLog2 register positions
+    dev_gates_host.clear();
+    std::vector<int> round_pos;
+    int r = -1;
+    auto close_round = [&]() {
+        if (r < 0) return;
+        Round& R = P.rounds[r];
+        // pad with the highest unused positions so the lanes keep the low positions
+        uint32_t used = 0;
+        for (int p : round_pos) used |= 1u << p;
+        for (int p = kTileLog2 - 1; (int)round_pos.size() < kRegLog2 && p >= 0; --p)
+            if (!(used & (1u << p))) round_pos.push_back(p), used |= 1u << p;
+        R.npos = kRegLog2;
+        for (int j = 0; j < kRegLog2; ++j) R.pos[j] = round_pos[j];
+    };
+    std::vector<int> gate_round(count);
+    for (int i = 0; i < count; ++i) {
+        const qs_gate& g = prog[first + i];
+        int p = g.kind == QS_KIND_CUTPHASE ? -1 : pos_of(g.target);
+        bool fits = r >= 0;
+        if (fits && p >= 0 &&
+            std::find(round_pos.begin(), round_pos.end(), p) == round_pos.end() &&
+            (int)round_pos.size() >= kRegLog2)
+            fits = false;
+        if (!fits) {
+            close_round();
+            ++r;
+            if (r >= kMaxRounds) return fail(QS_ERR_VALUE, "planner: too many rounds");
+            round_pos.clear();
+            P.rounds[r].first_gate = i;
+            P.rounds[r].num_gates = 0;
+        }
+        if (p >= 0 && std::find(round_pos.begin(), round_pos.end(), p) == round_pos.end())
+            round_pos.push_back(p);
+        P.rounds[r].num_gates++;
+        gate_round[i] = r;
+    }
+    close_round();
+    P.num_rounds = r + 1;
+    for (int i = 0; i < count; ++i) {
+        const qs_gate& g = prog[first + i];
+        DevGate d;
+        d.kind = g.kind;
+        d.offset = g.offset;
+        d.stride = g.stride;
+        d.pad = 0;
+        d.tpos = 0;
+        d.control = -1;
+        if (g.kind != QS_KIND_CUTPHASE) {
+            const Round& R = P.rounds[gate_round[i]];
+            int p = pos_of(g.target);
+            for (int j = 0; j < kRegLog2; ++j)
+                if (R.pos[j] == p) d.tpos = j;
+            if (g.kind == QS_KIND_CTRL) {
+                int pc = pos_of(g.control);
+                if (pc < 0) {
+                    d.control = (3 << 8) | g.control;
+                } else {
+                    int jc = -1;
+                    for (int j = 0; j < kRegLog2; ++j)
+                        if (R.pos[j] == pc) jc = j;
+                    d.control = jc >= 0 ? ((1 << 8) | jc) : ((2 << 8) | pc);
+                }
+            }
+        }
+        dev_gates_host.push_back(d);
+    }
+    int rc = grow(&st->d_gates, &st->gates_cap, dev_gates_host.size());
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(st->d_gates, dev_gates_host.data(), sizeof(DevGate) * count,
+                             cudaMemcpyHostToDevice, st->stream));
+    {
+        LaunchScope ls(st, kLaunchTile);
+        launch_tile_pass(st->psi, st->num_states, P, st->d_gates, st->d_mats, ct, st->stream);
+    }
+    CHECK_LAUNCH();
+    return QS_OK;
+}
+
+int validate_gate(const qs_state* st, const qs_gate& g, uint64_t mats_len, int num_edges) {
+    const int n = st->n, m = st->m;
+    uint64_t entry;
+    if (g.kind == QS_KIND_1Q || g.kind == QS_KIND_CTRL) {
+        if (g.target < 0 || g.target >= n)
+            return fail(QS_ERR_VALUE, "qubit %d out of range for n=%d", g.target, n);
+        if (g.target >= m)
+            return fail(QS_ERR_LOCALITY,
+                        "qubit %d is global for m=%d; route through the distribution module",
+                        g.target, m);
+        if (g.kind == QS_KIND_CTRL) {
+            if (g.control == g.target) return fail(QS_ERR_VALUE, "control and target must differ");
+            if (g.control < 0 || g.control >= n)
+                return fail(QS_ERR_VALUE, "qubit %d out of range for n=%d", g.control, n);
+            if (g.control >= m)
+                return fail(QS_ERR_LOCALITY,
+                            "both qubits must be local for the local controlled kernel");
+        }
+        entry = 8;
+    } else if (g.kind == QS_KIND_CUTPHASE) {
+        entry = 2 * uint64_t(num_edges + 1);
+    } else {
+        return fail(QS_ERR_VALUE, "unknown gate kind %d", g.kind);
+    }
+    uint64_t last = g.offset + uint64_t(st->num_states - 1) * g.stride + entry;
+    if (last > mats_len)
+        return fail(QS_ERR_VALUE, "gate table entry [%llu, %llu) beyond %llu doubles",
+                    (unsigned long long)g.offset, (unsigned long long)last,
+                    (unsigned long long)mats_len);
+    return QS_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int qs_abi_version(void) { return QSB200_ABI_VERSION; }
+
+const char* qs_last_error(void) { return g_last_error.c_str(); }
+
+int qs_device_count(int32_t* out) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        *out = 0;
+        return fail(QS_ERR_CUDA, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+    }
+    *out = n;
+    return QS_OK;
+}
+
+int qs_counters(const qs_state* st, uint64_t* messages, uint64_t* amplitudes) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    *messages = st->messages;
+    *amplitudes = st->amplitudes;
+    return QS_OK;
+}
+
+int qs_state_create(int32_t num_qubits, int32_t num_local_qubits, int32_t rank_index,
+                    int32_t num_states, int32_t device, qs_state** out) {
+    *out = nullptr;
+    const int n = num_qubits, m = num_local_qubits;
+    if (!(0 < m && m <= n))
+        return fail(QS_ERR_VALUE, "need 0 < num_local_qubits <= num_qubits, got m=%d, n=%d", m, n);
+    if (n > 62) return fail(QS_ERR_VALUE, "at most 62 qubits");
+    if (!(0 <= rank_index && (uint64_t)rank_index < (uint64_t(1) << (n - m))))
+        return fail(QS_ERR_VALUE, "rank_index %d out of range for %d rank bits", rank_index, n - m);
+    if (num_states < 1) return fail(QS_ERR_VALUE, "need at least one state");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(QS_ERR_CUDA, "no CUDA device (%s); the B200 core has no CPU fallback",
+                    cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(QS_ERR_VALUE, "device %d of %d", device, ndev);
+    qs_state* st = new (std::nothrow) qs_state();
+    if (!st) return fail(QS_ERR_NOMEM, "host allocation");
+    st->n = n;
+    st->m = m;
+    st->rank = rank_index;
+    st->num_states = num_states;
+    st->device = device;
+    st->amps_per_state = uint64_t(1) << m;
+    int rc = QS_OK;
+    do {
+        if ((e = cudaSetDevice(device)) != cudaSuccess) break;
+        if ((e = cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking)) != cudaSuccess) break;
+        if ((e = cudaStreamCreateWithFlags(&st->comm_stream, cudaStreamNonBlocking)) != cudaSuccess)
+            break;
+        size_t bytes = sizeof(double2) * st->amps_per_state * size_t(num_states);
+        if ((e = cudaMalloc(&st->psi, bytes)) != cudaSuccess) break;
+        if ((e = cudaMalloc(&st->d_u, 8 * sizeof(double))) != cudaSuccess) break;
+        for (auto& ev : st->ev)
+            if ((e = cudaEventCreate(&ev)) != cudaSuccess) break;
+        if (e != cudaSuccess) break;
+        if ((e = cudaMemsetAsync(st->psi, 0, bytes, st->stream)) != cudaSuccess) break;
+    } while (0);
+    if (e != cudaSuccess) {
+        rc = fail(e == cudaErrorMemoryAllocation ? QS_ERR_NOMEM : QS_ERR_CUDA,
+                  "qs_state_create(n=%d, m=%d, states=%d): %s", n, m, num_states,
+                  cudaGetErrorString(e));
+        qs_state_destroy(st);
+        return rc;
+    }
+    *out = st;
+    return QS_OK;
+}
+
+int qs_state_destroy(qs_state* st) {
+    if (!st) return QS_OK;
+    cudaSetDevice(st->device);
+    if (st->stream) cudaStreamSynchronize(st->stream);
+    if (st->comm && g_nccl.loaded) g_nccl.CommDestroy(st->comm);
+    for (auto& r : st->recs) cudaEventDestroy(r.start), cudaEventDestroy(r.stop);
+    for (auto& ev : st->ev)
+        if (ev) cudaEventDestroy(ev);
+    cudaFree(st->psi);
+    cudaFree(st->d_mats);
+    cudaFree(st->d_gates);
+    cudaFree(st->d_scratch);
+    cudaFree(st->d_u);
+    cudaFree(st->d_stage[0]);
+    cudaFree(st->d_stage[1]);
+    if (st->h_out) cudaFreeHost(st->h_out);
+    if (st->stream) cudaStreamDestroy(st->stream);
+    if (st->comm_stream) cudaStreamDestroy(st->comm_stream);
+    delete st;
+    return QS_OK;
+}
+
+int qs_state_info(const qs_state* st, int32_t* n, int32_t* m, int32_t* r, int32_t* ns,
+                  uint64_t* aps) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    *n = st->n;
+    *m = st->m;
+    *r = st->rank;
+    *ns = st->num_states;
+    *aps = st->amps_per_state;
+    return QS_OK;
+}
+
+int qs_state_device_ptr(const qs_state* st, void** out) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    *out = st->psi;
+    return QS_OK;
+}
+
+int qs_synchronize(qs_state* st) {
+    if (int rc = ensure_device(st)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QS_OK;
+}
+
+int qs_state_upload(qs_state* st, const double* host, uint64_t offset, uint64_t count) {
+    if (int rc = ensure_device(st)) return rc;
+    uint64_t total = st->amps_per_state * uint64_t(st->num_states);
+    if (offset > total || count > total - offset)
+        return fail(QS_ERR_VALUE, "upload range [%llu, +%llu) beyond %llu amplitudes",
+                    (unsigned long long)offset, (unsigned long long)count,
+                    (unsigned long long)total);
+    if (count == 0) return QS_OK;
+    CUDA_TRY(cudaMemcpyAsync(st->psi + offset, host, count * sizeof(double2),
+                             cudaMemcpyHostToDevice, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QS_OK;
+}
+
+int qs_state_download(qs_state* st, double* host, uint64_t offset, uint64_t count) {
+    if (int rc = ensure_device(st)) return rc;
+    uint64_t total = st->amps_per_state * uint64_t(st->num_states);
+    if (offset > total || count > total - offset)
+        return fail(QS_ERR_VALUE, "download range beyond the state");
+    if (count == 0) return QS_OK;
+    CUDA_TRY(cudaMemcpyAsync(host, st->psi + offset, count * sizeof(double2),
+                             cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QS_OK;
+}
+
+int qs_init_zero(qs_state* st) {
+    if (int rc = ensure_device(st)) return rc;
+    CUDA_TRY(cudaMemsetAsync(st->psi, 0,
+                             sizeof(double2) * st->amps_per_state * size_t(st->num_states),
+                             st->stream));
+    return QS_OK;
+}
+
+int qs_init_basis(qs_state* st, uint64_t index) {
+    if (int rc = ensure_device(st)) return rc;
+    if (index >= (uint64_t(1) << st->n))
+        return fail(QS_ERR_VALUE, "basis index %llu out of range for %d qubits",
+                    (unsigned long long)index, st->n);
+    if (int rc = qs_init_zero(st)) return rc;
+    if ((index >> st->m) == uint64_t(st->rank)) {
+        const double2 one = make_double2(1.0, 0.0);
+        const uint64_t off = index & (st->amps_per_state - 1);
+        for (int s = 0; s < st->num_states; ++s)
+            CUDA_TRY(cudaMemcpyAsync(st->psi + uint64_t(s) * st->amps_per_state + off, &one,
+                                     sizeof(one), cudaMemcpyHostToDevice, st->stream));
+        CUDA_TRY(cudaStreamSynchronize(st->stream));
+    }
+    return QS_OK;
+}
+
+int qs_init_constant(qs_state* st, double re, double im) {
+    if (int rc = ensure_device(st)) return rc;
+    launch_fill(st->psi, st->amps_per_state * uint64_t(st->num_states), make_double2(re, im),
+                st->stream);
+    CHECK_LAUNCH();
+    return QS_OK;
+}
+
+int qs_init_gaussian(qs_state* st, uint64_t seed) {
+    if (int rc = ensure_device(st)) return rc;
+    launch_gaussian(st->psi, st->amps_per_state, st->num_states, uint64_t(st->rank) << st->m, seed,
+                    st->stream);
+    CHECK_LAUNCH();
+    return QS_OK;
+}
+
+int qs_scale(qs_state* st, double factor) {
+    if (int rc = ensure_device(st)) return rc;
+    launch_scale(st->psi, st->amps_per_state * uint64_t(st->num_states), factor, st->stream);
+    CHECK_LAUNCH();
+    return QS_OK;
+}
+
+int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const double* mats,
+                     uint64_t mats_len, const int32_t* edges, int32_t num_edges, int32_t fuse) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (count < 0) return fail(QS_ERR_VALUE, "negative gate count");
+    if (count == 0) {
+        st->last_passes = 0;
+        return QS_OK;
+    }
+    if (int rc = ensure_device(st)) return rc;
+    CutTerms ct;
+    bool has_phase = false;
+    for (int i = 0; i < count; ++i) has_phase |= gates[i].kind == QS_KIND_CUTPHASE;
+    if (has_phase) {
+        if (int rc = build_cut_terms(edges, num_edges, st->n, &ct)) return rc;
+    } else {
+        memset(&ct, 0, sizeof(ct));
+        num_edges = 0;
+    }
+    for (int i = 0; i < count; ++i)
+        if (int rc = validate_gate(st, gates[i], mats_len, num_edges)) return rc;
+    if (int rc = grow(&st->d_mats, &st->mats_cap, mats_len ? mats_len : 1)) return rc;
+    if (mats_len)
+        CUDA_TRY(cudaMemcpyAsync(st->d_mats, mats, mats_len * sizeof(double),
+                                 cudaMemcpyHostToDevice, st->stream));
+    // Greedy pass formation: extend while the union of targets plus the three
+    // coalescing qubits fits a 2^12-amplitude tile.
+    const bool tile_ok = fuse && st->m >= kTileLog2;
+    std::vector<DevGate> scratch;
+    int passes = 0;
+    int i = 0;
+    while (i < count) {
+        int j = i;
+        if (tile_ok) {
+            uint64_t need = 0x7;
+            while (j < count && j - i < kMaxPassGates) {
+                uint64_t nn = need;
+                if (gates[j].kind != QS_KIND_CUTPHASE) nn |= uint64_t(1) << gates[j].target;
+                if (__builtin_popcountll(nn) > kTileLog2) break;
+                need = nn;
+                ++j;
+            }
+        } else {
+            j = i + 1;
+        }
+        int rc;
+        if (j - i == 1)
+            rc = launch_single(st, gates[i], ct, mats);
+        else
+            rc = launch_tile(st, gates, i, j - i, ct, scratch);
+        if (rc == QS_ERR_VALUE && j - i > 1) {
+            // planner could not fit the rounds: split in half and retry
+            j = i + (j - i) / 2;
+            continue;
+        }
+        if (rc) return rc;
+        ++passes;
+        i = j;
+    }
+    st->last_passes = passes;
+    // no host sync: pageable H2D copies are staged before cudaMemcpyAsync returns,
+    // so the caller may reuse `mats`, and the device tables are stream-ordered.
+    return QS_OK;
+}
+
+int qs_last_program_passes(const qs_state* st, int32_t* passes) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    *passes = st->last_passes;
+    return QS_OK;
+}
+
+int qs_apply_1q(qs_state* st, int32_t q, const double* u, uint64_t u_stride) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (q < 0) return fail(QS_ERR_VALUE, "negative qubit index");
+    qs_gate g{QS_KIND_1Q, q, -1, 0, 0, u_stride};
+    uint64_t len = u_stride ? u_stride * uint64_t(st->num_states - 1) + 8 : 8;
+    return qs_apply_program(st, &g, 1, u, len, nullptr, 0, 0);
+}
+
+int qs_apply_controlled(qs_state* st, int32_t control, int32_t target, const double* u,
+                        uint64_t u_stride) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    qs_gate g{QS_KIND_CTRL, target, control, 0, 0, u_stride};
+    uint64_t len = u_stride ? u_stride * uint64_t(st->num_states - 1) + 8 : 8;
+    return qs_apply_program(st, &g, 1, u, len, nullptr, 0, 0);
+}
+
+int qs_apply_cut_phase(qs_state* st, const int32_t* edges, int32_t num_edges, const double* lut,
+                       uint64_t lut_stride) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    qs_gate g{QS_KIND_CUTPHASE, 0, -1, 0, 0, lut_stride};
+    uint64_t entry = 2 * uint64_t(num_edges + 1);
+    uint64_t len = lut_stride ? lut_stride * uint64_t(st->num_states - 1) + entry : entry;
+    return qs_apply_program(st, &g, 1, lut, len, edges, num_edges, 0);
+}
+
+int qs_observable(qs_state* st, int32_t kind, int32_t q, const int32_t* edges, int32_t num_edges,
+                  double* out) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (int rc = ensure_device(st)) return rc;
+    CutTerms ct;
+    memset(&ct, 0, sizeof(ct));
+    if (kind == QS_OBS_PROB || kind == QS_OBS_Z) {
+        if (q < 0 || q >= st->n) return fail(QS_ERR_VALUE, "qubit %d out of range", q);
+    } else if (kind == QS_OBS_MAXCUT) {
+        if (int rc = build_cut_terms(edges, num_edges, st->n, &ct)) return rc;
+    } else if (kind != QS_OBS_NORM) {
+        return fail(QS_ERR_VALUE, "unknown observable %d", kind);
+    }
+    int eff_kind = kind;
+    bool zero = false;
+    if (kind == QS_OBS_PROB && q >= st->m) {
+        // statevector.py:225-228: a global qubit selects the whole slice or nothing
+        if ((st->rank >> (q - st->m)) & 1)
+            eff_kind = QS_OBS_NORM;
+        else
+            zero = true;
+    }
+    if (zero) {
+        for (int s = 0; s < st->num_states; ++s) out[s] = 0.0;
+        return QS_OK;
+    }
+    size_t need = reduce_scratch_doubles(st->m, st->num_states) + st->num_states;
+    if (int rc = grow(&st->d_scratch, &st->scratch_cap, need)) return rc;
+    if (st->h_out_cap < size_t(st->num_states)) {
+        if (st->h_out) cudaFreeHost(st->h_out);
+        st->h_out = nullptr;
+        CUDA_TRY(cudaMallocHost(&st->h_out, sizeof(double) * st->num_states));
+        st->h_out_cap = st->num_states;
+    }
+    double* out_dev = st->d_scratch + reduce_scratch_doubles(st->m, st->num_states);
+    {
+        LaunchScope ls(st, kLaunchReduce);
+        launch_observable(st->psi, st->m, st->num_states, eff_kind, q, uint64_t(st->rank) << st->m,
+                          ct, st->d_scratch, out_dev, st->stream);
+    }
+    CHECK_LAUNCH();
+    CUDA_TRY(cudaMemcpyAsync(st->h_out, out_dev, sizeof(double) * st->num_states,
+                             cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    memcpy(out, st->h_out, sizeof(double) * st->num_states);
+    return QS_OK;
+}
+
+// ---- global-qubit path --------------------------------------------------------
+int qs_exchange_gate_peer(qs_state* st, void* peer_amps, int32_t is_lower, const double* u,
+                          int32_t control_local) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (!peer_amps) return fail(QS_ERR_VALUE, "null peer pointer");
+    if (st->num_states != 1) return fail(QS_ERR_VALUE, "exchange needs a single-state handle");
+    if (control_local >= st->m) return fail(QS_ERR_LOCALITY, "control %d is not local", control_local);
+    if (int rc = ensure_device(st)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(st->d_u, u, 8 * sizeof(double), cudaMemcpyHostToDevice, st->stream));
+    {
+        LaunchScope ls(st, kLaunchExchange);
+        launch_exchange_peer(st->psi, reinterpret_cast<double2*>(peer_amps), st->m, is_lower != 0,
+                             st->d_u, control_local, st->stream);
+    }
+    CHECK_LAUNCH();
+    // accounting in TransportCounters terms: one transfer out and one back,
+    // 2 * 2^(m-1) amplitudes leave this rank (reads by the partner + writes to it)
+    uint64_t moved = st->amps_per_state >> (control_local >= 0 ? 1 : 0);
+    st->messages += 2;
+    st->amplitudes += moved;
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QS_OK;
+}
+
+int qs_state_ipc_handle(const qs_state* st, unsigned char* handle64) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    CUDA_TRY(cudaSetDevice(st->device));
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, st->psi));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    memcpy(handle64, &h, 64);
+    return QS_OK;
+}
+
+int qs_peer_open(qs_state* st, const unsigned char* handle64, void** peer_amps) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    CUDA_TRY(cudaSetDevice(st->device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, 64);
+    CUDA_TRY(cudaIpcOpenMemHandle(peer_amps, h, cudaIpcMemLazyEnablePeerAccess));
+    return QS_OK;
+}
+
+int qs_peer_close(qs_state* st, void* peer_amps) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    CUDA_TRY(cudaSetDevice(st->device));
+    CUDA_TRY(cudaIpcCloseMemHandle(peer_amps));
+    return QS_OK;
+}
+
+int qs_nccl_unique_id(unsigned char* id128) {
+    if (int rc = nccl_load()) return rc;
+    NcclId id;
+    NCCL_TRY(g_nccl.GetUniqueId(&id));
+    memcpy(id128, id.internal, 128);
+    return QS_OK;
+}
+
+int qs_comm_init(qs_state* st, const unsigned char* id128, int32_t nranks, int32_t rank) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (int rc = nccl_load()) return rc;
+    if (int rc = ensure_device(st)) return rc;
+    NcclId id;
+    memcpy(id.internal, id128, 128);
+    NCCL_TRY(g_nccl.CommInitRank(&st->comm, nranks, id, rank));
+    return QS_OK;
+}
+
+int qs_comm_destroy(qs_state* st) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (st->comm && g_nccl.loaded) {
+        ensure_device(st);
+        NCCL_TRY(g_nccl.CommDestroy(st->comm));
+    }
+    st->comm = nullptr;
+    return QS_OK;
+}
+
+// The reference's three-step scheme (distribution.py:121-178) as a pipelined
+// NCCL exchange: chunk k goes out and comes back on the comm stream while the
+// compute stream updates chunk k-1; updated halves land in place in the
+// outbound half, which is what lets the pipeline run without a half-state
+// receive buffer.
+int qs_exchange_gate_nccl(qs_state* st, int32_t peer, int32_t is_lower, const double* u,
+                          int32_t control_local, uint64_t chunk) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (!st->comm) return fail(QS_ERR_COMM, "qs_comm_init was not called");
+    if (st->num_states != 1) return fail(QS_ERR_VALUE, "exchange needs a single-state handle");
+    if (chunk == 0) return fail(QS_ERR_VALUE, "chunk must be positive");
+    if (control_local >= st->m) return fail(QS_ERR_LOCALITY, "control %d is not local", control_local);
+    if (int rc = ensure_device(st)) return rc;
+    const uint64_t half = st->amps_per_state / 2;
+    const uint64_t c = std::min<uint64_t>(chunk, half);
+    if (int rc = grow(&st->d_stage[0], &st->stage_cap, c)) return rc;
+    if (st->stage_cap > 0 && st->d_stage[1] == nullptr) {
+        CUDA_TRY(cudaMalloc(&st->d_stage[1], st->stage_cap * sizeof(double2)));
+    }
+    CUDA_TRY(cudaMemcpyAsync(st->d_u, u, 8 * sizeof(double), cudaMemcpyHostToDevice, st->stream));
+    double2* mine = is_lower ? st->psi : st->psi + half;
+    double2* outbound = is_lower ? st->psi + half : st->psi;
+    const uint64_t mine_first = is_lower ? 0 : half;
+    const uint64_t nchunks = (half + c - 1) / c;
+    cudaEvent_t ev_in[2], ev_done[2], ev_start;
+    for (int k = 0; k < 2; ++k) {
+        CUDA_TRY(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev_start, st->stream));
+    CUDA_TRY(cudaStreamWaitEvent(st->comm_stream, ev_start, 0));
+    const size_t dbl = 2;  // doubles per amplitude
+    for (uint64_t k = 0; k <= nchunks; ++k) {
+        // comm: send chunk k out / receive partner's chunk k; return chunk k-1
+        if (k > 0) CUDA_TRY(cudaStreamWaitEvent(st->comm_stream, ev_done[(k - 1) & 1], 0));
+        NCCL_TRY(g_nccl.GroupStart());
+        if (k < nchunks) {
+            uint64_t len = std::min(c, half - k * c);
+            NCCL_TRY(g_nccl.Send(outbound + k * c, len * dbl, kNcclFloat64, peer, st->comm,
+                                 st->comm_stream));
+            NCCL_TRY(g_nccl.Recv(st->d_stage[k & 1], len * dbl, kNcclFloat64, peer, st->comm,
+                                 st->comm_stream));
+            st->messages += 1;
+            st->amplitudes += len;
+        }
+        if (k > 0) {
+            uint64_t len = std::min(c, half - (k - 1) * c);
+            NCCL_TRY(g_nccl.Send(st->d_stage[(k - 1) & 1], len * dbl, kNcclFloat64, peer, st->comm,
+                                 st->comm_stream));
+            NCCL_TRY(g_nccl.Recv(outbound + (k - 1) * c, len * dbl, kNcclFloat64, peer, st->comm,
+                                 st->comm_stream));
+            st->messages += 1;
+            st->amplitudes += len;
+        }
+        NCCL_TRY(g_nccl.GroupEnd());
+        if (k < nchunks) {
+            CUDA_TRY(cudaEventRecord(ev_in[k & 1], st->comm_stream));
+            // compute: pair update of chunk k (mine[k], partner's chunk in stage)
+            CUDA_TRY(cudaStreamWaitEvent(st->stream, ev_in[k & 1], 0));
+            uint64_t len = std::min(c, half - k * c);
+            double2* a = is_lower ? mine + k * c : st->d_stage[k & 1];
+            double2* b = is_lower ? st->d_stage[k & 1] : mine + k * c;
+            {
+                LaunchScope ls(st, kLaunchExchange);
+                launch_pair_update_halves(a, b, len, mine_first + k * c, st->d_u, control_local,
+                                          st->stream);
+            }
+            CHECK_LAUNCH();
+            CUDA_TRY(cudaEventRecord(ev_done[k & 1], st->stream));
+        }
+    }
+    cudaEvent_t ev_end;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev_end, st->comm_stream));
+    CUDA_TRY(cudaStreamWaitEvent(st->stream, ev_end, 0));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    for (int k = 0; k < 2; ++k) cudaEventDestroy(ev_in[k]), cudaEventDestroy(ev_done[k]);
+    cudaEventDestroy(ev_start);
+    cudaEventDestroy(ev_end);
+    return QS_OK;
+}
+
+// ---- timing ------------------------------------------------------------------
+int qs_event_record(qs_state* st, int32_t slot) {
+    if (!st || slot < 0 || slot >= 8) return fail(QS_ERR_VALUE, "bad event slot");
+    if (int rc = ensure_device(st)) return rc;
+    CUDA_TRY(cudaEventRecord(st->ev[slot], st->stream));
+    return QS_OK;
+}
+
+int qs_event_elapsed_ms(qs_state* st, int32_t a, int32_t b, float* ms) {
+    if (!st || a < 0 || a >= 8 || b < 0 || b >= 8) return fail(QS_ERR_VALUE, "bad event slot");
+    if (int rc = ensure_device(st)) return rc;
+    CUDA_TRY(cudaEventSynchronize(st->ev[b]));
+    CUDA_TRY(cudaEventElapsedTime(ms, st->ev[a], st->ev[b]));
+    return QS_OK;
+}
+
+int qs_launch_log(qs_state* st, int32_t enable) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    st->launch_log = enable != 0;
+    return QS_OK;
+}
+
+// Read (and clear) the per-launch log: kind codes 1 gate1q, 2 controlled,
+// 3 cut-phase, 4 tile pass, 5 exchange, 6 reduction.
+int qs_launch_log_read(qs_state* st, float* ms, int32_t* kinds, int32_t cap, int32_t* count) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (int rc = ensure_device(st)) return rc;
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    int k = 0;
+    for (auto& r : st->recs) {
+        if (k < cap) {
+            float t = 0;
+            cudaEventElapsedTime(&t, r.start, r.stop);
+            ms[k] = t;
+            kinds[k] = r.kind;
+        }
+        ++k;
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    st->recs.clear();
+    *count = k;
+    return QS_OK;
+}
+
+}  // extern "C"

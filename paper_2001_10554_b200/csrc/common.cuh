@@ -1,0 +1,122 @@
+// Shared declarations of the B200 state-vector core (libqsb200.so).
+//
+// Arithmetic contract: the reference evaluates
+// pair_update (statevector.py:144-150) with numpy complex128 ufuncs, which on
+// an FMA host compute x*y as (fma(xr,yr,-(xi*yi)), fma(xr,yi,xi*yr)) with the
+// LEFT operand as x, then plain IEEE adds.  Every kernel here spells that out
+// with __fma_rn/__dmul_rn/__dadd_rn so no contraction choice of the compiler
+// can change a bit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/qsb200.h"
+
+namespace qsb {
+
+// ---- numpy-exact complex arithmetic ----------------------------------------
+__device__ __forceinline__ double2 cmul(double2 x, double2 y) {
+    return make_double2(__fma_rn(x.x, y.x, -__dmul_rn(x.y, y.y)),
+                        __fma_rn(x.x, y.y, __dmul_rn(x.y, y.x)));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+    return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+}
+// (a, b) <- (u00 a + u01 b, u10 a + u11 b), statevector.py:150
+__device__ __forceinline__ void pair_update(double2& a, double2& b, const double2 u[4]) {
+    double2 na = cadd(cmul(u[0], a), cmul(u[1], b));
+    double2 nb = cadd(cmul(u[2], a), cmul(u[3], b));
+    a = na;
+    b = nb;
+}
+// |psi|^2 as the reference evaluates it: a.real*a.real + a.imag*a.imag
+// (separate ufuncs, no FMA; statevector.py:212)
+__device__ __forceinline__ double abs2(double2 a) {
+    return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
+}
+
+// insert a zero bit at position b
+__host__ __device__ __forceinline__ uint64_t insert0(uint64_t x, int b) {
+    uint64_t lowmask = (uint64_t(1) << b) - 1;
+    return (x & lowmask) | ((x & ~lowmask) << 1);
+}
+
+// cut(i) = sum over edges of bit_u(i) xor bit_v(i) (graphs.py:35-42), grouped by
+// vertex distance d = v-u: popc((i ^ (i >> d)) & mask_d).
+constexpr int kMaxCutTerms = 64;
+struct CutTerms {
+    int32_t count;
+    int32_t shift[kMaxCutTerms];
+    uint64_t mask[kMaxCutTerms];
+};
+__device__ __forceinline__ int cut_of(uint64_t i, const CutTerms& ct) {
+    int c = 0;
+    for (int k = 0; k < ct.count; ++k) c += __popcll((i ^ (i >> ct.shift[k])) & ct.mask[k]);
+    return c;
+}
+
+// ---- device-side gate descriptors --------------------------------------------
+struct DevGate {
+    int32_t kind;      // QS_KIND_*
+    int32_t tpos;      // target: tile position (tile kernel) or qubit (single-gate kernels)
+    int32_t control;   // control qubit (local index) or -1
+    int32_t pad;
+    uint64_t offset;   // doubles into the device matrix table
+    uint64_t stride;   // doubles per state
+};
+
+// Tile pass description for the fused kernel (lives in kernel params).
+constexpr int kTileLog2 = 12;          // 4096 amplitudes = 64 KiB of shared memory
+constexpr int kTileThreads = 256;      // 16 amplitudes per thread = 4 register qubits
+constexpr int kRegLog2 = kTileLog2 - 8;
+constexpr int kMaxRounds = 32;
+constexpr int kMaxPassGates = 128;
+
+struct Round {
+    int32_t first_gate;   // index into the pass's gate array
+    int32_t num_gates;
+    int32_t npos;         // number of tile positions held in registers (<= kRegLog2)
+    int32_t pos[kRegLog2];
+};
+
+struct TilePass {
+    int32_t m;                 // local qubits per state
+    int32_t num_rounds;
+    int32_t low_run;           // tile positions 0..low_run-1 are qubits 0..low_run-1
+    int32_t tile_bits[kTileLog2];  // ascending local qubit of each tile position
+    uint64_t tiles_per_state;  // 2^(m - kTileLog2)
+    uint64_t num_tiles;        // num_states * tiles_per_state
+    uint64_t rank_offset;      // rank_index << m (global index of local offset 0)
+    Round rounds[kMaxRounds];
+};
+
+// ---- launchers (gate_kernels.cu / reduce_kernels.cu / exchange.cu) ---------
+void launch_gate1q(double2* psi, int m, int num_states, int q, const double* mats,
+                   uint64_t offset, uint64_t stride, cudaStream_t s);
+void launch_controlled(double2* psi, int m, int num_states, int c, int t, const double* mats,
+                       uint64_t offset, uint64_t stride, bool diag_one, cudaStream_t s);
+void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
+                      const CutTerms& ct, const double* mats, uint64_t offset, uint64_t stride,
+                      cudaStream_t s);
+void launch_tile_pass(double2* psi, int num_states, const TilePass& pass, const DevGate* gates,
+                      const double* mats, const CutTerms& ct, cudaStream_t s);
+void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s);
+void launch_gaussian(double2* psi, uint64_t count_per_state, int num_states, uint64_t rank_offset,
+                     uint64_t seed, cudaStream_t s);
+void launch_scale(double2* psi, uint64_t count, double factor, cudaStream_t s);
+
+// Observables: per-state tree sums.  `scratch` must hold at least
+// reduce_scratch_doubles(m, num_states) doubles.
+uint64_t reduce_scratch_doubles(int m, int num_states);
+void launch_observable(const double2* psi, int m, int num_states, int kind, int q,
+                       uint64_t rank_offset, const CutTerms& ct, double* scratch, double* out_dev,
+                       cudaStream_t s);
+
+void launch_exchange_peer(double2* mine, double2* peer, int m, bool is_lower, const double* u_dev,
+                          int control_local, cudaStream_t s);
+void launch_pair_update_halves(double2* a, double2* b, uint64_t count, uint64_t first_offset,
+                               const double* u_dev, int control_local, cudaStream_t s);
+
+}  // namespace qsb

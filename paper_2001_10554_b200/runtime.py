@@ -1,0 +1,424 @@
+"""Circuit execution over the B200 core -- the caller side of the boundary
+(reference pkg/src/qpool/runtime.py: apply_gate 115-152, run_circuit
+155-162, run_circuit_pool 192-209, measure_* 212-227, simulate_circuit
+291-302).
+
+Differences by design, not in results:
+  * Gates are queued per device state and flushed as one program into
+    libqsb200, whose native planner fuses consecutive local gates into
+    shared-memory tile passes (one HBM read+write per pass).  Per-amplitude
+    arithmetic and order are unchanged, so the state is bit-identical to
+    gate-by-gate execution.  A global-qubit gate, an observable, or the
+    every-100-gates norm check (runtime.py:146-152) flushes the queue.
+  * Pool mode (pool.py / runtime.py:192-209) is one batched device state of
+    S independent partitions per GPU with per-state matrix/LUT tables: one
+    launch per fused pass for the whole pool instead of one circuit per rank
+    group.  Pools are split across GPUs by contiguous state blocks (no state
+    exchange).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from . import distribution as dist
+from . import gates as gates_mod
+from . import statevector as sv
+from .graphs import edge_array, phase_lut
+
+NORM_CHECK_INTERVAL = 100
+NORM_TOL = 1e-10
+
+
+class NormDriftError(RuntimeError):
+    """The running state stopped being normalized (runtime.py:40-41)."""
+
+
+# ---- gate queue -> qs_apply_program ------------------------------------------------
+class GateQueue:
+    """Pending gates of one device state, flushed as one fused program."""
+
+    def __init__(self, state: _native.DeviceState, fuse: bool = True):
+        self.state = state
+        self.fuse = fuse
+        self.gates: list = []
+        self.tables: list = []
+        self.size = 0  # doubles
+        self.edges: np.ndarray | None = None
+        self.passes_total = 0
+        self.gates_total = 0
+
+    def __len__(self) -> int:
+        return len(self.gates)
+
+    def _add(self, kind: int, target: int, control: int, table: np.ndarray, per_state: bool):
+        table = np.ascontiguousarray(table, dtype=np.float64).reshape(-1)
+        stride = table.size // self.state.num_states if per_state else 0
+        g = _native.QsGate(kind, target, control, 0, self.size, stride)
+        self.gates.append(g)
+        self.tables.append(table)
+        self.size += table.size
+
+    def one_qubit(self, q: int, u) -> None:
+        """u: (2,2) shared or (S,2,2) per state."""
+        u = np.asarray(u, dtype=np.complex128)
+        self._add(_native.QS_KIND_1Q, q, -1, u.view(np.float64), u.ndim == 3)
+
+    def controlled(self, c: int, t: int, u) -> None:
+        u = np.asarray(u, dtype=np.complex128)
+        self._add(_native.QS_KIND_CTRL, t, c, u.view(np.float64), u.ndim == 3)
+
+    def cut_phase(self, graph, gamma) -> None:
+        edges = edge_array(graph)
+        if self.edges is not None and not np.array_equal(self.edges, edges):
+            self.flush()
+        self.edges = edges
+        gam = np.asarray(gamma, dtype=np.float64)
+        if gam.ndim == 0:
+            lut = phase_lut(float(gam), len(edges))
+            self._add(_native.QS_KIND_CUTPHASE, 0, -1, lut.view(np.float64), False)
+        else:
+            luts = np.stack([phase_lut(float(g), len(edges)) for g in gam])
+            self._add(_native.QS_KIND_CUTPHASE, 0, -1, luts.view(np.float64), True)
+
+    def flush(self) -> int:
+        if not self.gates:
+            return 0
+        mats = np.concatenate(self.tables) if self.tables else np.zeros(1)
+        passes = self.state.apply_program(self.gates, mats, self.edges, self.fuse)
+        self.passes_total += passes
+        self.gates_total += len(self.gates)
+        self.gates, self.tables, self.size = [], [], 0
+        self.edges = None
+        return passes
+
+
+def _matrix_for(gate) -> np.ndarray:
+    kind = gate.kind
+    if kind in gates_mod.FIXED_GATES:
+        return gates_mod.FIXED_GATES[kind]
+    if kind in gates_mod.ROTATION_GATES:
+        return gates_mod.ROTATION_GATES[kind](_angle(gate))
+    if kind in ("custom", "cu"):
+        return gates_mod.gate_matrix(gate.matrix)
+    if kind == "cx":
+        return gates_mod.PAULI_X
+    if kind == "cz":
+        return gates_mod.PAULI_Z
+    if kind == "cphase":
+        return gates_mod.cphase(_angle(gate))
+    raise ValueError(f"no matrix for gate kind {kind!r}")
+
+
+def _angle(gate) -> float:
+    if isinstance(gate.param, str):
+        raise ValueError(f"gate {gate.kind} has unbound slot {gate.param}")
+    return float(gate.param)
+
+
+# ---- contexts ------------------------------------------------------------------------
+@dataclass
+class RankContext:
+    """What one rank (one GPU or one emulated rank) needs to run circuits."""
+
+    comm: dist.GroupComm
+    num_qubits: int
+    num_states: int = 1
+    device: int = 0
+    fuse: bool = True
+    norm_check_interval: int = NORM_CHECK_INTERVAL
+    topology: dist.RankTopology = field(init=False)
+    partition: sv.StatePartition | None = field(init=False, default=None)
+    pool: "PoolState | None" = field(init=False, default=None)
+    queue: GateQueue | None = field(init=False, default=None)
+    gates_applied: int = field(init=False, default=0)
+
+    def __post_init__(self) -> None:
+        size = self.comm.size if self.num_states == 1 else 1
+        self.topology = dist.RankTopology(size, self.num_qubits)
+        if self.num_states > 1 and self.comm.size > 1:
+            raise ValueError("pool contexts hold whole states; split pools with split_pool()")
+        if self.comm.rank < self.topology.effective_ranks:
+            if self.num_states == 1:
+                self.partition = sv.allocate_partition(
+                    self.num_qubits, self.topology.num_local_qubits, self.comm.rank,
+                    device=self.device)
+                sv.init_basis_state(self.partition, 0)
+                self.queue = GateQueue(self.partition.state, self.fuse)
+            else:
+                self.pool = PoolState(self.num_qubits, self.num_states, self.device, self.fuse)
+                self.queue = self.pool.queue
+        self.comm.attach(self.partition)
+
+    @property
+    def is_idle(self) -> bool:
+        return self.queue is None
+
+    @property
+    def state(self) -> _native.DeviceState:
+        return self.partition.state if self.partition is not None else self.pool.state
+
+    def flush(self) -> None:
+        if self.queue is not None:
+            if self.partition is not None:
+                self.partition.sync_in()
+            self.queue.flush()
+
+
+def make_context(comm: dist.GroupComm | None, num_qubits: int, num_states: int = 1,
+                 device: int = 0, fuse: bool = True) -> RankContext:
+    return RankContext(comm or dist.single_rank_comm(), num_qubits, num_states, device, fuse)
+
+
+def reset_state(ctx: RankContext, index: int = 0) -> None:
+    if ctx.is_idle:
+        return
+    ctx.queue.gates, ctx.queue.tables, ctx.queue.size, ctx.queue.edges = [], [], 0, None
+    if ctx.partition is not None:
+        sv.init_basis_state(ctx.partition, index)
+    else:
+        _native.call("qs_init_basis", ctx.pool.state.handle, index)
+    ctx.gates_applied = 0
+
+
+def apply_gate(ctx: RankContext, gate) -> None:
+    """Queue one gate; global-qubit gates flush and exchange (runtime.py:115-152)."""
+    if ctx.is_idle:
+        return
+    kind = gate.kind
+    topo = ctx.topology
+    q = ctx.queue
+    if kind == "diagcost":
+        q.cut_phase(gate.graph, _angle(gate))
+    elif kind in ("cx", "cz", "cphase", "cu"):
+        c, t = gate.qubits
+        u = _matrix_for(gate)
+        route = dist.route_controlled(ctx.comm.rank, topo, c, t)
+        if route[0] == "local_controlled":
+            q.controlled(c, t, u)
+        elif route[0] == "local_one_qubit":
+            q.one_qubit(t, u)
+        elif route[0] == "exchange":
+            ctx.flush()
+            dist.apply_controlled_gate(ctx.partition, topo, ctx.comm, c, t, u)
+    else:
+        qb = gate.qubits[0]
+        u = _matrix_for(gate)
+        route = dist.route_one_qubit(ctx.comm.rank, topo, qb)
+        if route[0] == "local":
+            q.one_qubit(qb, u)
+        else:
+            ctx.flush()
+            dist.apply_one_qubit_gate(ctx.partition, topo, ctx.comm, qb, u)
+    ctx.gates_applied += 1
+    if ctx.norm_check_interval and ctx.gates_applied % ctx.norm_check_interval == 0:
+        norm_sq = measure_norm_squared(ctx)
+        if abs(norm_sq - 1.0) >= NORM_TOL:
+            raise NormDriftError(f"norm^2 drifted to {norm_sq!r} after {ctx.gates_applied} gates")
+
+
+def run_circuit(ctx: RankContext, circuit, bindings: dict | None = None) -> None:
+    bound = circuit.bind(bindings) if bindings else circuit
+    bound.require_bound()
+    for gate in bound.gates:
+        apply_gate(ctx, gate)
+    ctx.flush()
+
+
+def _group_reduce(ctx: RankContext, partial: float) -> float:
+    return dist.group_reduce_sum(partial, ctx.topology, ctx.comm)
+
+
+def measure_norm_squared(ctx: RankContext):
+    if ctx.is_idle:
+        return 0.0
+    ctx.flush()
+    if ctx.pool is not None:
+        return ctx.pool.observable(_native.QS_OBS_NORM)
+    return _group_reduce(ctx, sv.norm_squared(ctx.partition))
+
+
+def measure_probability(ctx: RankContext, q: int):
+    if ctx.is_idle:
+        return 0.0
+    ctx.flush()
+    if ctx.pool is not None:
+        return ctx.pool.observable(_native.QS_OBS_PROB, q)
+    return _group_reduce(ctx, sv.get_probability(ctx.partition, q))
+
+
+def measure_z(ctx: RankContext, q: int):
+    if ctx.is_idle:
+        return 0.0
+    ctx.flush()
+    if ctx.pool is not None:
+        return ctx.pool.observable(_native.QS_OBS_Z, q)
+    return _group_reduce(ctx, sv.z_expectation(ctx.partition, q))
+
+
+def measure_maxcut(ctx: RankContext, graph):
+    if ctx.is_idle:
+        return 0.0
+    ctx.flush()
+    if ctx.pool is not None:
+        return ctx.pool.observable(_native.QS_OBS_MAXCUT, 0, edge_array(graph))
+    return _group_reduce(ctx, sv.maxcut_expectation(ctx.partition, graph))
+
+
+def gather_group_state(ctx: RankContext) -> np.ndarray | None:
+    """Full amplitude vector of the (single) state on rank 0 (runtime.py:239-258).
+    Threaded communicators gather through the fabric; TorchComm through
+    torch.distributed.gather_object."""
+    if ctx.is_idle and not isinstance(ctx.comm, dist.TorchComm):
+        return None
+    if not ctx.is_idle:
+        ctx.flush()
+    mine = ctx.state.download() if not ctx.is_idle else None
+    comm = ctx.comm
+    if comm.size == 1:
+        return mine
+    if isinstance(comm, dist.ThreadComm):
+        fab = comm.fabric
+        with fab._lock:
+            fab._gather.setdefault("state", {})[comm.rank] = mine
+        comm.allgather(0.0, ctx.topology.effective_ranks)
+        if comm.rank != 0:
+            return None
+        with fab._lock:
+            parts = [fab._gather["state"][r] for r in range(ctx.topology.effective_ranks)]
+        return np.concatenate(parts)
+    import torch.distributed as tdist
+
+    out = [None] * comm.size if comm.rank == 0 else None
+    tdist.gather_object(mine, out, dst=comm._global(0), group=comm.group)
+    if comm.rank != 0:
+        return None
+    return np.concatenate([p for p in out[: ctx.topology.effective_ranks]])
+
+
+# ---- pool mode -----------------------------------------------------------------------
+class PoolState:
+    """S independent n-qubit states, batched in one device allocation."""
+
+    def __init__(self, num_qubits: int, num_states: int, device: int = 0, fuse: bool = True):
+        self.num_qubits = num_qubits
+        self.num_states = num_states
+        self.state = _native.DeviceState(num_qubits, num_qubits, 0, num_states, device)
+        self.queue = GateQueue(self.state, fuse)
+        _native.call("qs_init_basis", self.state.handle, 0)
+
+    def observable(self, kind: int, q: int = 0, edges=None) -> np.ndarray:
+        self.queue.flush()
+        return self.state.observable(kind, q, edges)
+
+    def amplitudes(self) -> np.ndarray:
+        self.queue.flush()
+        return self.state.download().reshape(self.num_states, -1)
+
+
+def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None) -> None:
+    """Every pool state runs `circuit`; state s binds slot_tables[name][s]
+    (runtime.py:192-209).  Per-state matrices/LUTs go to the device as tables."""
+    if not slot_tables:
+        run_circuit(ctx, circuit)
+        return
+    if ctx.is_idle:
+        return
+    S = ctx.num_states
+    for name, vals in slot_tables.items():
+        if len(vals) != S:
+            raise ValueError(f"table for ${name} has {len(vals)} entries for {S} states")
+    tables = {k: np.asarray(v, dtype=np.float64) for k, v in slot_tables.items()}
+    q = ctx.queue
+    for gate in circuit.gates:
+        slot = gate.slot if isinstance(getattr(gate, "param", None), str) else None
+        if slot is None:
+            if ctx.pool is None:
+                apply_gate(ctx, gate)
+                continue
+            _queue_fixed(q, gate)
+            continue
+        if slot not in tables:
+            raise ValueError(f"gate {gate.kind} has unbound slot ${slot}")
+        vals = tables[slot]
+        if ctx.pool is None:
+            # single state: bind value 0 (run_circuit semantics)
+            from dataclasses import replace
+            apply_gate(ctx, replace(gate, param=float(vals[0])))
+            continue
+        if gate.kind == "diagcost":
+            q.cut_phase(gate.graph, vals)
+        elif gate.kind in gates_mod.ROTATION_GATES:
+            fn = gates_mod.ROTATION_GATES[gate.kind]
+            mats = np.stack([fn(float(v)) for v in vals])
+            q.one_qubit(gate.qubits[0], mats)
+        elif gate.kind == "cphase":
+            mats = np.stack([gates_mod.cphase(float(v)) for v in vals])
+            q.controlled(gate.qubits[0], gate.qubits[1], mats)
+        else:
+            raise ValueError(f"gate kind {gate.kind} takes no parameter")
+    q.flush()
+
+
+def _queue_fixed(q: GateQueue, gate) -> None:
+    if gate.kind == "diagcost":
+        q.cut_phase(gate.graph, _angle(gate))
+    elif gate.kind in ("cx", "cz", "cphase", "cu"):
+        q.controlled(gate.qubits[0], gate.qubits[1], _matrix_for(gate))
+    else:
+        q.one_qubit(gate.qubits[0], _matrix_for(gate))
+
+
+def split_pool(num_states: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block [first, first+count) of pool states owned by `rank`
+    (the contiguous-group rule of pool.build_pool, pool.py:118-128)."""
+    base, extra = divmod(num_states, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+# ---- SPMD driver and convenience entry -------------------------------------------------
+def run_spmd(world_size: int, fn, timeout: float = 30.0, exchange_mode: str = "peer") -> list:
+    """fn(comm) on one thread per rank (runtime.py:261-288)."""
+    import threading
+
+    fabric = dist.ThreadFabric(world_size, timeout=timeout, exchange_mode=exchange_mode)
+    if world_size == 1:
+        return [fn(fabric.endpoint(0))]
+    results: list = [None] * world_size
+    failures: list = []
+    lock = threading.Lock()
+
+    def worker(rank: int) -> None:
+        try:
+            results[rank] = fn(fabric.endpoint(rank))
+        except BaseException as exc:  # noqa: BLE001 - re-raised below
+            with lock:
+                failures.append((rank, exc))
+
+    threads = [threading.Thread(target=worker, args=(r,), daemon=True) for r in range(world_size)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if failures:
+        failures.sort(key=lambda p: p[0])
+        rank, exc = failures[0]
+        raise RuntimeError(f"rank {rank} failed: {exc!r}") from exc
+    return results
+
+
+def simulate_circuit(circuit, num_ranks: int = 1, bindings: dict | None = None,
+                     device: int = 0, fuse: bool = True, timeout: float = 30.0,
+                     exchange_mode: str = "peer") -> np.ndarray:
+    """Run a circuit over `num_ranks` emulated ranks and return the full state
+    (runtime.py:291-302).  All emulated ranks share `device`."""
+
+    def rank_fn(comm):
+        ctx = make_context(comm, circuit.num_qubits, 1, device, fuse)
+        run_circuit(ctx, circuit, bindings)
+        return gather_group_state(ctx)
+
+    return run_spmd(num_ranks, rank_fn, timeout=timeout, exchange_mode=exchange_mode)[0]
