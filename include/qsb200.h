@@ -124,6 +124,10 @@ int qs_apply_cut_phase(qs_state* st, const int32_t* edges, int32_t num_edges,
 int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count,
                      const double* mats, uint64_t mats_len,
                      const int32_t* edges, int32_t num_edges, int32_t fuse);
+/* Planner only, no device needed: first gate index of every pass the fused
+ * program would launch (starts[0..min(cap, *npasses))). */
+int qs_plan_program(int32_t num_local_qubits, const qs_gate* gates, int32_t count, int32_t fuse,
+                    int32_t* starts, int32_t cap, int32_t* npasses);
 /* Number of HBM passes the last qs_apply_program launched (planner output). */
 int qs_last_program_passes(const qs_state* st, int32_t* passes);
 
@@ -157,9 +161,15 @@ int qs_nccl_unique_id(unsigned char* id128);
 int qs_comm_init(qs_state* st, const unsigned char* id128, int32_t nranks, int32_t rank);
 int qs_comm_destroy(qs_state* st);
 
-/* ---- timing helper for the benchmark: events on the handle's stream ---- */
+/* ---- timing helpers for the benchmark: events on the handle's stream ---- */
 int qs_event_record(qs_state* st, int32_t slot);
 int qs_event_elapsed_ms(qs_state* st, int32_t slot_a, int32_t slot_b, float* ms);
+/* Per-launch log: with enable != 0 every kernel launch is bracketed by CUDA
+ * events; qs_launch_log_read returns (and clears) durations in ms and kind
+ * codes (1 gate1q, 2 controlled, 3 cut phase, 4 tile pass, 5 exchange,
+ * 6 reduction). */
+int qs_launch_log(qs_state* st, int32_t enable);
+int qs_launch_log_read(qs_state* st, float* ms, int32_t* kinds, int32_t cap, int32_t* count);
 
 #ifdef __cplusplus
 }

@@ -27,7 +27,7 @@ EXPORTS = (
     "qs_synchronize", "qs_state_upload", "qs_state_download",
     "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
     "qs_apply_1q", "qs_apply_controlled", "qs_apply_cut_phase", "qs_apply_program",
-    "qs_last_program_passes", "qs_observable",
+    "qs_plan_program", "qs_last_program_passes", "qs_observable",
     "qs_exchange_gate_peer", "qs_exchange_gate_nccl", "qs_state_ipc_handle", "qs_peer_open",
     "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
     "qs_event_record", "qs_event_elapsed_ms", "qs_launch_log", "qs_launch_log_read",
@@ -86,6 +86,7 @@ _SIGNATURES = {
     "qs_apply_controlled": ([_P, _I, _I, _DP, _U], ctypes.c_int),
     "qs_apply_cut_phase": ([_P, _IP, _I, _DP, _U], ctypes.c_int),
     "qs_apply_program": ([_P, ctypes.POINTER(QsGate), _I, _DP, _U, _IP, _I, _I], ctypes.c_int),
+    "qs_plan_program": ([_I, ctypes.POINTER(QsGate), _I, _I, _IP, _I, _IP], ctypes.c_int),
     "qs_last_program_passes": ([_P, _IP], ctypes.c_int),
     "qs_observable": ([_P, _I, _I, _IP, _I, _DP], ctypes.c_int),
     "qs_exchange_gate_peer": ([_P, _P, _I, _DP, _I], ctypes.c_int),
@@ -146,6 +147,17 @@ def device_count() -> int:
     n = ctypes.c_int32(0)
     rc = load().qs_device_count(ctypes.byref(n))
     return n.value if rc == QS_OK else 0
+
+
+def plan_program(num_local_qubits: int, gates, fuse: bool = True) -> list[int]:
+    """First gate index of every pass the native planner would launch (CPU only)."""
+    n = len(gates)
+    arr = gates if isinstance(gates, ctypes.Array) else (QsGate * max(n, 1))(*gates)
+    starts = (ctypes.c_int32 * max(n, 1))()
+    count = ctypes.c_int32(0)
+    call("qs_plan_program", num_local_qubits, arr, n, 1 if fuse else 0, starts, max(n, 1),
+         ctypes.byref(count))
+    return list(starts[:count.value])
 
 
 def dptr(a: np.ndarray):

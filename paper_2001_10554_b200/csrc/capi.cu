@@ -123,8 +123,8 @@ struct qs_state {
     // device scratch
     double* d_mats = nullptr;
     size_t mats_cap = 0;  // doubles
-    DevGate* d_gates = nullptr;
-    size_t gates_cap = 0;
+    TilePass* d_pass = nullptr;
+    size_t pass_cap = 0;
     double* d_scratch = nullptr;
     size_t scratch_cap = 0;
     double* d_u = nullptr;  // 8 doubles for exchange gates
@@ -246,15 +246,16 @@ int launch_single(qs_state* st, const qs_gate& g, const CutTerms& ct, const doub
 
 
 
-// Build the TilePass + device gate list for program[first, first+count).
+// Build the TilePass for program[first, first+count) and launch it.
 int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const CutTerms& ct,
-                std::vector<DevGate>& dev_gates_host) {
+                const double* mats_host) {
+    if (count > kMaxPassGates) return fail(QS_ERR_VALUE, "planner: pass too long");
     // tile bits: the targets, plus qubits 0..2 for 128-byte rows, filled upward
     uint64_t need = 0x7;
     for (int i = 0; i < count; ++i)
         if (prog[first + i].kind != QS_KIND_CUTPHASE) need |= uint64_t(1) << prog[first + i].target;
     for (int b = 0; __builtin_popcountll(need) < kTileLog2 && b < st->m; ++b) need |= uint64_t(1) << b;
-    TilePass P;
+    static thread_local TilePass P;
     memset(&P, 0, sizeof(P));
     P.m = st->m;
     int k = 0;
@@ -271,19 +272,37 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         return -1;
     };
     // rounds: consecutive gates whose targets fit in kRegLog2 register positions
-    dev_gates_host.clear();
     std::vector<int> round_pos;
+    std::vector<std::vector<int>> all_pos;
     int r = -1;
     auto close_round = [&]() {
         if (r < 0) return;
-        Round& R = P.rounds[r];
         // pad with the highest unused positions so the lanes keep the low positions
         uint32_t used = 0;
         for (int p : round_pos) used |= 1u << p;
         for (int p = kTileLog2 - 1; (int)round_pos.size() < kRegLog2 && p >= 0; --p)
             if (!(used & (1u << p))) round_pos.push_back(p), used |= 1u << p;
-        R.npos = kRegLog2;
-        for (int j = 0; j < kRegLog2; ++j) R.pos[j] = round_pos[j];
+        Round& R = P.rounds[r];
+        int nonround[kTileLog2 - kRegLog2], c = 0;
+        for (int p = 0; p < kTileLog2; ++p)
+            if (!(used & (1u << p))) nonround[c++] = p;
+        for (int v = 0; v < 16; ++v) {
+            int lo = 0, hi = 0, kk = 0;
+            for (int b = 0; b < 4; ++b) {
+                if ((v >> b) & 1) {
+                    lo |= 1 << nonround[b];
+                    hi |= 1 << nonround[4 + b];
+                    kk |= 1 << round_pos[b];
+                }
+            }
+            R.dlo[v] = uint16_t(lo);
+            R.dhi[v] = uint16_t(hi);
+            R.dk[v] = uint16_t(kk);
+            R.slo[v] = uint16_t(swz(lo));
+            R.shi[v] = uint16_t(swz(hi));
+            R.sk[v] = uint16_t(swz(kk));
+        }
+        all_pos.push_back(round_pos);
     };
     std::vector<int> gate_round(count);
     for (int i = 0; i < count; ++i) {
@@ -299,7 +318,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
             ++r;
             if (r >= kMaxRounds) return fail(QS_ERR_VALUE, "planner: too many rounds");
             round_pos.clear();
-            P.rounds[r].first_gate = i;
+            P.rounds[r].first_gate = int16_t(i);
             P.rounds[r].num_gates = 0;
         }
         if (p >= 0 && std::find(round_pos.begin(), round_pos.end(), p) == round_pos.end())
@@ -311,42 +330,90 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     P.num_rounds = r + 1;
     for (int i = 0; i < count; ++i) {
         const qs_gate& g = prog[first + i];
-        DevGate d;
+        TileGate& d = P.gates[i];
         d.kind = g.kind;
         d.offset = g.offset;
         d.stride = g.stride;
-        d.pad = 0;
-        d.tpos = 0;
-        d.control = -1;
-        if (g.kind != QS_KIND_CUTPHASE) {
-            const Round& R = P.rounds[gate_round[i]];
-            int p = pos_of(g.target);
-            for (int j = 0; j < kRegLog2; ++j)
-                if (R.pos[j] == p) d.tpos = j;
-            if (g.kind == QS_KIND_CTRL) {
-                int pc = pos_of(g.control);
-                if (pc < 0) {
-                    d.control = (3 << 8) | g.control;
-                } else {
-                    int jc = -1;
-                    for (int j = 0; j < kRegLog2; ++j)
-                        if (R.pos[j] == pc) jc = j;
-                    d.control = jc >= 0 ? ((1 << 8) | jc) : ((2 << 8) | pc);
-                }
+        d.j = 0;
+        d.ctype = 0;
+        d.cval = 0;
+        if (g.kind == QS_KIND_CUTPHASE) continue;
+        if (g.stride == 0) memcpy(d.u, mats_host + g.offset, 8 * sizeof(double));
+        const std::vector<int>& rp = all_pos[gate_round[i]];
+        int p = pos_of(g.target);
+        for (int j = 0; j < kRegLog2; ++j)
+            if (rp[j] == p) d.j = j;
+        if (g.kind == QS_KIND_CTRL) {
+            int pc = pos_of(g.control);
+            if (pc < 0) {
+                d.ctype = 3;
+                d.cval = g.control;
+            } else {
+                int jc = -1;
+                for (int j = 0; j < kRegLog2; ++j)
+                    if (rp[j] == pc) jc = j;
+                d.ctype = jc >= 0 ? 1 : 2;
+                d.cval = jc >= 0 ? jc : pc;
             }
         }
-        dev_gates_host.push_back(d);
     }
-    int rc = grow(&st->d_gates, &st->gates_cap, dev_gates_host.size());
-    if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(st->d_gates, dev_gates_host.data(), sizeof(DevGate) * count,
-                             cudaMemcpyHostToDevice, st->stream));
+    if (int rc = grow(&st->d_pass, &st->pass_cap, 1)) return rc;
+    CUDA_TRY(cudaMemcpyAsync(st->d_pass, &P, sizeof(P), cudaMemcpyHostToDevice, st->stream));
     {
         LaunchScope ls(st, kLaunchTile);
-        launch_tile_pass(st->psi, st->num_states, P, st->d_gates, st->d_mats, ct, st->stream);
+        launch_tile_pass(st->psi, P, st->d_pass, st->d_mats, ct, st->stream);
     }
     CHECK_LAUNCH();
     return QS_OK;
+}
+
+// Greedy pass formation (the native fusion planner).  A pass grows while
+//  * the union of its target qubits plus qubits 0..2 (128-byte rows) fits the
+//    2^kTileLog2-amplitude tile, and
+//  * its register rounds (consecutive gates touching <= kRegLog2 distinct
+//    targets) stay within kMaxRounds.
+// Phase gates need no tile bit.  Single-gate passes use the streaming kernels.
+struct PassPlan {
+    int first, count;
+};
+
+std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool fuse) {
+    std::vector<PassPlan> out;
+    const bool tile_ok = fuse && m >= kTileLog2;
+    int i = 0;
+    while (i < count) {
+        int j = i + 1;
+        if (tile_ok) {
+            uint64_t need = 0x7;
+            if (gates[i].kind != QS_KIND_CUTPHASE) need |= uint64_t(1) << gates[i].target;
+            uint64_t round_set = gates[i].kind != QS_KIND_CUTPHASE ? (uint64_t(1) << gates[i].target) : 0;
+            int rounds = 1;
+            while (j < count && j - i < kMaxPassGates) {
+                const qs_gate& g = gates[j];
+                uint64_t nn = need, rs = round_set;
+                int nr = rounds;
+                if (g.kind != QS_KIND_CUTPHASE) {
+                    uint64_t b = uint64_t(1) << g.target;
+                    nn |= b;
+                    if (!(rs & b)) {
+                        if (__builtin_popcountll(rs) >= kRegLog2) {
+                            rs = 0;
+                            ++nr;
+                        }
+                        rs |= b;
+                    }
+                }
+                if (__builtin_popcountll(nn) > kTileLog2 || nr > kMaxRounds) break;
+                need = nn;
+                round_set = rs;
+                rounds = nr;
+                ++j;
+            }
+        }
+        out.push_back({i, j - i});
+        i = j;
+    }
+    return out;
 }
 
 int validate_gate(const qs_state* st, const qs_gate& g, uint64_t mats_len, int num_edges) {
@@ -467,7 +534,7 @@ int qs_state_destroy(qs_state* st) {
         if (ev) cudaEventDestroy(ev);
     cudaFree(st->psi);
     cudaFree(st->d_mats);
-    cudaFree(st->d_gates);
+    cudaFree(st->d_pass);
     cudaFree(st->d_scratch);
     cudaFree(st->d_u);
     cudaFree(st->d_stage[0]);
@@ -600,43 +667,32 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
     if (mats_len)
         CUDA_TRY(cudaMemcpyAsync(st->d_mats, mats, mats_len * sizeof(double),
                                  cudaMemcpyHostToDevice, st->stream));
-    // Greedy pass formation: extend while the union of targets plus the three
-    // coalescing qubits fits a 2^12-amplitude tile.
-    const bool tile_ok = fuse && st->m >= kTileLog2;
-    std::vector<DevGate> scratch;
+    std::vector<PassPlan> plan = plan_passes(gates, count, st->m, fuse != 0);
     int passes = 0;
-    int i = 0;
-    while (i < count) {
-        int j = i;
-        if (tile_ok) {
-            uint64_t need = 0x7;
-            while (j < count && j - i < kMaxPassGates) {
-                uint64_t nn = need;
-                if (gates[j].kind != QS_KIND_CUTPHASE) nn |= uint64_t(1) << gates[j].target;
-                if (__builtin_popcountll(nn) > kTileLog2) break;
-                need = nn;
-                ++j;
-            }
-        } else {
-            j = i + 1;
-        }
-        int rc;
-        if (j - i == 1)
-            rc = launch_single(st, gates[i], ct, mats);
-        else
-            rc = launch_tile(st, gates, i, j - i, ct, scratch);
-        if (rc == QS_ERR_VALUE && j - i > 1) {
-            // planner could not fit the rounds: split in half and retry
-            j = i + (j - i) / 2;
-            continue;
-        }
+    for (const PassPlan& pp : plan) {
+        int rc = pp.count == 1 ? launch_single(st, gates[pp.first], ct, mats)
+                               : launch_tile(st, gates, pp.first, pp.count, ct, mats);
         if (rc) return rc;
         ++passes;
-        i = j;
     }
     st->last_passes = passes;
     // no host sync: pageable H2D copies are staged before cudaMemcpyAsync returns,
     // so the caller may reuse `mats`, and the device tables are stream-ordered.
+    return QS_OK;
+}
+
+// Planning only (no device needed): writes the first gate index of every
+// pass into starts[] (up to cap) and the pass count into *npasses.
+int qs_plan_program(int32_t num_local_qubits, const qs_gate* gates, int32_t count, int32_t fuse,
+                    int32_t* starts, int32_t cap, int32_t* npasses) {
+    if (count < 0 || num_local_qubits < 1) return fail(QS_ERR_VALUE, "bad plan arguments");
+    for (int i = 0; i < count; ++i)
+        if (gates[i].kind != QS_KIND_CUTPHASE &&
+            (gates[i].target < 0 || gates[i].target >= num_local_qubits))
+            return fail(QS_ERR_VALUE, "target %d outside the local qubits", gates[i].target);
+    std::vector<PassPlan> plan = plan_passes(gates, count, num_local_qubits, fuse != 0);
+    for (size_t k = 0; k < plan.size() && (int)k < cap; ++k) starts[k] = plan[k].first;
+    *npasses = (int32_t)plan.size();
     return QS_OK;
 }
 

@@ -57,39 +57,53 @@ __device__ __forceinline__ int cut_of(uint64_t i, const CutTerms& ct) {
     return c;
 }
 
-// ---- device-side gate descriptors --------------------------------------------
-struct DevGate {
-    int32_t kind;      // QS_KIND_*
-    int32_t tpos;      // target: tile position (tile kernel) or qubit (single-gate kernels)
-    int32_t control;   // control qubit (local index) or -1
-    int32_t pad;
-    uint64_t offset;   // doubles into the device matrix table
-    uint64_t stride;   // doubles per state
-};
-
-// Tile pass description for the fused kernel (lives in kernel params).
+// Tile pass description for the fused kernel.  Everything the kernel needs
+// per pass -- tile layout, register rounds, gate descriptors and shared 2x2
+// matrices -- is copied to the device once per pass and staged into shared
+// memory by each persistent CTA.
 constexpr int kTileLog2 = 12;          // 4096 amplitudes = 64 KiB of shared memory
 constexpr int kTileThreads = 256;      // 16 amplitudes per thread = 4 register qubits
 constexpr int kRegLog2 = kTileLog2 - 8;
-constexpr int kMaxRounds = 32;
-constexpr int kMaxPassGates = 128;
+constexpr int kMaxRounds = 24;
+constexpr int kMaxPassGates = 64;
 
-struct Round {
-    int32_t first_gate;   // index into the pass's gate array
-    int32_t num_gates;
-    int32_t npos;         // number of tile positions held in registers (<= kRegLog2)
-    int32_t pos[kRegLog2];
+// swizzle of a tile element index into its shared-memory slot; linear over
+// GF(2), so swz(a ^ b) == swz(a) ^ swz(b)
+__host__ __device__ __forceinline__ int swz(int e) {
+    return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7);
+}
+
+struct TileGate {
+    int32_t kind;    // QS_KIND_*
+    int32_t j;       // register bit of the target within its round
+    int32_t ctype;   // 0 none | 1 register bit cval | 2 tile position cval (outside the
+                     // round) | 3 local qubit cval outside the tile (tile-uniform)
+    int32_t cval;
+    uint64_t offset; // per-state table (stride != 0) or LUT, in doubles
+    uint64_t stride;
+    double u[8];     // the matrix when stride == 0
 };
 
-struct TilePass {
+struct Round {
+    int16_t first_gate, num_gates;
+    // tile-element deposits: thread id low/high nibble into the 8 positions not
+    // held in registers, register index k into the 4 round positions; the s*
+    // tables are the same values swizzled
+    uint16_t dlo[16], dhi[16], dk[16];
+    uint16_t slo[16], shi[16], sk[16];
+};
+
+struct alignas(16) TilePass {
     int32_t m;                 // local qubits per state
     int32_t num_rounds;
     int32_t low_run;           // tile positions 0..low_run-1 are qubits 0..low_run-1
+    int32_t pad;
     int32_t tile_bits[kTileLog2];  // ascending local qubit of each tile position
     uint64_t tiles_per_state;  // 2^(m - kTileLog2)
     uint64_t num_tiles;        // num_states * tiles_per_state
     uint64_t rank_offset;      // rank_index << m (global index of local offset 0)
     Round rounds[kMaxRounds];
+    TileGate gates[kMaxPassGates];
 };
 
 // ---- launchers (gate_kernels.cu / reduce_kernels.cu / exchange.cu) ---------
@@ -100,7 +114,7 @@ void launch_controlled(double2* psi, int m, int num_states, int c, int t, const 
 void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
                       const CutTerms& ct, const double* mats, uint64_t offset, uint64_t stride,
                       cudaStream_t s);
-void launch_tile_pass(double2* psi, int num_states, const TilePass& pass, const DevGate* gates,
+void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                       const double* mats, const CutTerms& ct, cudaStream_t s);
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s);
 void launch_gaussian(double2* psi, uint64_t count_per_state, int num_states, uint64_t rank_offset,

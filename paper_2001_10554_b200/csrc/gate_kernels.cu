@@ -128,7 +128,6 @@ __global__ void __launch_bounds__(kThreads) k_cut_phase(double2* __restrict__ ps
 }
 
 // ---- fused tile pass ------------------------------------------------------------
-__device__ __forceinline__ int swz(int e) { return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7); }
 
 constexpr int kTileAmps = 1 << kTileLog2;
 constexpr int kRegAmps = 1 << kRegLog2;
@@ -147,19 +146,24 @@ __device__ __forceinline__ void reg_gate(double2 (&a)[kRegAmps], const double2 u
     }
 }
 
-// Gate descriptor encoding inside a tile pass (built by the planner in capi.cu):
-//  tpos    register bit (0..kRegLog2-1) of the target within its round
-//  control -1 none; (1<<8)|j register bit j; (2<<8)|p tile position p (outside the
-//          round); (3<<8)|c local qubit c outside the tile (tile-uniform)
 __global__ void __launch_bounds__(kTileThreads, 2)
-    k_tile(double2* __restrict__ psi, const __grid_constant__ TilePass P,
-           const DevGate* __restrict__ gates, const double* __restrict__ mats,
-           const __grid_constant__ CutTerms ct) {
+    k_tile(double2* __restrict__ psi, const TilePass* __restrict__ pass_dev,
+           const double* __restrict__ mats, const __grid_constant__ CutTerms ct) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* tile = reinterpret_cast<double2*>(smem_raw);
     uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double2) * kTileAmps);
-
+    TilePass* pass_s = reinterpret_cast<TilePass*>(smem_raw + sizeof(double2) * kTileAmps +
+                                                   sizeof(uint64_t) * (kTileAmps >> 3));
     const int tid = threadIdx.x;
+    {
+        // the pass description (rounds, gates, shared matrices) is read once per
+        // persistent CTA and then served from shared memory (uniform broadcasts)
+        const uint4* src = reinterpret_cast<const uint4*>(pass_dev);
+        uint4* dst = reinterpret_cast<uint4*>(pass_s);
+        for (int i = tid; i < int(sizeof(TilePass) / 16); i += kTileThreads) dst[i] = src[i];
+        __syncthreads();
+    }
+    const TilePass& P = *pass_s;
     const int low_run = P.low_run;
     const int nrows = kTileAmps >> low_run;
     const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
@@ -198,59 +202,45 @@ __global__ void __launch_bounds__(kTileThreads, 2)
 
         for (int r = 0; r < P.num_rounds; ++r) {
             const Round& R = P.rounds[r];
-            int pbit[kRegLog2];
-            uint32_t inround = 0;
-#pragma unroll
-            for (int j = 0; j < kRegLog2; ++j) {
-                pbit[j] = 1 << R.pos[j];
-                inround |= pbit[j];
-            }
-            // positions not held in registers, ascending, receive the thread id bits
-            int ebase = 0;
-            for (int p = 0, bit = 0; p < kTileLog2; ++p) {
-                if (inround & (1u << p)) continue;
-                ebase |= ((tid >> bit) & 1) << p;
-                ++bit;
-            }
-#define QSB_EOFF(k)                                                                       \
-    (ebase | (((k)&1) ? pbit[0] : 0) | (((k)&2) ? pbit[1] : 0) | (((k)&4) ? pbit[2] : 0) | \
-     (((k)&8) ? pbit[3] : 0))
+            const int eb = R.dlo[tid & 15] | R.dhi[tid >> 4];
+            const int sb = R.slo[tid & 15] ^ R.shi[tid >> 4];
             double2 a[kRegAmps];
 #pragma unroll
-            for (int k = 0; k < kRegAmps; ++k) a[k] = tile[swz(QSB_EOFF(k))];
+            for (int k = 0; k < kRegAmps; ++k) a[k] = tile[sb ^ R.sk[k]];
 
-            for (int g = R.first_gate; g < R.first_gate + R.num_gates; ++g) {
-                const DevGate G = gates[g];
+            const int g_end = R.first_gate + R.num_gates;
+            for (int g = R.first_gate; g < g_end; ++g) {
+                const TileGate& G = P.gates[g];
                 if (G.kind == QS_KIND_CUTPHASE) {
                     const double2* lut =
                         reinterpret_cast<const double2*>(mats + G.offset + s * G.stride);
 #pragma unroll
                     for (int k = 0; k < kRegAmps; ++k) {
-                        const int e = QSB_EOFF(k);
+                        const int e = eb | R.dk[k];
                         uint64_t local = base_local + rowoff[e >> low_run] + (uint64_t(e) & lowmask);
                         a[k] = cmul(a[k], __ldg(lut + cut_of(P.rank_offset | local, ct)));
                     }
                     continue;
                 }
+                if (G.ctype == 2 && !((eb >> G.cval) & 1)) continue;
+                if (G.ctype == 3 && !((base_local >> G.cval) & 1)) continue;
                 double2 u[4];
-                load_u(u, mats + G.offset + s * G.stride);
-                const int j = G.tpos;
-                int ctype = G.control < 0 ? 0 : (G.control >> 8);
-                int cval = G.control & 0xff;
-                bool uniform_on = true;
-                if (ctype == 2) uniform_on = (ebase >> cval) & 1;
-                if (ctype == 3) uniform_on = (base_local >> cval) & 1;
-                if (!uniform_on) continue;
-                switch (j) {
-                    case 0: reg_gate<0>(a, u, ctype == 1, cval); break;
-                    case 1: reg_gate<1>(a, u, ctype == 1, cval); break;
-                    case 2: reg_gate<2>(a, u, ctype == 1, cval); break;
-                    default: reg_gate<3>(a, u, ctype == 1, cval); break;
+                if (G.stride == 0) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) u[q] = make_double2(G.u[2 * q], G.u[2 * q + 1]);
+                } else {
+                    load_u(u, mats + G.offset + s * G.stride);
+                }
+                const bool rc = G.ctype == 1;
+                switch (G.j) {
+                    case 0: reg_gate<0>(a, u, rc, G.cval); break;
+                    case 1: reg_gate<1>(a, u, rc, G.cval); break;
+                    case 2: reg_gate<2>(a, u, rc, G.cval); break;
+                    default: reg_gate<3>(a, u, rc, G.cval); break;
                 }
             }
 #pragma unroll
-            for (int k = 0; k < kRegAmps; ++k) tile[swz(QSB_EOFF(k))] = a[k];
-#undef QSB_EOFF
+            for (int k = 0; k < kRegAmps; ++k) tile[sb ^ R.sk[k]] = a[k];
             __syncthreads();
         }
 
@@ -338,25 +328,27 @@ void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
                                                                        ct, mats, offset, stride);
 }
 
-size_t tile_smem_bytes() { return sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3); }
+size_t tile_smem_bytes() {
+    return sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3) + sizeof(TilePass);
+}
 
-void launch_tile_pass(double2* psi, int num_states, const TilePass& pass, const DevGate* gates,
+void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                       const double* mats, const CutTerms& ct, cudaStream_t s) {
     static bool configured = false;
     const size_t smem = tile_smem_bytes();
+    static int sms = 148, per_sm = 2;
     if (!configured) {
         cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile, kTileThreads, smem);
+        if (per_sm < 1) per_sm = 1;
         configured = true;
     }
-    int dev = 0, sms = 148, per_sm = 3;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile, kTileThreads, smem);
-    if (per_sm < 1) per_sm = 1;
     uint64_t grid = uint64_t(sms) * per_sm;
     if (grid > pass.num_tiles) grid = pass.num_tiles;
-    (void)num_states;
-    k_tile<<<unsigned(grid), kTileThreads, smem, s>>>(psi, pass, gates, mats, ct);
+    k_tile<<<unsigned(grid), kTileThreads, smem, s>>>(psi, pass_dev, mats, ct);
 }
 
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s) {

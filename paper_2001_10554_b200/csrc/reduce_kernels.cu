@@ -71,8 +71,54 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// Fast path for chunks of exactly 2048 elements: warp w of the block covers
+// elements [256w, 256w+256) as 8 coalesced groups of 32; each group is reduced
+// by a shuffle butterfly (xor 1,2,4,8,16 pairs adjacent elements first, and
+// IEEE addition is commutative, so every lane ends with the tree sum of the
+// group), the 8 group sums are combined as a tree in registers, and the 8
+// warp sums as a tree in shared memory -- the same association as tree_sum.
+constexpr int kWideLog2 = 11;
+__device__ __forceinline__ double warp_tree(double v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_tree_wide(const double2* __restrict__ psi, const double* __restrict__ src,
+                double* __restrict__ dst, int m, int kind, int q, uint64_t rank_offset,
+                const __grid_constant__ CutTerms ct, uint64_t elems_per_state,
+                uint64_t total_chunks) {
+    __shared__ double wsum[kThreads / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t chunks_per_state = elems_per_state >> kWideLog2;
+    for (uint64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
+        const uint64_t s = c / chunks_per_state;
+        const uint64_t first = ((c - s * chunks_per_state) << kWideLog2) + warp * 256 + lane;
+        double v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint64_t j = first + i * 32;
+            v[i] = psi ? obs_value(psi, m, kind, q, rank_offset, ct, s, j)
+                       : src[s * elems_per_state + j];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = warp_tree(v[i]);
+        double t = __dadd_rn(__dadd_rn(__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3])),
+                             __dadd_rn(__dadd_rn(v[4], v[5]), __dadd_rn(v[6], v[7])));
+        if (lane == 0) wsum[warp] = t;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double b = __dadd_rn(__dadd_rn(__dadd_rn(wsum[0], wsum[1]), __dadd_rn(wsum[2], wsum[3])),
+                                 __dadd_rn(__dadd_rn(wsum[4], wsum[5]), __dadd_rn(wsum[6], wsum[7])));
+            dst[c] = b;
+        }
+        __syncthreads();
+    }
+}
+
 inline unsigned grid_cap(uint64_t n) {
-    uint64_t cap = 148ull * 8;
+    uint64_t cap = 148ull * 16;
     return unsigned(n < cap ? (n ? n : 1) : cap);
 }
 
@@ -97,12 +143,17 @@ void launch_observable(const double2* psi, int m, int num_states, int kind, int 
     while (true) {
         int lg = 0;
         while ((uint64_t(1) << lg) < elems) ++lg;
-        int chunk_log2 = lg < kChunkLog2 ? lg : kChunkLog2;
+        const bool wide = lg >= kWideLog2;
+        int chunk_log2 = wide ? kWideLog2 : lg;
         uint64_t chunks_per_state = elems >> chunk_log2;
         uint64_t total = chunks_per_state * uint64_t(num_states);
         double* dst = chunks_per_state == 1 ? out_dev : bufs[level & 1];
-        k_tree<<<grid_cap(total), kThreads, 0, s>>>(state, src, dst, m, kind, q, rank_offset, ct,
-                                                    elems, chunk_log2, total);
+        if (wide)
+            k_tree_wide<<<grid_cap(total), kThreads, 0, s>>>(state, src, dst, m, kind, q,
+                                                             rank_offset, ct, elems, total);
+        else
+            k_tree<<<grid_cap(total), kThreads, 0, s>>>(state, src, dst, m, kind, q, rank_offset,
+                                                        ct, elems, chunk_log2, total);
         if (chunks_per_state == 1) break;
         src = dst;
         state = nullptr;
