@@ -17,6 +17,7 @@ using namespace qsb;
 
 namespace qsb {
 size_t tile_smem_bytes();
+int prof_read(unsigned long long* out);
 }
 
 // ---------------------------------------------------------------------------
@@ -286,21 +287,23 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         int nonround[kTileLog2 - kRegLog2], c = 0;
         for (int p = 0; p < kTileLog2; ++p)
             if (!(used & (1u << p))) nonround[c++] = p;
-        for (int v = 0; v < 16; ++v) {
-            int lo = 0, hi = 0, kk = 0;
-            for (int b = 0; b < 4; ++b) {
-                if ((v >> b) & 1) {
-                    lo |= 1 << nonround[b];
-                    hi |= 1 << nonround[4 + b];
-                    kk |= 1 << round_pos[b];
-                }
-            }
-            R.dlo[v] = uint16_t(lo);
-            R.dhi[v] = uint16_t(hi);
-            R.dk[v] = uint16_t(kk);
-            R.slo[v] = uint16_t(swz(lo));
-            R.shi[v] = uint16_t(swz(hi));
-            R.sk[v] = uint16_t(swz(kk));
+        auto deposit = [](int v, const int* pos, int nbits) {
+            int out = 0;
+            for (int b = 0; b < nbits; ++b)
+                if ((v >> b) & 1) out |= 1 << pos[b];
+            return out;
+        };
+        for (int v = 0; v < (1 << kLaneLoBits); ++v) {
+            R.dlo[v] = uint16_t(deposit(v, nonround, kLaneLoBits));
+            R.slo[v] = uint16_t(swz(R.dlo[v]));
+        }
+        for (int v = 0; v < (1 << kLaneHiBits); ++v) {
+            R.dhi[v] = uint16_t(deposit(v, nonround + kLaneLoBits, kLaneHiBits));
+            R.shi[v] = uint16_t(swz(R.dhi[v]));
+        }
+        for (int v = 0; v < (1 << kRegLog2); ++v) {
+            R.dk[v] = uint16_t(deposit(v, round_pos.data(), kRegLog2));
+            R.sk[v] = uint16_t(swz(R.dk[v]));
         }
         all_pos.push_back(round_pos);
     };
@@ -334,15 +337,17 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         d.kind = g.kind;
         d.offset = g.offset;
         d.stride = g.stride;
-        d.j = 0;
+        d.variant = 0;
         d.ctype = 0;
         d.cval = 0;
+        d.seq = 0;
         if (g.kind == QS_KIND_CUTPHASE) continue;
-        if (g.stride == 0) memcpy(d.u, mats_host + g.offset, 8 * sizeof(double));
+        if (g.stride == 0) memcpy(&d.u[0], mats_host + g.offset, 8 * sizeof(double));
         const std::vector<int>& rp = all_pos[gate_round[i]];
-        int p = pos_of(g.target);
-        for (int j = 0; j < kRegLog2; ++j)
-            if (rp[j] == p) d.j = j;
+        int p = pos_of(g.target), j = 0;
+        for (int jj = 0; jj < kRegLog2; ++jj)
+            if (rp[jj] == p) j = jj;
+        d.variant = j;
         if (g.kind == QS_KIND_CTRL) {
             int pc = pos_of(g.control);
             if (pc < 0) {
@@ -350,11 +355,25 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
                 d.cval = g.control;
             } else {
                 int jc = -1;
-                for (int j = 0; j < kRegLog2; ++j)
-                    if (rp[j] == pc) jc = j;
+                for (int jj = 0; jj < kRegLog2; ++jj)
+                    if (rp[jj] == pc) jc = jj;
                 d.ctype = jc >= 0 ? 1 : 2;
                 d.cval = jc >= 0 ? jc : pc;
+                if (jc >= 0) d.variant = kRegLog2 + kRegLog2 * jc + j;
             }
+        }
+    }
+    // mark runs of uncontrolled gates on register bits 0,1,2 (in order, same round)
+    for (int i = 0; i < count;) {
+        int n = 0;
+        while (i + n < count && n < kRegLog2 && P.gates[i + n].kind == QS_KIND_1Q &&
+               P.gates[i + n].variant == n && gate_round[i + n] == gate_round[i])
+            ++n;
+        if (n >= 1) {
+            P.gates[i].seq = n;
+            i += n;
+        } else {
+            ++i;
         }
     }
     if (int rc = grow(&st->d_pass, &st->pass_cap, 1)) return rc;
@@ -935,6 +954,9 @@ int qs_exchange_gate_nccl(qs_state* st, int32_t peer, int32_t is_lower, const do
     cudaEventDestroy(ev_end);
     return QS_OK;
 }
+
+// Debug builds (-DQSB_PROF): cycle counters of the tile kernel's phases.
+int qs_debug_prof(unsigned long long* out8) { return prof_read(out8) ? QS_OK : QS_ERR_VALUE; }
 
 // ---- timing ------------------------------------------------------------------
 int qs_event_record(qs_state* st, int32_t slot) {

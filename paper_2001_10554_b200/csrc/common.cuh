@@ -62,8 +62,10 @@ __device__ __forceinline__ int cut_of(uint64_t i, const CutTerms& ct) {
 // matrices -- is copied to the device once per pass and staged into shared
 // memory by each persistent CTA.
 constexpr int kTileLog2 = 12;          // 4096 amplitudes = 64 KiB of shared memory
-constexpr int kTileThreads = 256;      // 16 amplitudes per thread = 4 register qubits
-constexpr int kRegLog2 = kTileLog2 - 8;
+constexpr int kRegLog2 = 4;            // 16 amplitudes per thread = 4 register qubits
+constexpr int kTileThreads = 1 << (kTileLog2 - kRegLog2);   // 512
+constexpr int kLaneLoBits = 4;
+constexpr int kLaneHiBits = kTileLog2 - kRegLog2 - kLaneLoBits;
 constexpr int kMaxRounds = 24;
 constexpr int kMaxPassGates = 64;
 
@@ -73,24 +75,28 @@ __host__ __device__ __forceinline__ int swz(int e) {
     return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7);
 }
 
-struct TileGate {
+struct alignas(16) TileGate {
+    double2 u[4];    // the matrix when stride == 0 (16-byte aligned: LDS.128 broadcasts)
+    uint64_t offset; // per-state table (stride != 0) or LUT, in doubles
+    uint64_t stride;
     int32_t kind;    // QS_KIND_*
-    int32_t j;       // register bit of the target within its round
+    int32_t variant; // j (target register bit, uncontrolled) or kRegLog2 + kRegLog2*c + j
+                     // (controlled by register bit c)
     int32_t ctype;   // 0 none | 1 register bit cval | 2 tile position cval (outside the
                      // round) | 3 local qubit cval outside the tile (tile-uniform)
     int32_t cval;
-    uint64_t offset; // per-state table (stride != 0) or LUT, in doubles
-    uint64_t stride;
-    double u[8];     // the matrix when stride == 0
+    int32_t seq;     // > 1 at the first gate of a run of `seq` uncontrolled gates on
+                     // register bits 0,1,..,seq-1 in order (compiled fast path)
+    int32_t pad[3];
 };
 
 struct Round {
     int16_t first_gate, num_gates;
-    // tile-element deposits: thread id low/high nibble into the 8 positions not
-    // held in registers, register index k into the 4 round positions; the s*
+    // tile-element deposits: thread id low/high bits into the positions not
+    // held in registers, register index k into the round positions; the s*
     // tables are the same values swizzled
-    uint16_t dlo[16], dhi[16], dk[16];
-    uint16_t slo[16], shi[16], sk[16];
+    uint16_t dlo[1 << kLaneLoBits], dhi[1 << kLaneHiBits], dk[1 << kRegLog2];
+    uint16_t slo[1 << kLaneLoBits], shi[1 << kLaneHiBits], sk[1 << kRegLog2];
 };
 
 struct alignas(16) TilePass {

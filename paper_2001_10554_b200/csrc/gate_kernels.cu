@@ -131,36 +131,135 @@ __global__ void __launch_bounds__(kThreads) k_cut_phase(double2* __restrict__ ps
 
 constexpr int kTileAmps = 1 << kTileLog2;
 constexpr int kRegAmps = 1 << kRegLog2;
-constexpr int kLoadsPerThread = kTileAmps / kTileThreads;  // 16
+constexpr int kLoadsPerThread = kTileAmps / kTileThreads;
 
-// 2x2 update on register bit J of the 16 amplitudes a thread holds; with
-// reg_control the pair is skipped unless register bit cval of its index is 1.
-template <int J>
-__device__ __forceinline__ void reg_gate(double2 (&a)[kRegAmps], const double2 u[4],
-                                         bool reg_control, int cval) {
+// 2x2 update on register bit J of the 16 amplitudes a thread holds.  C < 0:
+// uncontrolled; C >= 0: only pairs whose register bit C is 1.  Both are
+// compile-time, so the 8 (or 4) pair updates form one basic block the
+// scheduler can interleave (the FP64 dependency chains hide each other).
+template <int J, int C>
+__device__ __forceinline__ void reg_gate(double2 (&a)[kRegAmps], const double2 u[4]) {
 #pragma unroll
     for (int k = 0; k < kRegAmps; ++k) {
         if ((k >> J) & 1) continue;
-        if (reg_control && !((k >> cval) & 1)) continue;
+        if (C >= 0 && !((k >> C) & 1)) continue;
         pair_update(a[k], a[k | (1 << J)], u);
     }
 }
 
-__global__ void __launch_bounds__(kTileThreads, 2)
+// variant = j (uncontrolled) or kRegLog2 + kRegLog2*c + j (controlled by register bit c)
+#define QSB_V(J, C) ((C) < 0 ? (J) : kRegLog2 + kRegLog2 * (C) + (J))
+__device__ __forceinline__ void reg_gate_dispatch(double2 (&a)[kRegAmps], const double2 u[4],
+                                                  int variant) {
+    switch (variant) {
+        case QSB_V(0, -1): reg_gate<0, -1>(a, u); break;
+        case QSB_V(1, -1): reg_gate<1, -1>(a, u); break;
+        case QSB_V(2, -1): reg_gate<2, -1>(a, u); break;
+        case QSB_V(1, 0): reg_gate<1, 0>(a, u); break;
+        case QSB_V(2, 0): reg_gate<2, 0>(a, u); break;
+        case QSB_V(0, 1): reg_gate<0, 1>(a, u); break;
+        case QSB_V(2, 1): reg_gate<2, 1>(a, u); break;
+        case QSB_V(0, 2): reg_gate<0, 2>(a, u); break;
+        case QSB_V(1, 2): reg_gate<1, 2>(a, u); break;
+#if 1
+        case QSB_V(3, -1): reg_gate<3, -1>(a, u); break;
+        case QSB_V(3, 0): reg_gate<3, 0>(a, u); break;
+        case QSB_V(3, 1): reg_gate<3, 1>(a, u); break;
+        case QSB_V(3, 2): reg_gate<3, 2>(a, u); break;
+        case QSB_V(0, 3): reg_gate<0, 3>(a, u); break;
+        case QSB_V(1, 3): reg_gate<1, 3>(a, u); break;
+        case QSB_V(2, 3): reg_gate<2, 3>(a, u); break;
+#endif
+        default: break;
+    }
+}
+static_assert(kRegLog2 == 3 || kRegLog2 == 4, "dispatch table covers 3 or 4 register qubits");
+
+__device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, const double* mats,
+                                            uint64_t s) {
+    if (G.stride == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = G.u[q];  // shared memory (LDS.128 broadcast)
+    } else {
+        load_u(u, mats + G.offset + s * G.stride);  // per-state table in global memory
+    }
+}
+
+// Fast path: N uncontrolled gates on register bits 0..N-1 in program order as
+// one straight-line block (no dispatch, no register shuffling between gates).
+template <int N>
+__device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* G,
+                                        const double* mats, uint64_t s) {
+    double2 u[4];
+    gate_matrix(u, G[0], mats, s);
+    reg_gate<0, -1>(a, u);
+    if (N > 1) {
+        gate_matrix(u, G[1], mats, s);
+        reg_gate<1, -1>(a, u);
+    }
+    if (N > 2) {
+        gate_matrix(u, G[2], mats, s);
+        reg_gate<2, -1>(a, u);
+    }
+    if (N > 3) {
+        gate_matrix(u, G[3], mats, s);
+        reg_gate<3, -1>(a, u);
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+#ifdef QSB_PROF
+__device__ unsigned long long g_prof[8];
+#define PROF_T(v) long long v = clock64()
+#define PROF_ADD(i, a, b) if ((threadIdx.x & 31) == 0) atomicAdd(&g_prof[i], (unsigned long long)((b) - (a)))
+#else
+#define PROF_T(v)
+#define PROF_ADD(i, a, b)
+#endif
+// Persistent CTA, one per SM, of two warp groups ("ping-pong").  Each group
+// owns a 2^12-amplitude tile buffer and walks its own tiles; the FP64 sections
+// of the two groups alternate through a pair of named barriers, so one
+// group's arithmetic always runs while the other group moves data (cp.async
+// tile loads, the shared-memory round trips between register rounds and the
+// write-back to HBM).  Barrier ids: 1,2 group-local; 3,4 "turn of group g".
+#ifndef QSB_TILE_GROUPS
+#define QSB_TILE_GROUPS 2
+#endif
+constexpr int kGroups = QSB_TILE_GROUPS;
+constexpr int kCtaThreads = kGroups * kTileThreads;
+
+// PHASE: the pass has cut-phase gates; GENERIC: it has gates outside the
+// uncontrolled in-order runs (controlled gates, repeated register bits).
+template <bool PHASE, bool GENERIC>
+__global__ void __launch_bounds__(kCtaThreads, 1)
     k_tile(double2* __restrict__ psi, const TilePass* __restrict__ pass_dev,
            const double* __restrict__ mats, const __grid_constant__ CutTerms ct) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* tile = reinterpret_cast<double2*>(smem_raw);
-    uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double2) * kTileAmps);
-    TilePass* pass_s = reinterpret_cast<TilePass*>(smem_raw + sizeof(double2) * kTileAmps +
+    uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + kGroups * sizeof(double2) * kTileAmps);
+    TilePass* pass_s = reinterpret_cast<TilePass*>(smem_raw + kGroups * sizeof(double2) * kTileAmps +
                                                    sizeof(uint64_t) * (kTileAmps >> 3));
-    const int tid = threadIdx.x;
     {
         // the pass description (rounds, gates, shared matrices) is read once per
         // persistent CTA and then served from shared memory (uniform broadcasts)
         const uint4* src = reinterpret_cast<const uint4*>(pass_dev);
         uint4* dst = reinterpret_cast<uint4*>(pass_s);
-        for (int i = tid; i < int(sizeof(TilePass) / 16); i += kTileThreads) dst[i] = src[i];
+        for (int i = threadIdx.x; i < int(sizeof(TilePass) / 16); i += kCtaThreads) dst[i] = src[i];
         __syncthreads();
     }
     const TilePass& P = *pass_s;
@@ -168,7 +267,7 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     const int nrows = kTileAmps >> low_run;
     const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
     // row offsets: deposit of the row index into the tile bits above the low run
-    for (int r = tid; r < nrows; r += kTileThreads) {
+    for (int r = threadIdx.x; r < nrows; r += kCtaThreads) {
         uint64_t off = 0;
         for (int k = 0; k < kTileLog2 - low_run; ++k)
             if ((r >> k) & 1) off |= uint64_t(1) << P.tile_bits[low_run + k];
@@ -176,82 +275,108 @@ __global__ void __launch_bounds__(kTileThreads, 2)
     }
     __syncthreads();
 
+    const int group = threadIdx.x / kTileThreads;  // warp-uniform
+    const int tid = threadIdx.x % kTileThreads;
+    const int gbar = 1 + group;
+    const int my_turn = 3 + group, other_turn = 4 - group;
+    double2* tile = reinterpret_cast<double2*>(smem_raw) + group * kTileAmps;
     const int m = P.m;
     const int tps_log2 = m - kTileLog2;
-    for (uint64_t tile_id = blockIdx.x; tile_id < P.num_tiles; tile_id += gridDim.x) {
-        const uint64_t s = tile_id >> tps_log2;
-        uint64_t x = tile_id & (P.tiles_per_state - 1);
-#pragma unroll
-        for (int k = 0; k < kTileLog2; ++k) x = insert0(x, P.tile_bits[k]);
-        const uint64_t base_local = x;                  // local offset of tile element 0
-        double2* gbase = psi + ((s << m) | base_local);
+    const uint64_t stride_tiles = uint64_t(kGroups) * gridDim.x;
+    const uint64_t iters = (P.num_tiles + stride_tiles - 1) / stride_tiles;
+    if (kGroups > 1 && group == 1) named_arrive(3, kCtaThreads);  // group 0 computes first
 
-        // HBM -> shared: consecutive threads read consecutive amplitudes of a row
+    for (uint64_t it = 0; it < iters; ++it) {
+        const uint64_t tile_id = it * stride_tiles + uint64_t(blockIdx.x) * kGroups + group;
+        const bool valid = tile_id < P.num_tiles;
+        const uint64_t s = tile_id >> tps_log2;
+        uint64_t base_local = tile_id & (P.tiles_per_state - 1);
 #pragma unroll
-        for (int h = 0; h < kLoadsPerThread; h += 8) {
-            double2 v[8];
+        for (int k = 0; k < kTileLog2; ++k) base_local = insert0(base_local, P.tile_bits[k]);
+        double2* gbase = psi + ((s << m) | base_local);
+        if (valid) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                int e = tid + (h + i) * kTileThreads;
-                v[i] = gbase[rowoff[e >> low_run] + (e & lowmask)];
+            for (int i = 0; i < kLoadsPerThread; ++i) {
+                const int e = tid + i * kTileThreads;
+                cp_async16(tile + swz(e), gbase + rowoff[e >> low_run] + (e & lowmask));
             }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) tile[swz(tid + (h + i) * kTileThreads)] = v[i];
         }
-        __syncthreads();
+        PROF_T(t0);
+        cp_async_commit();
+        cp_async_wait_all();
+        named_sync(gbar, kTileThreads);
+        PROF_T(t1);
+        PROF_ADD(0, t0, t1);
 
         for (int r = 0; r < P.num_rounds; ++r) {
+            PROF_T(r0);
             const Round& R = P.rounds[r];
-            const int eb = R.dlo[tid & 15] | R.dhi[tid >> 4];
-            const int sb = R.slo[tid & 15] ^ R.shi[tid >> 4];
+            const int eb = R.dlo[tid & 15] | R.dhi[tid >> kLaneLoBits];
+            const int sb = R.slo[tid & 15] ^ R.shi[tid >> kLaneLoBits];
             double2 a[kRegAmps];
 #pragma unroll
             for (int k = 0; k < kRegAmps; ++k) a[k] = tile[sb ^ R.sk[k]];
 
-            const int g_end = R.first_gate + R.num_gates;
-            for (int g = R.first_gate; g < g_end; ++g) {
-                const TileGate& G = P.gates[g];
-                if (G.kind == QS_KIND_CUTPHASE) {
-                    const double2* lut =
-                        reinterpret_cast<const double2*>(mats + G.offset + s * G.stride);
+            PROF_T(r1);
+            if (kGroups > 1) named_sync(my_turn, kCtaThreads);
+            PROF_T(r2);
+            if (valid) {
+                const int g_end = R.first_gate + R.num_gates;
+                for (int g = R.first_gate; g < g_end; ++g) {
+                    const TileGate& G = P.gates[g];
+                    if (PHASE && G.kind == QS_KIND_CUTPHASE) {
+                        const double2* lut =
+                            reinterpret_cast<const double2*>(mats + G.offset + s * G.stride);
 #pragma unroll
-                    for (int k = 0; k < kRegAmps; ++k) {
-                        const int e = eb | R.dk[k];
-                        uint64_t local = base_local + rowoff[e >> low_run] + (uint64_t(e) & lowmask);
-                        a[k] = cmul(a[k], __ldg(lut + cut_of(P.rank_offset | local, ct)));
+                        for (int k = 0; k < kRegAmps; ++k) {
+                            const int e = eb | R.dk[k];
+                            uint64_t local =
+                                base_local + rowoff[e >> low_run] + (uint64_t(e) & lowmask);
+                            a[k] = cmul(a[k], __ldg(lut + cut_of(P.rank_offset | local, ct)));
+                        }
+                        continue;
                     }
-                    continue;
-                }
-                if (G.ctype == 2 && !((eb >> G.cval) & 1)) continue;
-                if (G.ctype == 3 && !((base_local >> G.cval) & 1)) continue;
-                double2 u[4];
-                if (G.stride == 0) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) u[q] = make_double2(G.u[2 * q], G.u[2 * q + 1]);
-                } else {
-                    load_u(u, mats + G.offset + s * G.stride);
-                }
-                const bool rc = G.ctype == 1;
-                switch (G.j) {
-                    case 0: reg_gate<0>(a, u, rc, G.cval); break;
-                    case 1: reg_gate<1>(a, u, rc, G.cval); break;
-                    case 2: reg_gate<2>(a, u, rc, G.cval); break;
-                    default: reg_gate<3>(a, u, rc, G.cval); break;
+                    switch (G.seq) {
+                        case 4: reg_seq<4>(a, &G, mats, s); g += 3; continue;
+                        case 3: reg_seq<3>(a, &G, mats, s); g += 2; continue;
+                        case 2: reg_seq<2>(a, &G, mats, s); g += 1; continue;
+                        case 1: reg_seq<1>(a, &G, mats, s); continue;
+                        default: break;
+                    }
+                    if (GENERIC) {
+                        if (G.ctype == 2 && !((eb >> G.cval) & 1)) continue;
+                        if (G.ctype == 3 && !((base_local >> G.cval) & 1)) continue;
+                        double2 u[4];
+                        gate_matrix(u, G, mats, s);
+                        reg_gate_dispatch(a, u, G.variant);
+                    }
                 }
             }
+            PROF_T(r3);
+            if (kGroups > 1) named_arrive(other_turn, kCtaThreads);
 #pragma unroll
             for (int k = 0; k < kRegAmps; ++k) tile[sb ^ R.sk[k]] = a[k];
-            __syncthreads();
+            named_sync(gbar, kTileThreads);
+            PROF_T(r4);
+            PROF_ADD(1, r0, r1);
+            PROF_ADD(2, r1, r2);
+            PROF_ADD(3, r2, r3);
+            PROF_ADD(4, r3, r4);
         }
+        PROF_T(s0);
 
-        // shared -> HBM
+        if (valid) {
 #pragma unroll
-        for (int i = 0; i < kLoadsPerThread; ++i) {
-            int e = tid + i * kTileThreads;
-            gbase[rowoff[e >> low_run] + (e & lowmask)] = tile[swz(e)];
+            for (int i = 0; i < kLoadsPerThread; ++i) {
+                const int e = tid + i * kTileThreads;
+                gbase[rowoff[e >> low_run] + (e & lowmask)] = tile[swz(e)];
+            }
         }
-        __syncthreads();
+        named_sync(gbar, kTileThreads);
+        PROF_T(s1);
+        PROF_ADD(5, s0, s1);
     }
+    if (kGroups > 1 && group == 0) named_sync(3, kCtaThreads);  // consume group 1's last hand-over
 }
 
 __global__ void k_fill(double2* __restrict__ psi, uint64_t count, double2 value) {
@@ -329,26 +454,64 @@ void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
 }
 
 size_t tile_smem_bytes() {
-    return sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3) + sizeof(TilePass);
+    return kGroups * sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3) +
+           sizeof(TilePass);
 }
 
-void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
-                      const double* mats, const CutTerms& ct, cudaStream_t s) {
+template <bool PH, bool GE>
+void launch_tile_variant(double2* psi, const TilePass* pass_dev, const double* mats,
+                         const CutTerms& ct, uint64_t num_tiles, cudaStream_t s) {
     static bool configured = false;
+    static int sms = 148, per_sm = 1;
     const size_t smem = tile_smem_bytes();
-    static int sms = 148, per_sm = 2;
     if (!configured) {
-        cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_tile<PH, GE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile, kTileThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<PH, GE>, kCtaThreads, smem);
         if (per_sm < 1) per_sm = 1;
         configured = true;
     }
     uint64_t grid = uint64_t(sms) * per_sm;
-    if (grid > pass.num_tiles) grid = pass.num_tiles;
-    k_tile<<<unsigned(grid), kTileThreads, smem, s>>>(psi, pass_dev, mats, ct);
+    const uint64_t need = (num_tiles + kGroups - 1) / kGroups;
+    if (grid > need) grid = need;
+    k_tile<PH, GE><<<unsigned(grid), kCtaThreads, smem, s>>>(psi, pass_dev, mats, ct);
+}
+
+void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
+                      const double* mats, const CutTerms& ct, cudaStream_t s) {
+    bool phase = false, generic = false;
+    for (int r = 0; r < pass.num_rounds; ++r) {
+        const Round& R = pass.rounds[r];
+        for (int g = R.first_gate; g < R.first_gate + R.num_gates; ++g) {
+            const TileGate& G = pass.gates[g];
+            if (G.kind == QS_KIND_CUTPHASE) {
+                phase = true;
+            } else if (G.seq > 0) {
+                g += G.seq - 1;
+            } else {
+                generic = true;
+            }
+        }
+    }
+    if (phase && generic) launch_tile_variant<true, true>(psi, pass_dev, mats, ct, pass.num_tiles, s);
+    else if (phase) launch_tile_variant<true, false>(psi, pass_dev, mats, ct, pass.num_tiles, s);
+    else if (generic) launch_tile_variant<false, true>(psi, pass_dev, mats, ct, pass.num_tiles, s);
+    else launch_tile_variant<false, false>(psi, pass_dev, mats, ct, pass.num_tiles, s);
+}
+
+int prof_read(unsigned long long* out) {
+#ifdef QSB_PROF
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, g_prof, sizeof(g_prof));
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+    return 1;
+#else
+    (void)out;
+    return 0;
+#endif
 }
 
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s) {

@@ -95,5 +95,27 @@ def main():
             print(json.dumps({"kernel": "k_tree", "obs": kind, "ms": med, "gbs": rd / med / 1e6}))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--scan" not in sys.argv:
     main()
+
+
+def pass_scan(m=30, reps=3):
+    """Tile-pass time vs number of fused gates (low targets 0..k-1 / high targets)."""
+    st = N.DeviceState(m, m)
+    device_gaussian(st, 5)
+    rng = np.random.default_rng(1)
+    amps = 1 << m
+    for base in (0, 18):
+        for k in (2, 3, 6, 9, 12):
+            if base + k > m or (base > 0 and k > 9):
+                continue
+            us = np.stack([haar_2x2(rng) for _ in range(k)]).view(np.float64).reshape(-1)
+            gates = [N.QsGate(0, base + i, -1, 0, 8 * i, 0) for i in range(k)]
+            med, _ = timed(st, lambda: st.apply_program(gates, us, fuse=True), reps)
+            print(json.dumps({"scan": "tile", "first_target": base, "gates": k, "ms": med,
+                              "gbs": 32 * amps / med / 1e6,
+                              "ms_per_gate_fp64_floor": 10 * amps * k / 18e12 * 1e3}))
+
+
+if __name__ == "__main__" and "--scan" in sys.argv:
+    pass_scan()
