@@ -303,7 +303,10 @@ def run_ours(args):
                                              "share": float(np.sum(v) / ms_dev)}
     bytes_per_launch = 32.0 * (2 ** m)  # one pass: read + write every amplitude once
     achieved = bytes_per_launch / (dom_ms / 1e3) / 1e9
-    traffic = ncu_traffic(LAUNCH_KINDS.get(dom, ""))
+    tr = ncu_traffic(LAUNCH_KINDS.get(dom, ""))
+    traffic = None
+    if tr and tr.get("bytes_per_amplitude"):
+        traffic = tr["bytes_per_amplitude"] * (2 ** m)
 
     # e2e through the public API with host buffers (upload + sweep + download)
     e2e = run_e2e(args, ctx, st, sweeps, step, m, n, dist)
