@@ -231,6 +231,8 @@ def run_reference(args):
 # ---- our arm ----------------------------------------------------------------------------
 def run_ours(args):
     world, rank, local = dist_env()
+    if os.environ.get("QSB_ALL_RANKS_ON_DEVICE0"):
+        local = 0  # functional multi-rank run on one GPU (exchange kernels never wait on each other)
     dist = init_dist(world)
     import paper_2001_10554_b200 as qs
     from paper_2001_10554_b200 import _native, runtime

@@ -63,11 +63,11 @@ class GateQueue:
 
     def one_qubit(self, q: int, u) -> None:
         """u: (2,2) shared or (S,2,2) per state."""
-        u = np.asarray(u, dtype=np.complex128)
+        u = np.ascontiguousarray(u, dtype=np.complex128)
         self._add(_native.QS_KIND_1Q, q, -1, u.view(np.float64), u.ndim == 3)
 
     def controlled(self, c: int, t: int, u) -> None:
-        u = np.asarray(u, dtype=np.complex128)
+        u = np.ascontiguousarray(u, dtype=np.complex128)
         self._add(_native.QS_KIND_CTRL, t, c, u.view(np.float64), u.ndim == 3)
 
     def cut_phase(self, graph, gamma) -> None:
