@@ -415,8 +415,170 @@ def run_e2e(args, ctx, st, sweeps, step, m, n, dist):
             "note": "per GPU bytes; wall clock around upload + sweep + download"}
 
 
+QAOA_N, QAOA_P, QAOA_POOL = 20, 4, 512
+
+
+def pso_step(pos, vel, best_pos, best_val, gbest, values, rng, lo=0.0, hi=np.pi):
+    """Standard PSO move (reference optimize.py:79-117 restated for the pool
+    driver): fold in values, then v <- w v + phi_p r_p (best - x) + phi_g r_g (g - x)."""
+    better = values > best_val
+    best_val = np.where(better, values, best_val)
+    best_pos = np.where(better[:, None], pos, best_pos)
+    k = int(np.argmax(best_val))
+    gbest = best_pos[k].copy()
+    r = rng.random((pos.shape[0], 2))
+    vel = 0.66 * vel + 1.6 * r[:, :1] * (best_pos - pos) + 0.62 * r[:, 1:] * (gbest - pos)
+    pos = lo + np.mod(pos + vel - lo, hi - lo)
+    return pos, vel, best_pos, best_val, gbest
+
+
+def qaoa_tables(positions, depth):
+    from paper_2001_10554_b200.circuit import qaoa_bindings
+
+    S = positions.shape[0]
+    tables = {}
+    for s in range(S):
+        for name, v in qaoa_bindings(depth, positions[s]).items():
+            tables.setdefault(name, np.empty(S))[s] = v
+    return tables
+
+
+def exact_maxcut(graph, n):
+    idx = np.arange(1 << n, dtype=np.uint64)
+    cuts = np.zeros(idx.shape, dtype=np.float64)
+    for u, v in graph.edges:
+        cuts += ((idx >> np.uint64(u)) ^ (idx >> np.uint64(v))) & np.uint64(1)
+    return float(cuts.max())
+
+
+def cpu_qaoa_sample(graph, positions, depth, threads):
+    """Reference algorithm (oracle port) on the host: `threads` QAOA circuits
+    evaluated concurrently, one per host thread (numpy releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import circuit as ocirc
+    from oracle import statevector as osv
+
+    n = graph.num_vertices
+    edges = list(graph.edges)
+
+    def one(pos):
+        prog = [{"kind": "h", "qubits": (q,)} for q in range(n)]
+        for k in range(depth):
+            prog.append({"kind": "diagcost", "param": pos[k], "edges": edges})
+            prog += [{"kind": "rx", "qubits": (q,), "param": 2.0 * pos[depth + k]}
+                     for q in range(n)]
+        return osv.maxcut_expectation(ocirc.run(n, prog), edges)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        vals = list(ex.map(one, positions[:threads]))
+    dt = time.perf_counter() - t0
+    return len(vals) / dt, dt, vals
+
+
 def run_qaoa(args, dist, comm, world, rank, local):
-    raise SystemExit("qaoa workload: see bench_qaoa.py")
+    """BASELINE config 5: a pool of 512 QAOA MaxCut circuits (n=20, p=4) per
+    swarm step, split across GPUs in contiguous blocks (no state exchange).
+    A step = reset + 104 gates on every pool state + <C> per state + the
+    host PSO move; parameter tables go host->device and <C> device->host
+    inside every step (so the step is end to end)."""
+    from paper_2001_10554_b200 import runtime
+    from paper_2001_10554_b200.circuit import build_qaoa_circuit
+    from paper_2001_10554_b200.workloads import random_3regular_graph
+
+    n, depth, S = QAOA_N, QAOA_P, QAOA_POOL
+    first, count = runtime.split_pool(S, rank, world)
+    rng = np.random.default_rng(args.seed)
+    graph = random_3regular_graph(n, rng)
+    circ = build_qaoa_circuit(graph, depth)
+    exact = exact_maxcut(graph, n)
+    pos = rng.uniform(0, np.pi, size=(S, 2 * depth))[first:first + count]
+    vel = rng.uniform(-0.5, 0.5, size=(S, 2 * depth))[first:first + count]
+    best_pos, best_val = pos.copy(), np.full(count, -np.inf)
+    gbest = pos[0].copy()
+    ctx = runtime.make_context(None, n, num_states=count, device=local, fuse=not args.no_fuse)
+    ctx.norm_check_interval = 0
+    st = ctx.state
+    edges = np.asarray(graph.edges, dtype=np.int32)
+    prng = np.random.default_rng(args.seed + rank)
+
+    def step():
+        nonlocal pos, vel, best_pos, best_val, gbest
+        runtime.reset_state(ctx)
+        runtime.run_circuit_pool(ctx, circ, qaoa_tables(pos, depth))
+        values = ctx.pool.observable(3, 0, edges) / exact
+        pos, vel, best_pos, best_val, gbest = pso_step(pos, vel, best_pos, best_val, gbest,
+                                                       values, prng)
+        return values
+
+    for _ in range(args.warmup):
+        step()
+    st.synchronize()
+    barrier(dist)
+    clocks = ClockSampler(local)
+    clocks.start()
+    st.launch_log(True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        values = step()
+    st.synchronize()
+    wall = time.perf_counter() - t0
+    st.launch_log(False)
+    launch_ms, launch_kind = st.read_launch_log()
+    clock = clocks.stop()
+    wall = max_over_ranks(dist, wall)
+    gates_per_circuit = len(circ.gates)
+    circuits = S * args.steps
+    units = circuits * gates_per_circuit * (2.0 ** n) / 2.0 ** 30
+    value = units / wall
+    kinds = {}
+    for k, t in zip(launch_kind, launch_ms):
+        kinds.setdefault(int(k), []).append(float(t))
+    dev_ms = sum(sum(v) for v in kinds.values())
+    dom = max(kinds, key=lambda k: sum(kinds[k]))
+    dom_ms = float(np.mean(kinds[dom]))
+    peak, peak_src = measured_peak()
+    bytes_per_launch = 32.0 * (2 ** n) * count
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import cpu_baseline as cb
+
+        cps, dt, _ = cpu_qaoa_sample(graph, pos, depth, cb.threads())
+        cpu = {"value": cps * gates_per_circuit * (2.0 ** n) / 2.0 ** 30, "unit": UNIT,
+               "cores": cb.threads(), "kind": "port",
+               "sample": f"{cb.threads()} QAOA circuits (n={n}, p={depth}, {gates_per_circuit} "
+                         f"gates + <C>) on {cb.threads()} host threads, oracle port, {dt:.2f} s",
+               "circuits_per_s": cps}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c128 (f64 pairs)", "data": "synthetic",
+            "config": {"workload": f"config 5: QAOA MaxCut pool, {S} circuits per swarm step "
+                                   f"(n={n}, p={depth}, random 3-regular graph), <C> per "
+                                   "circuit, host PSO move", "pool": S, "per_gpu": count,
+                       "gates_per_circuit": gates_per_circuit, "fused": not args.no_fuse},
+            "circuits_per_s": circuits / wall,
+            "best_ratio": float(np.max(best_val)),
+            "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
+                         "achieved": bytes_per_launch / (dom_ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_per_launch / (dom_ms / 1e3) / 1e9 / peak,
+                         "traffic": None, "avg_launch_ms": dom_ms, "peak_source": peak_src},
+            "kernel_share": {LAUNCH_KINDS.get(k, str(k)): {"launches": len(v),
+                                                           "share": float(np.sum(v) / dev_ms)}
+                             for k, v in kinds.items()},
+            "gpu_launches": int(len(launch_ms)),
+            "clocks": clock,
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(count * (2 * depth * 8 * n + 2 * 31 * 16 * depth)),
+                    "d2h_bytes_per_step": int(8 * count),
+                    "note": "the step itself is end to end: parameter tables up, <C> down"},
+        }
+        print(json.dumps(line))
+    barrier(dist)
+    return 0
 
 
 def main():

@@ -26,7 +26,7 @@ from . import _native
 from . import distribution as dist
 from . import gates as gates_mod
 from . import statevector as sv
-from .graphs import edge_array, phase_lut
+from .graphs import edge_array, phase_lut, phase_lut_batch
 
 NORM_CHECK_INTERVAL = 100
 NORM_TOL = 1e-10
@@ -80,7 +80,7 @@ class GateQueue:
             lut = phase_lut(float(gam), len(edges))
             self._add(_native.QS_KIND_CUTPHASE, 0, -1, lut.view(np.float64), False)
         else:
-            luts = np.stack([phase_lut(float(g), len(edges)) for g in gam])
+            luts = phase_lut_batch(gam, len(edges))
             self._add(_native.QS_KIND_CUTPHASE, 0, -1, luts.view(np.float64), True)
 
     def flush(self) -> int:
@@ -351,9 +351,7 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None)
         if gate.kind == "diagcost":
             q.cut_phase(gate.graph, vals)
         elif gate.kind in gates_mod.ROTATION_GATES:
-            fn = gates_mod.ROTATION_GATES[gate.kind]
-            mats = np.stack([fn(float(v)) for v in vals])
-            q.one_qubit(gate.qubits[0], mats)
+            q.one_qubit(gate.qubits[0], gates_mod.rotation_batch(gate.kind, vals))
         elif gate.kind == "cphase":
             mats = np.stack([gates_mod.cphase(float(v)) for v in vals])
             q.controlled(gate.qubits[0], gate.qubits[1], mats)

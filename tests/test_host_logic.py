@@ -173,3 +173,11 @@ def test_cut_phase_callable_matches_reference_function():
     idx = np.arange(32, dtype=np.uint64)
     from oracle import statevector as osv
     assert np.array_equal(phase(idx), 0.37 * osv.cut_counts(g.edges, idx))
+
+
+def test_batched_matrices_and_luts_bit_identical_to_scalar():
+    th = np.random.default_rng(4).uniform(0, 2 * np.pi, 257)
+    for kind, fn in (("rx", gates.rx), ("ry", gates.ry), ("rz", gates.rz)):
+        assert bits_equal(gates.rotation_batch(kind, th), np.stack([fn(float(t)) for t in th]))
+    assert bits_equal(graphs.phase_lut_batch(th, 30),
+                      np.stack([graphs.phase_lut(float(t), 30) for t in th]))
