@@ -331,6 +331,14 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     }
     close_round();
     P.num_rounds = r + 1;
+    {
+        // the last round can store straight from registers when its lanes cover
+        // tile positions 0,1,2 (i.e. none of them is held in registers)
+        bool low_free = true;
+        for (int p : all_pos.back())
+            if (p < 3) low_free = false;
+        P.direct_store = (low_free && P.low_run >= 3) ? 1 : 0;
+    }
     for (int i = 0; i < count; ++i) {
         const qs_gate& g = prog[first + i];
         TileGate& d = P.gates[i];

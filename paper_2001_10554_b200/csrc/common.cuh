@@ -103,7 +103,7 @@ struct alignas(16) TilePass {
     int32_t m;                 // local qubits per state
     int32_t num_rounds;
     int32_t low_run;           // tile positions 0..low_run-1 are qubits 0..low_run-1
-    int32_t pad;
+    int32_t direct_store;      // last round writes registers straight to HBM (coalesced)
     int32_t tile_bits[kTileLog2];  // ascending local qubit of each tile position
     uint64_t tiles_per_state;  // 2^(m - kTileLog2)
     uint64_t num_tiles;        // num_states * tiles_per_state

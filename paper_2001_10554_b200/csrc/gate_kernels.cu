@@ -133,6 +133,8 @@ constexpr int kTileAmps = 1 << kTileLog2;
 constexpr int kRegAmps = 1 << kRegLog2;
 constexpr int kLoadsPerThread = kTileAmps / kTileThreads;
 
+static_assert(kRegLog2 == 4, "the register paths are written for 4 register qubits");
+
 // 2x2 update on register bit J of the 16 amplitudes a thread holds.  C < 0:
 // uncontrolled; C >= 0: only pairs whose register bit C is 1.  Both are
 // compile-time, so the 8 (or 4) pair updates form one basic block the
@@ -147,33 +149,6 @@ __device__ __forceinline__ void reg_gate(double2 (&a)[kRegAmps], const double2 u
     }
 }
 
-// variant = j (uncontrolled) or kRegLog2 + kRegLog2*c + j (controlled by register bit c)
-#define QSB_V(J, C) ((C) < 0 ? (J) : kRegLog2 + kRegLog2 * (C) + (J))
-__device__ __forceinline__ void reg_gate_dispatch(double2 (&a)[kRegAmps], const double2 u[4],
-                                                  int variant) {
-    switch (variant) {
-        case QSB_V(0, -1): reg_gate<0, -1>(a, u); break;
-        case QSB_V(1, -1): reg_gate<1, -1>(a, u); break;
-        case QSB_V(2, -1): reg_gate<2, -1>(a, u); break;
-        case QSB_V(1, 0): reg_gate<1, 0>(a, u); break;
-        case QSB_V(2, 0): reg_gate<2, 0>(a, u); break;
-        case QSB_V(0, 1): reg_gate<0, 1>(a, u); break;
-        case QSB_V(2, 1): reg_gate<2, 1>(a, u); break;
-        case QSB_V(0, 2): reg_gate<0, 2>(a, u); break;
-        case QSB_V(1, 2): reg_gate<1, 2>(a, u); break;
-#if 1
-        case QSB_V(3, -1): reg_gate<3, -1>(a, u); break;
-        case QSB_V(3, 0): reg_gate<3, 0>(a, u); break;
-        case QSB_V(3, 1): reg_gate<3, 1>(a, u); break;
-        case QSB_V(3, 2): reg_gate<3, 2>(a, u); break;
-        case QSB_V(0, 3): reg_gate<0, 3>(a, u); break;
-        case QSB_V(1, 3): reg_gate<1, 3>(a, u); break;
-        case QSB_V(2, 3): reg_gate<2, 3>(a, u); break;
-#endif
-        default: break;
-    }
-}
-static_assert(kRegLog2 == 3 || kRegLog2 == 4, "dispatch table covers 3 or 4 register qubits");
 
 __device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, const double* mats,
                                             uint64_t s) {
@@ -185,25 +160,62 @@ __device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, con
     }
 }
 
-// Fast path: N uncontrolled gates on register bits 0..N-1 in program order as
-// one straight-line block (no dispatch, no register shuffling between gates).
-template <int N>
-__device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* G,
+// Fast path: n (1..4) uncontrolled gates on register bits 0..n-1 in program
+// order as one straight-line block; later gates are skipped by uniform
+// branches, so one copy of the code serves every run length.
+__device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* G, int n,
                                         const double* mats, uint64_t s) {
     double2 u[4];
     gate_matrix(u, G[0], mats, s);
     reg_gate<0, -1>(a, u);
-    if (N > 1) {
+    if (n > 1) {
         gate_matrix(u, G[1], mats, s);
         reg_gate<1, -1>(a, u);
+        if (n > 2) {
+            gate_matrix(u, G[2], mats, s);
+            reg_gate<2, -1>(a, u);
+            if (n > 3) {
+                gate_matrix(u, G[3], mats, s);
+                reg_gate<3, -1>(a, u);
+            }
+        }
     }
-    if (N > 2) {
-        gate_matrix(u, G[2], mats, s);
-        reg_gate<2, -1>(a, u);
+}
+
+// The common case, a full run of 4: straight-line code with no branch between
+// gates, so the scheduler overlaps one gate's tail with the next gate's head.
+__device__ __forceinline__ void reg_seq4(double2 (&a)[kRegAmps], const TileGate* G,
+                                         const double* mats, uint64_t s) {
+    double2 u[4];
+    gate_matrix(u, G[0], mats, s);
+    reg_gate<0, -1>(a, u);
+    gate_matrix(u, G[1], mats, s);
+    reg_gate<1, -1>(a, u);
+    gate_matrix(u, G[2], mats, s);
+    reg_gate<2, -1>(a, u);
+    gate_matrix(u, G[3], mats, s);
+    reg_gate<3, -1>(a, u);
+}
+
+// Generic gate: target register bit j, pairs filtered by a uniform mask over
+// the register index of the pair's lower member (controls in registers).
+template <int J>
+__device__ __forceinline__ void reg_gate_masked(double2 (&a)[kRegAmps], const double2 u[4],
+                                                unsigned mask) {
+#pragma unroll
+    for (int k = 0; k < kRegAmps; ++k) {
+        if ((k >> J) & 1) continue;
+        if ((mask >> k) & 1) pair_update(a[k], a[k | (1 << J)], u);
     }
-    if (N > 3) {
-        gate_matrix(u, G[3], mats, s);
-        reg_gate<3, -1>(a, u);
+}
+
+__device__ __forceinline__ void reg_gate_generic(double2 (&a)[kRegAmps], const double2 u[4], int j,
+                                                 unsigned mask) {
+    switch (j) {
+        case 0: reg_gate_masked<0>(a, u, mask); break;
+        case 1: reg_gate_masked<1>(a, u, mask); break;
+        case 2: reg_gate_masked<2>(a, u, mask); break;
+        default: reg_gate_masked<3>(a, u, mask); break;
     }
 }
 
@@ -286,23 +298,36 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     const uint64_t iters = (P.num_tiles + stride_tiles - 1) / stride_tiles;
     if (kGroups > 1 && group == 1) named_arrive(3, kCtaThreads);  // group 0 computes first
 
-    for (uint64_t it = 0; it < iters; ++it) {
-        const uint64_t tile_id = it * stride_tiles + uint64_t(blockIdx.x) * kGroups + group;
-        const bool valid = tile_id < P.num_tiles;
-        const uint64_t s = tile_id >> tps_log2;
-        uint64_t base_local = tile_id & (P.tiles_per_state - 1);
+    auto tile_base = [&](uint64_t t) {
+        uint64_t x = t & (P.tiles_per_state - 1);
 #pragma unroll
-        for (int k = 0; k < kTileLog2; ++k) base_local = insert0(base_local, P.tile_bits[k]);
-        double2* gbase = psi + ((s << m) | base_local);
-        if (valid) {
+        for (int k = 0; k < kTileLog2; ++k) x = insert0(x, P.tile_bits[k]);
+        return x;
+    };
+    auto prefetch = [&](uint64_t t) {
+#ifndef QSB_NO_GMEM
+        if (t < P.num_tiles) {
+            const double2* g = psi + (((t >> tps_log2) << m) | tile_base(t));
 #pragma unroll
             for (int i = 0; i < kLoadsPerThread; ++i) {
                 const int e = tid + i * kTileThreads;
-                cp_async16(tile + swz(e), gbase + rowoff[e >> low_run] + (e & lowmask));
+                cp_async16(tile + swz(e), g + rowoff[e >> low_run] + (e & lowmask));
             }
         }
-        PROF_T(t0);
+#endif
         cp_async_commit();
+    };
+    const bool direct = P.direct_store != 0;
+    prefetch(uint64_t(blockIdx.x) * kGroups + group);
+
+    for (uint64_t it = 0; it < iters; ++it) {
+        const uint64_t tile_id = it * stride_tiles + uint64_t(blockIdx.x) * kGroups + group;
+        const uint64_t next_id = tile_id + stride_tiles;
+        const bool valid = tile_id < P.num_tiles;
+        const uint64_t s = tile_id >> tps_log2;
+        const uint64_t base_local = tile_base(tile_id);
+        double2* gbase = psi + ((s << m) | base_local);
+        PROF_T(t0);
         cp_async_wait_all();
         named_sync(gbar, kTileThreads);
         PROF_T(t1);
@@ -311,11 +336,22 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
         for (int r = 0; r < P.num_rounds; ++r) {
             PROF_T(r0);
             const Round& R = P.rounds[r];
+            const bool last = r == P.num_rounds - 1;
             const int eb = R.dlo[tid & 15] | R.dhi[tid >> kLaneLoBits];
             const int sb = R.slo[tid & 15] ^ R.shi[tid >> kLaneLoBits];
             double2 a[kRegAmps];
+#ifdef QSB_NO_SMEM_ROUND
+#pragma unroll
+            for (int k = 0; k < kRegAmps; ++k) a[k] = make_double2(sb * 1e-3 + k, eb * 1e-3);
+#else
 #pragma unroll
             for (int k = 0; k < kRegAmps; ++k) a[k] = tile[sb ^ R.sk[k]];
+#endif
+            if (last && direct) {
+                // the tile now lives in registers: the buffer is free for the next tile
+                named_sync(gbar, kTileThreads);
+                prefetch(next_id);
+            }
 
             PROF_T(r1);
             if (kGroups > 1) named_sync(my_turn, kCtaThreads);
@@ -336,26 +372,65 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                         }
                         continue;
                     }
-                    switch (G.seq) {
-                        case 4: reg_seq<4>(a, &G, mats, s); g += 3; continue;
-                        case 3: reg_seq<3>(a, &G, mats, s); g += 2; continue;
-                        case 2: reg_seq<2>(a, &G, mats, s); g += 1; continue;
-                        case 1: reg_seq<1>(a, &G, mats, s); continue;
-                        default: break;
+                    if (G.seq == 4) {
+                        reg_seq4(a, &G, mats, s);
+                        g += 3;
+                        continue;
+                    }
+                    if (G.seq > 0) {
+                        reg_seq(a, &G, G.seq, mats, s);
+                        g += G.seq - 1;
+                        continue;
                     }
                     if (GENERIC) {
                         if (G.ctype == 2 && !((eb >> G.cval) & 1)) continue;
                         if (G.ctype == 3 && !((base_local >> G.cval) & 1)) continue;
                         double2 u[4];
                         gate_matrix(u, G, mats, s);
-                        reg_gate_dispatch(a, u, G.variant);
+                        // register control c: only pairs whose register index has bit c set
+                        unsigned mask = 0xffffu;
+                        if (G.ctype == 1) {
+                            mask = 0;
+#pragma unroll
+                            for (int k = 0; k < kRegAmps; ++k)
+                                if ((k >> G.cval) & 1) mask |= 1u << k;
+                        }
+                        reg_gate_generic(a, u, G.variant % kRegLog2, mask);
                     }
                 }
             }
             PROF_T(r3);
             if (kGroups > 1) named_arrive(other_turn, kCtaThreads);
+            if (last && direct) {
+                // last round straight from registers to HBM: lanes 0-7 cover tile
+                // positions 0,1,2 (128-byte rows), so every warp store is 4 full rows
+#ifndef QSB_NO_GMEM
+                if (valid) {
+#pragma unroll
+                    for (int k = 0; k < kRegAmps; ++k) {
+                        const int e = eb | R.dk[k];
+                        gbase[rowoff[e >> low_run] + (e & lowmask)] = a[k];
+                    }
+                }
+#endif
+                PROF_T(r4);
+                PROF_ADD(1, r0, r1);
+                PROF_ADD(2, r1, r2);
+                PROF_ADD(3, r2, r3);
+                PROF_ADD(5, r3, r4);
+                break;
+            }
+#ifdef QSB_NO_SMEM_ROUND
+            {
+                double2 acc = a[0];
+#pragma unroll
+                for (int k = 1; k < kRegAmps; ++k) acc = cadd(acc, a[k]);
+                if (acc.x == 12345.678) tile[sb] = acc;  // keep the arithmetic alive
+            }
+#else
 #pragma unroll
             for (int k = 0; k < kRegAmps; ++k) tile[sb ^ R.sk[k]] = a[k];
+#endif
             named_sync(gbar, kTileThreads);
             PROF_T(r4);
             PROF_ADD(1, r0, r1);
@@ -363,18 +438,22 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             PROF_ADD(3, r2, r3);
             PROF_ADD(4, r3, r4);
         }
-        PROF_T(s0);
-
-        if (valid) {
+        if (!direct) {
+            PROF_T(s0);
+#ifndef QSB_NO_GMEM
+            if (valid) {
 #pragma unroll
-            for (int i = 0; i < kLoadsPerThread; ++i) {
-                const int e = tid + i * kTileThreads;
-                gbase[rowoff[e >> low_run] + (e & lowmask)] = tile[swz(e)];
+                for (int i = 0; i < kLoadsPerThread; ++i) {
+                    const int e = tid + i * kTileThreads;
+                    gbase[rowoff[e >> low_run] + (e & lowmask)] = tile[swz(e)];
+                }
             }
+#endif
+            named_sync(gbar, kTileThreads);
+            prefetch(next_id);
+            PROF_T(s1);
+            PROF_ADD(5, s0, s1);
         }
-        named_sync(gbar, kTileThreads);
-        PROF_T(s1);
-        PROF_ADD(5, s0, s1);
     }
     if (kGroups > 1 && group == 0) named_sync(3, kCtaThreads);  // consume group 1's last hand-over
 }
