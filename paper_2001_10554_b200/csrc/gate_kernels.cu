@@ -254,6 +254,11 @@ __device__ unsigned long long g_prof[8];
 #define QSB_TILE_GROUPS 2
 #endif
 constexpr int kGroups = QSB_TILE_GROUPS;
+#ifdef QSB_NO_PINGPONG
+constexpr bool kPingPong = false;
+#else
+constexpr bool kPingPong = kGroups > 1;
+#endif
 constexpr int kCtaThreads = kGroups * kTileThreads;
 
 // PHASE: the pass has cut-phase gates; GENERIC: it has gates outside the
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     const int tps_log2 = m - kTileLog2;
     const uint64_t stride_tiles = uint64_t(kGroups) * gridDim.x;
     const uint64_t iters = (P.num_tiles + stride_tiles - 1) / stride_tiles;
-    if (kGroups > 1 && group == 1) named_arrive(3, kCtaThreads);  // group 0 computes first
+    if (kPingPong && group == 1) named_arrive(3, kCtaThreads);  // group 0 computes first
 
     auto tile_base = [&](uint64_t t) {
         uint64_t x = t & (P.tiles_per_state - 1);
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             }
 
             PROF_T(r1);
-            if (kGroups > 1) named_sync(my_turn, kCtaThreads);
+            if (kPingPong) named_sync(my_turn, kCtaThreads);
             PROF_T(r2);
             if (valid) {
                 const int g_end = R.first_gate + R.num_gates;
@@ -400,7 +405,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                 }
             }
             PROF_T(r3);
-            if (kGroups > 1) named_arrive(other_turn, kCtaThreads);
+            if (kPingPong) named_arrive(other_turn, kCtaThreads);
             if (last && direct) {
                 // last round straight from registers to HBM: lanes 0-7 cover tile
                 // positions 0,1,2 (128-byte rows), so every warp store is 4 full rows
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             PROF_ADD(5, s0, s1);
         }
     }
-    if (kGroups > 1 && group == 0) named_sync(3, kCtaThreads);  // consume group 1's last hand-over
+    if (kPingPong && group == 0) named_sync(3, kCtaThreads);  // consume group 1's last hand-over
 }
 
 __global__ void k_fill(double2* __restrict__ psi, uint64_t count, double2 value) {

@@ -438,3 +438,73 @@ def test_n28_sampled_pairs_roundtrip_and_norm():
     assert abs(mid_norm - 1.0) < 1e-10
     assert max_dev(back, start) <= TOL
     assert not bits_equal(psi0, after)
+
+
+@pytest.mark.slow
+def test_n30_controlled_gates_properties():
+    """Config 3 at full size: sampled control=1 pairs are bit-exact against the
+    oracle's pair update, control=0 amplitudes are untouched, CNOT twice and
+    CPhase(phi)CPhase(-phi) return the state (CNOT exactly, CPhase to 1e-12)."""
+    from paper_2001_10554_b200 import _native as N
+    n = 30
+    st = N.DeviceState(n, n)
+    N.call("qs_init_gaussian", st.handle, 11)
+    rng = np.random.default_rng(8)
+    cases = [(0, 1), (1, 0), (5, 29), (29, 5), (13, 14)]
+    for c, t in cases:
+        u = ogates.random_unitary_2x2(rng)
+        before = st.download()
+        st.apply_program([N.QsGate(1, t, c, 0, 0, 0)], u.view(np.float64).ravel(), fuse=False)
+        after = st.download()
+        j = rng.integers(0, 1 << (n - 2), size=1 << 18, dtype=np.int64)
+        lo_b, hi_b = min(c, t), max(c, t)
+        x = ((j >> lo_b) << (lo_b + 1)) | (j & ((1 << lo_b) - 1))
+        x = ((x >> hi_b) << (hi_b + 1)) | (x & ((1 << hi_b) - 1))
+        lo = x | (1 << c)
+        hi = lo | (1 << t)
+        a, b = osv.pair_update(before[lo], before[hi], u)
+        assert bits_equal(after[lo], a) and bits_equal(after[hi], b), (c, t)
+        untouched = x  # control bit 0, target bit 0
+        assert bits_equal(after[untouched], before[untouched])
+        assert bits_equal(after[untouched | (1 << t)], before[untouched | (1 << t)])
+    start = st.download()
+    X = qs.gates.PAULI_X.view(np.float64).ravel()
+    for _ in range(2):
+        st.apply_program([N.QsGate(1, 17, 3, 0, 0, 0)], X, fuse=False)
+    assert bits_equal(st.download(), start)
+    phi = 1.234
+    st.apply_program([N.QsGate(1, 9, 22, 0, 0, 0)], qs.gates.cphase(phi).view(np.float64).ravel(),
+                     fuse=False)
+    st.apply_program([N.QsGate(1, 9, 22, 0, 0, 0)], qs.gates.cphase(-phi).view(np.float64).ravel(),
+                     fuse=False)
+    assert max_dev(st.download(), start) <= TOL
+
+
+@pytest.mark.slow
+def test_full_pool_512x20_sample_vs_oracle():
+    """Config 5 at full size: 512 pooled n=20 QAOA circuits in one batch; a
+    sample of states checked bit for bit against the oracle, all <C> finite."""
+    g = golden("golden_cfg5.npz")
+    graph = make_graph(20, g["edges"])
+    depth, S = 4, 512
+    rng = np.random.default_rng(21)
+    params = rng.uniform(0, np.pi, size=(S, 2 * depth))
+    tables = {}
+    for s in range(S):
+        for name, v in qaoa_bindings(depth, params[s]).items():
+            tables.setdefault(name, np.empty(S))[s] = v
+    ctx = runtime.make_context(None, 20, num_states=S)
+    runtime.run_circuit_pool(ctx, build_qaoa_circuit(graph, depth), tables)
+    values = runtime.measure_maxcut(ctx, graph)
+    assert values.shape == (S,) and np.all(np.isfinite(values))
+    amps = ctx.pool.amplitudes()
+    edges = [tuple(e) for e in g["edges"]]
+    for s in (0, 255, 511):
+        prog = [{"kind": "h", "qubits": (q,)} for q in range(20)]
+        for k in range(depth):
+            prog.append({"kind": "diagcost", "param": params[s][k], "edges": edges})
+            prog += [{"kind": "rx", "qubits": (q,), "param": 2.0 * params[s][depth + k]}
+                     for q in range(20)]
+        expect = ocirc.run(20, prog)
+        assert bits_equal(amps[s], expect)
+        assert values[s] == osv.maxcut_expectation(expect, edges)
