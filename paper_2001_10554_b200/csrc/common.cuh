@@ -61,9 +61,15 @@ __device__ __forceinline__ int cut_of(uint64_t i, const CutTerms& ct) {
 // per pass -- tile layout, register rounds, gate descriptors and shared 2x2
 // matrices -- is copied to the device once per pass and staged into shared
 // memory by each persistent CTA.
-constexpr int kTileLog2 = 12;          // 4096 amplitudes = 64 KiB of shared memory
-constexpr int kRegLog2 = 4;            // 16 amplitudes per thread = 4 register qubits
-constexpr int kTileThreads = 1 << (kTileLog2 - kRegLog2);   // 512
+#ifndef QSB_TILE_LOG2
+#define QSB_TILE_LOG2 12
+#endif
+#ifndef QSB_REG_LOG2
+#define QSB_REG_LOG2 4
+#endif
+constexpr int kTileLog2 = QSB_TILE_LOG2;  // 2^12 amplitudes = 64 KiB of shared memory
+constexpr int kRegLog2 = QSB_REG_LOG2;    // 16 amplitudes per thread = 4 register qubits
+constexpr int kTileThreads = 1 << (kTileLog2 - kRegLog2);
 constexpr int kLaneLoBits = 4;
 constexpr int kLaneHiBits = kTileLog2 - kRegLog2 - kLaneLoBits;
 constexpr int kMaxRounds = 24;
@@ -72,7 +78,7 @@ constexpr int kMaxPassGates = 64;
 // swizzle of a tile element index into its shared-memory slot; linear over
 // GF(2), so swz(a ^ b) == swz(a) ^ swz(b)
 __host__ __device__ __forceinline__ int swz(int e) {
-    return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9)) & 7);
+    return e ^ (((e >> 3) ^ (e >> 6) ^ (e >> 9) ^ (e >> 12)) & 7);
 }
 
 struct alignas(16) TileGate {

@@ -133,7 +133,7 @@ constexpr int kTileAmps = 1 << kTileLog2;
 constexpr int kRegAmps = 1 << kRegLog2;
 constexpr int kLoadsPerThread = kTileAmps / kTileThreads;
 
-static_assert(kRegLog2 == 4, "the register paths are written for 4 register qubits");
+static_assert(kRegLog2 >= 3 && kRegLog2 <= 5, "register paths cover 3..5 register qubits");
 
 // 2x2 update on register bit J of the 16 amplitudes a thread holds.  C < 0:
 // uncontrolled; C >= 0: only pairs whose register bit C is 1.  Both are
@@ -160,9 +160,9 @@ __device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, con
     }
 }
 
-// Fast path: n (1..4) uncontrolled gates on register bits 0..n-1 in program
-// order as one straight-line block; later gates are skipped by uniform
-// branches, so one copy of the code serves every run length.
+// Fast path: n (1..kRegLog2) uncontrolled gates on register bits 0..n-1 in
+// program order; later gates are skipped by uniform branches, so one copy of
+// the code serves every run length.
 __device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* G, int n,
                                         const double* mats, uint64_t s) {
     double2 u[4];
@@ -174,18 +174,22 @@ __device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* 
         if (n > 2) {
             gate_matrix(u, G[2], mats, s);
             reg_gate<2, -1>(a, u);
-            if (n > 3) {
+            if (kRegLog2 > 3 && n > 3) {
                 gate_matrix(u, G[3], mats, s);
-                reg_gate<3, -1>(a, u);
+                reg_gate<(kRegLog2 > 3 ? 3 : 0), -1>(a, u);
+                if (kRegLog2 > 4 && n > 4) {
+                    gate_matrix(u, G[4], mats, s);
+                    reg_gate<(kRegLog2 > 4 ? 4 : 0), -1>(a, u);
+                }
             }
         }
     }
 }
 
-// The common case, a full run of 4: straight-line code with no branch between
-// gates, so the scheduler overlaps one gate's tail with the next gate's head.
-__device__ __forceinline__ void reg_seq4(double2 (&a)[kRegAmps], const TileGate* G,
-                                         const double* mats, uint64_t s) {
+// The common case, a full run of kRegLog2 gates: straight-line code with no
+// branch between gates, so one gate's tail overlaps the next gate's head.
+__device__ __forceinline__ void reg_seq_full(double2 (&a)[kRegAmps], const TileGate* G,
+                                             const double* mats, uint64_t s) {
     double2 u[4];
     gate_matrix(u, G[0], mats, s);
     reg_gate<0, -1>(a, u);
@@ -193,8 +197,14 @@ __device__ __forceinline__ void reg_seq4(double2 (&a)[kRegAmps], const TileGate*
     reg_gate<1, -1>(a, u);
     gate_matrix(u, G[2], mats, s);
     reg_gate<2, -1>(a, u);
-    gate_matrix(u, G[3], mats, s);
-    reg_gate<3, -1>(a, u);
+    if (kRegLog2 > 3) {
+        gate_matrix(u, G[3], mats, s);
+        reg_gate<(kRegLog2 > 3 ? 3 : 0), -1>(a, u);
+    }
+    if (kRegLog2 > 4) {
+        gate_matrix(u, G[4], mats, s);
+        reg_gate<(kRegLog2 > 4 ? 4 : 0), -1>(a, u);
+    }
 }
 
 // Generic gate: target register bit j, pairs filtered by a uniform mask over
@@ -215,7 +225,8 @@ __device__ __forceinline__ void reg_gate_generic(double2 (&a)[kRegAmps], const d
         case 0: reg_gate_masked<0>(a, u, mask); break;
         case 1: reg_gate_masked<1>(a, u, mask); break;
         case 2: reg_gate_masked<2>(a, u, mask); break;
-        default: reg_gate_masked<3>(a, u, mask); break;
+        case 3: reg_gate_masked<(kRegLog2 > 3 ? 3 : 0)>(a, u, mask); break;
+        default: reg_gate_masked<(kRegLog2 > 4 ? 4 : 0)>(a, u, mask); break;
     }
 }
 
@@ -377,9 +388,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                         }
                         continue;
                     }
-                    if (G.seq == 4) {
-                        reg_seq4(a, &G, mats, s);
-                        g += 3;
+                    if (G.seq == kRegLog2) {
+                        reg_seq_full(a, &G, mats, s);
+                        g += kRegLog2 - 1;
                         continue;
                     }
                     if (G.seq > 0) {
@@ -393,7 +404,7 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                         double2 u[4];
                         gate_matrix(u, G, mats, s);
                         // register control c: only pairs whose register index has bit c set
-                        unsigned mask = 0xffffu;
+                        unsigned mask = (kRegAmps >= 32) ? 0xffffffffu : ((1u << kRegAmps) - 1);
                         if (G.ctype == 1) {
                             mask = 0;
 #pragma unroll
