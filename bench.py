@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--local-qubits", type=int, default=30)
     ap.add_argument("--no-fuse", action="store_true")
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "qaoa"])
+    ap.add_argument("--workload", default="sweep", choices=["sweep", "qaoa", "cfg4"])
     ap.add_argument("--seed", type=int, default=20260809)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -258,14 +258,17 @@ def run_ours(args):
     total_steps = args.warmup + args.steps
     sweeps = [[haar(rng) for _ in range(n)] for _ in range(total_steps)]
 
+    from paper_2001_10554_b200.circuit import GateSpec
+
+    cx_pairs = [(q, n - 1 - q) for q in range(n // 2)] if args.workload == "cfg4" else []
+
     def step(us):
-        q = ctx.queue
+        # config 2: Haar gate on every qubit; config 4 adds CX(q, n-1-q), q < n/2
+        # (pairs cross the local/global boundary: routed like the reference)
         for k in range(n):
-            if k < m:
-                q.one_qubit(k, us[k])
-            else:
-                ctx.flush()
-                qdist.apply_one_qubit_gate(ctx.partition, ctx.topology, comm, k, us[k])
+            runtime.apply_gate(ctx, GateSpec("custom", (k,), matrix=us[k]))
+        for c, t in cx_pairs:
+            runtime.apply_gate(ctx, GateSpec("cx", (c, t)))
         ctx.flush()
 
     for s in range(args.warmup):
@@ -288,9 +291,11 @@ def run_ours(args):
     clock = clocks.stop()
     barrier(dist)
     ms_total = max_over_ranks(dist, ms_dev)
-    units_per_step = n * (2.0 ** n) / 2.0 ** 30
+    gates_per_step = n + len(cx_pairs)
+    units_per_step = gates_per_step * (2.0 ** n) / 2.0 ** 30
     value = units_per_step * args.steps / (ms_total / 1e3)
-    bytes_per_step_per_gpu = 32.0 * (2 ** m) * n  # algorithmic: every gate r+w of the slice
+    # algorithmic: every 1q gate r+w of the slice, a CX the control=1 half
+    bytes_per_step_per_gpu = 32.0 * (2 ** m) * n + 16.0 * (2 ** m) * len(cx_pairs)
     hbm_gbs = bytes_per_step_per_gpu * world * args.steps / (ms_total / 1e3) / 1e9
 
     # dominant kernel and its roofline
@@ -311,17 +316,24 @@ def run_ours(args):
         traffic = tr["bytes_per_amplitude"] * (2 ** m)
 
     # e2e through the public API with host buffers (upload + sweep + download)
-    e2e = run_e2e(args, ctx, st, sweeps, step, m, n, dist)
+    if m <= 31:
+        e2e = run_e2e(args, ctx, st, sweeps, step, m, n, dist)
+    else:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+               "note": f"skipped: a 2^{m}-amplitude pinned host copy does not fit beside the "
+                       "state on this host"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_sweep_sample(min(m, 30), 3, args.seed)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and m <= 30:
+        cpu = cpu_sweep_sample(m, 3, args.seed)
 
     # config 2's per-target table: each target as a single unfused gate kernel
-    per_target = per_target_table(st, m, args.seed) if not args.no_per_target else None
+    per_target = (per_target_table(st, m, args.seed)
+                  if not args.no_per_target and args.workload == "sweep" else None)
     passes_per_step = len(launch_ms) / max(args.steps, 1)
     actual_gbs = 32.0 * (2 ** m) * passes_per_step * args.steps / (ms_dev / 1e3) / 1e9
-    fp64_ops = 10.0 * (2 ** m) * n * args.steps  # numpy-exact pair update: 20 FP64 ops per pair
+    # numpy-exact pair update: 20 FP64 ops per pair (a CX touches half the pairs)
+    fp64_ops = 10.0 * (2 ** m) * (n + 0.5 * len(cx_pairs)) * args.steps
     fp64_rate = fp64_ops / (ms_dev / 1e3) / 1e12
     if rank == 0:
         line = {
@@ -330,10 +342,13 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128 (f64 pairs)", "data": "synthetic",
             "config": {
-                "workload": f"config 2 sweep: Haar 2x2 on each of the {n} qubits in turn, "
-                            f"fresh unitaries per step, normalised Gaussian state, "
+                "workload": (f"config 2 sweep: Haar 2x2 on each of the {n} qubits in turn, "
+                             if args.workload == "sweep" else
+                             f"config 4 layer: Haar 2x2 on each of the {n} qubits, then "
+                             f"CX(q, n-1-q) for q < {n // 2}, ")
+                            + f"fresh unitaries per step, normalised Gaussian state, "
                             f"2^{m} c128 amplitudes per GPU (n={n}, {p} global qubits)",
-                "qubits": n, "local_qubits": m, "gates_per_step": n,
+                "qubits": n, "local_qubits": m, "gates_per_step": gates_per_step,
                 "fused": not args.no_fuse, "parallelism": f"state sharded over {world} GPU(s)",
                 "exchange": args.exchange if world > 1 else None,
                 "l2": "inputs larger than L2 (16 GiB state vs 126 MB)"},
