@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--no-per-target", action="store_true")
+    ap.add_argument("--remap", action="store_true",
+                    help="gates on global qubits swap the qubit into a local position "
+                         "(half the NVLink traffic) instead of the pair exchange")
     return ap.parse_args()
 
 
@@ -249,7 +252,8 @@ def run_ours(args):
     comm = qdist.TorchComm(exchange_mode=args.exchange) if world > 1 else qdist.single_rank_comm()
     if args.workload == "qaoa":
         return run_qaoa(args, dist, comm, world, rank, local)
-    ctx = runtime.make_context(comm, n, 1, device=local, fuse=not args.no_fuse)
+    ctx = runtime.make_context(comm, n, 1, device=local, fuse=not args.no_fuse,
+                               remap=args.remap)
     ctx.norm_check_interval = 0
     st = ctx.state
     group_norm = (lambda x: qdist.group_reduce_sum(x, ctx.topology, comm)) if world > 1 else None
@@ -350,7 +354,9 @@ def run_ours(args):
                             f"2^{m} c128 amplitudes per GPU (n={n}, {p} global qubits)",
                 "qubits": n, "local_qubits": m, "gates_per_step": gates_per_step,
                 "fused": not args.no_fuse, "parallelism": f"state sharded over {world} GPU(s)",
-                "exchange": args.exchange if world > 1 else None,
+                "exchange": (None if world == 1 else
+                             "qubit remapping (peer swap of half the slice)" if args.remap
+                             else args.exchange),
                 "l2": "inputs larger than L2 (16 GiB state vs 126 MB)"},
             "hbm_gbs": hbm_gbs,
             "hbm_gbs_note": "algorithmic: 32 B/amplitude for every gate (what an unfused "

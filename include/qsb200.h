@@ -152,6 +152,14 @@ int qs_exchange_gate_peer(qs_state* st, void* peer_amps, int32_t is_lower,
  * per message) and double-buffered; requires qs_comm_init. */
 int qs_exchange_gate_nccl(qs_state* st, int32_t peer_rank, int32_t is_lower,
                           const double* u, int32_t control_local, uint64_t chunk);
+/* Qubit remapping: SWAP the physical position of a global
+ * qubit (this rank's bit value rank_bit; the partner is the handle behind
+ * peer_amps) with local qubit local_qubit -- half the state crosses NVLink
+ * (2^(m-1) amplitudes each way, half of a Fig. 3 exchange) and the gate
+ * that needed the global qubit then runs locally (fusable).  qs_swap_qubits_local
+ * swaps two local positions (used to restore the canonical layout). */
+int qs_swap_qubits_peer(qs_state* st, void* peer_amps, int32_t local_qubit, int32_t rank_bit);
+int qs_swap_qubits_local(qs_state* st, int32_t a, int32_t c);
 /* CUDA IPC for peer mapping across processes (64-byte handles). */
 int qs_state_ipc_handle(const qs_state* st, unsigned char* handle64);
 int qs_peer_open(qs_state* st, const unsigned char* handle64, void** peer_amps);

@@ -28,7 +28,8 @@ EXPORTS = (
     "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
     "qs_apply_1q", "qs_apply_controlled", "qs_apply_cut_phase", "qs_apply_program",
     "qs_plan_program", "qs_last_program_passes", "qs_observable",
-    "qs_exchange_gate_peer", "qs_exchange_gate_nccl", "qs_state_ipc_handle", "qs_peer_open",
+    "qs_exchange_gate_peer", "qs_exchange_gate_nccl", "qs_swap_qubits_peer",
+    "qs_swap_qubits_local", "qs_state_ipc_handle", "qs_peer_open",
     "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
     "qs_event_record", "qs_event_elapsed_ms", "qs_launch_log", "qs_launch_log_read",
 )
@@ -91,6 +92,8 @@ _SIGNATURES = {
     "qs_observable": ([_P, _I, _I, _IP, _I, _DP], ctypes.c_int),
     "qs_exchange_gate_peer": ([_P, _P, _I, _DP, _I], ctypes.c_int),
     "qs_exchange_gate_nccl": ([_P, _I, _I, _DP, _I, _U], ctypes.c_int),
+    "qs_swap_qubits_peer": ([_P, _P, _I, _I], ctypes.c_int),
+    "qs_swap_qubits_local": ([_P, _I, _I], ctypes.c_int),
     "qs_state_ipc_handle": ([_P, _BP], ctypes.c_int),
     "qs_peer_open": ([_P, _BP, ctypes.POINTER(_P)], ctypes.c_int),
     "qs_peer_close": ([_P, _P], ctypes.c_int),

@@ -826,6 +826,39 @@ int qs_exchange_gate_peer(qs_state* st, void* peer_amps, int32_t is_lower, const
     return QS_OK;
 }
 
+int qs_swap_qubits_peer(qs_state* st, void* peer_amps, int32_t local_qubit, int32_t rank_bit) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (!peer_amps) return fail(QS_ERR_VALUE, "null peer pointer");
+    if (st->num_states != 1) return fail(QS_ERR_VALUE, "swap needs a single-state handle");
+    if (local_qubit < 0 || local_qubit >= st->m)
+        return fail(QS_ERR_LOCALITY, "qubit %d is not local", local_qubit);
+    if (int rc = ensure_device(st)) return rc;
+    {
+        LaunchScope ls(st, kLaunchExchange);
+        launch_swap_peer(st->psi, reinterpret_cast<double2*>(peer_amps), st->m, local_qubit,
+                         rank_bit ? 1 : 0, st->stream);
+    }
+    CHECK_LAUNCH();
+    st->messages += 2;
+    st->amplitudes += st->amps_per_state >> 1;
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    return QS_OK;
+}
+
+int qs_swap_qubits_local(qs_state* st, int32_t a, int32_t c) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (a == c) return fail(QS_ERR_VALUE, "swap needs two different qubits");
+    if (a < 0 || c < 0 || a >= st->m || c >= st->m)
+        return fail(QS_ERR_LOCALITY, "both qubits must be local");
+    if (int rc = ensure_device(st)) return rc;
+    {
+        LaunchScope ls(st, kLaunchExchange);
+        launch_swap_local(st->psi, st->m, st->num_states, a, c, st->stream);
+    }
+    CHECK_LAUNCH();
+    return QS_OK;
+}
+
 int qs_state_ipc_handle(const qs_state* st, unsigned char* handle64) {
     if (!st) return fail(QS_ERR_VALUE, "null state");
     CUDA_TRY(cudaSetDevice(st->device));

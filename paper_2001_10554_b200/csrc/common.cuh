@@ -142,6 +142,8 @@ void launch_observable(const double2* psi, int m, int num_states, int kind, int 
 
 void launch_exchange_peer(double2* mine, double2* peer, int m, bool is_lower, const double* u_dev,
                           int control_local, cudaStream_t s);
+void launch_swap_peer(double2* mine, double2* peer, int m, int l, int rank_bit, cudaStream_t s);
+void launch_swap_local(double2* psi, int m, int num_states, int a, int c, cudaStream_t s);
 void launch_pair_update_halves(double2* a, double2* b, uint64_t count, uint64_t first_offset,
                                const double* u_dev, int control_local, cudaStream_t s);
 

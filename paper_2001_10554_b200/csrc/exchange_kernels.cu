@@ -80,7 +80,101 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// SWAP of physical qubits p (global: this rank's bit value b) and l (local)
+// between partner ranks: the amplitude at local offset o with bit l = 1-b
+// trades places with the partner's amplitude at o ^ 2^l.  Pure data movement;
+// the two ranks split the pairs on local bit s (!= l).
+__global__ void __launch_bounds__(kThreads)
+    k_swap_peer(double2* __restrict__ mine, double2* __restrict__ peer, int l, int s, int b,
+                uint64_t total) {
+    const uint64_t first = uint64_t(blockIdx.x) * (kThreads * kIlp) + threadIdx.x;
+    const uint64_t lbit = uint64_t(1) << l;
+    uint64_t off[kIlp];
+    double2 x[kIlp], y[kIlp];
+#pragma unroll
+    for (int i = 0; i < kIlp; ++i) {
+        uint64_t j = first + uint64_t(i) * kThreads;
+        if (j < total) {
+            uint64_t o;
+            if (s < 0) {
+                o = insert0(j, l);
+            } else {
+                int lb = l < s ? l : s, hb = l < s ? s : l;
+                o = insert0(insert0(j, lb), hb) | (uint64_t(b) << s);
+            }
+            o |= uint64_t(1 - b) << l;
+            off[i] = o;
+            x[i] = mine[o];
+            y[i] = peer[o ^ lbit];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kIlp; ++i) {
+        uint64_t j = first + uint64_t(i) * kThreads;
+        if (j < total) {
+            mine[off[i]] = y[i];
+            peer[off[i] ^ lbit] = x[i];
+        }
+    }
+}
+
+// SWAP of two local qubits a < c (all states of the handle): amplitudes with
+// (bit a, bit c) = (1, 0) trade places with (0, 1).
+__global__ void __launch_bounds__(kThreads)
+    k_swap_local(double2* __restrict__ psi, int m, int a, int c, uint64_t total) {
+    const uint64_t first = uint64_t(blockIdx.x) * (kThreads * kIlp) + threadIdx.x;
+    const uint64_t qmask = (uint64_t(1) << (m - 2)) - 1;
+    uint64_t lo[kIlp];
+    double2 x[kIlp], y[kIlp];
+#pragma unroll
+    for (int i = 0; i < kIlp; ++i) {
+        uint64_t p = first + uint64_t(i) * kThreads;
+        if (p < total) {
+            uint64_t st = p >> (m - 2), j = p & qmask;
+            uint64_t o = insert0(insert0(j, a), c);
+            lo[i] = (st << m) | o | (uint64_t(1) << a);
+            x[i] = psi[lo[i]];
+            y[i] = psi[lo[i] ^ (uint64_t(1) << a) ^ (uint64_t(1) << c)];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < kIlp; ++i) {
+        uint64_t p = first + uint64_t(i) * kThreads;
+        if (p < total) {
+            psi[lo[i]] = y[i];
+            psi[lo[i] ^ (uint64_t(1) << a) ^ (uint64_t(1) << c)] = x[i];
+        }
+    }
+}
+
 }  // namespace
+
+void launch_swap_peer(double2* mine, double2* peer, int m, int l, int rank_bit, cudaStream_t st) {
+    int s = -1;
+    uint64_t total;
+    if (m >= 2) {
+        s = (l == m - 1) ? m - 2 : m - 1;
+        total = uint64_t(1) << (m - 2);
+    } else {
+        if (rank_bit != 0) return;  // m == 1: the lower rank moves the single pair
+        total = 1;
+    }
+    uint64_t per_block = kThreads * kIlp;
+    unsigned grid = unsigned((total + per_block - 1) / per_block);
+    k_swap_peer<<<grid ? grid : 1, kThreads, 0, st>>>(mine, peer, l, s, rank_bit, total);
+}
+
+void launch_swap_local(double2* psi, int m, int num_states, int a, int c, cudaStream_t st) {
+    if (a > c) {
+        int t = a;
+        a = c;
+        c = t;
+    }
+    uint64_t total = uint64_t(num_states) << (m - 2);
+    uint64_t per_block = kThreads * kIlp;
+    unsigned grid = unsigned((total + per_block - 1) / per_block);
+    k_swap_local<<<grid ? grid : 1, kThreads, 0, st>>>(psi, m, a, c, total);
+}
 
 void launch_exchange_peer(double2* mine, double2* peer, int m, bool is_lower, const double* u_dev,
                           int control_local, cudaStream_t s) {

@@ -332,6 +332,98 @@ def _exchange_pairs(partition: sv.StatePartition, comm: GroupComm, q: int, u,
     comm.pair_barrier(partner)
 
 
+# ---- qubit remapping -------------------------------------------
+class QubitLayout:
+    """Logical -> physical qubit positions of a distributed state.  Physical
+    positions below m are local bits of the slice, the rest are rank bits.
+    Every rank keeps an identical copy (all updates are collective)."""
+
+    def __init__(self, num_qubits: int, num_local_qubits: int):
+        self.n, self.m = num_qubits, num_local_qubits
+        self.phys = list(range(num_qubits))
+        self.log = list(range(num_qubits))
+        self._next = 0
+        self.recent: list = []  # physical positions in order of last use (most recent last)
+
+    def use(self, phys: int) -> None:
+        if self.recent and self.recent[-1] == phys:
+            return
+        if phys in self.recent:
+            self.recent.remove(phys)
+        self.recent.append(phys)
+
+    def is_identity(self) -> bool:
+        return self.phys == list(range(self.n))
+
+    def swap(self, p1: int, p2: int) -> None:
+        a, b = self.log[p1], self.log[p2]
+        self.log[p1], self.log[p2] = b, a
+        self.phys[a], self.phys[b] = p2, p1
+        # recency follows the logical qubit: the positions trade places
+        self.recent = [p2 if x == p1 else p1 if x == p2 else x for x in self.recent]
+
+    def choose_slot(self, protected=()) -> int:
+        """A local physical slot to trade for a global qubit: round-robin over
+        the top local positions, skipping the ones the current gate uses."""
+        for _ in range(self.m):
+            slot = self.m - 1 - (self._next % self.m)
+            self._next += 1
+            if slot not in protected:
+                return slot
+        raise ValueError("no local slot available for the swap")
+
+
+def swap_global_local(partition, comm: GroupComm, topology: RankTopology, layout: QubitLayout,
+                      p: int, l: int) -> None:
+    """Collective SWAP of physical global position p with local position l
+    (half the slice crosses to the partner, k_swap_peer)."""
+    m = topology.num_local_qubits
+    if not (p >= m > l >= 0):
+        raise ValueError(f"swap needs a global and a local position, got {p}, {l}")
+    d = 1 << (p - m)
+    partner = comm.rank ^ d
+    bit = 1 if comm.rank & d else 0
+    st = partition.sync_in()
+    st.synchronize()
+    comm.pair_barrier(partner)
+    _native.call("qs_swap_qubits_peer", st.handle, comm.peer_pointer(partner), l, bit)
+    comm.pair_barrier(partner)
+    layout.swap(p, l)
+
+
+def make_local(partition, comm: GroupComm, topology: RankTopology, layout: QubitLayout,
+               q: int, protected=()) -> int:
+    """Physical local position of logical qubit q, swapping it in if global."""
+    p = layout.phys[q]
+    if p < topology.num_local_qubits:
+        return p
+    slot = layout.choose_slot(protected)
+    swap_global_local(partition, comm, topology, layout, p, slot)
+    return slot
+
+
+def restore_layout(partition, comm: GroupComm, topology: RankTopology,
+                   layout: QubitLayout) -> None:
+    """Bring every logical qubit back to its own physical position (collective)."""
+    m, n = topology.num_local_qubits, topology.num_qubits
+    for p in range(m, n):
+        if layout.log[p] == p:
+            continue
+        lp = layout.phys[p]
+        if lp >= m:  # logical p sits on another rank bit: bring it local first
+            slot = layout.choose_slot(protected=())
+            swap_global_local(partition, comm, topology, layout, lp, slot)
+            lp = slot
+        swap_global_local(partition, comm, topology, layout, p, lp)
+    st = partition.sync_in()
+    for l in range(m):
+        if layout.log[l] == l:
+            continue
+        lp = layout.phys[l]
+        _native.call("qs_swap_qubits_local", st.handle, l, lp)
+        layout.swap(l, lp)
+
+
 def apply_one_qubit_gate(partition, topology: RankTopology, comm: GroupComm, q: int, u,
                          chunk: int = DEFAULT_CHUNK_AMPLITUDES):
     """Collective one-qubit gate (distribution.py:181-192)."""

@@ -49,6 +49,7 @@ class GateQueue:
         self.edges: np.ndarray | None = None
         self.passes_total = 0
         self.gates_total = 0
+        self.touched: set = set()  # physical positions the queued gates act on
 
     def __len__(self) -> int:
         return len(self.gates)
@@ -65,16 +66,19 @@ class GateQueue:
         """u: (2,2) shared or (S,2,2) per state."""
         u = np.ascontiguousarray(u, dtype=np.complex128)
         self._add(_native.QS_KIND_1Q, q, -1, u.view(np.float64), u.ndim == 3)
+        self.touched.add(q)
 
     def controlled(self, c: int, t: int, u) -> None:
         u = np.ascontiguousarray(u, dtype=np.complex128)
         self._add(_native.QS_KIND_CTRL, t, c, u.view(np.float64), u.ndim == 3)
+        self.touched.update((c, t))
 
     def cut_phase(self, graph, gamma) -> None:
         edges = edge_array(graph)
         if self.edges is not None and not np.array_equal(self.edges, edges):
             self.flush()
         self.edges = edges
+        self.touched.update(int(x) for x in edges.ravel())
         gam = np.asarray(gamma, dtype=np.float64)
         if gam.ndim == 0:
             lut = phase_lut(float(gam), len(edges))
@@ -92,6 +96,7 @@ class GateQueue:
         self.gates_total += len(self.gates)
         self.gates, self.tables, self.size = [], [], 0
         self.edges = None
+        self.touched = set()
         return passes
 
 
@@ -128,8 +133,10 @@ class RankContext:
     num_states: int = 1
     device: int = 0
     fuse: bool = True
+    remap: bool = False
     norm_check_interval: int = NORM_CHECK_INTERVAL
     topology: dist.RankTopology = field(init=False)
+    layout: "dist.QubitLayout | None" = field(init=False, default=None)
     partition: sv.StatePartition | None = field(init=False, default=None)
     pool: "PoolState | None" = field(init=False, default=None)
     queue: GateQueue | None = field(init=False, default=None)
@@ -147,6 +154,9 @@ class RankContext:
                     device=self.device)
                 sv.init_basis_state(self.partition, 0)
                 self.queue = GateQueue(self.partition.state, self.fuse)
+                if self.remap and self.topology.rank_bits > 0:
+                    self.layout = dist.QubitLayout(self.num_qubits,
+                                                   self.topology.num_local_qubits)
             else:
                 self.pool = PoolState(self.num_qubits, self.num_states, self.device, self.fuse)
                 self.queue = self.pool.queue
@@ -168,24 +178,86 @@ class RankContext:
 
 
 def make_context(comm: dist.GroupComm | None, num_qubits: int, num_states: int = 1,
-                 device: int = 0, fuse: bool = True) -> RankContext:
-    return RankContext(comm or dist.single_rank_comm(), num_qubits, num_states, device, fuse)
+                 device: int = 0, fuse: bool = True, remap: bool = False) -> RankContext:
+    """remap=True: gates on global qubits first swap the qubit into a local
+    position (half the traffic of the reference's exchange, and the gate then
+    fuses with its neighbours); reads restore the canonical layout."""
+    return RankContext(comm or dist.single_rank_comm(), num_qubits, num_states, device, fuse,
+                       remap)
 
 
-def reset_state(ctx: RankContext, index: int = 0) -> None:
-    if ctx.is_idle:
+def _restore(ctx: RankContext) -> None:
+    if ctx.layout is not None and not ctx.layout.is_identity():
+        ctx.flush()
+        dist.restore_layout(ctx.partition, ctx.comm, ctx.topology, ctx.layout)
+
+
+def _apply_gate_remapped(ctx: RankContext, gate) -> None:
+    """apply_gate under a qubit layout: logical qubits are mapped to physical
+    positions; a gate on a global position swaps it in first."""
+    L, topo, q = ctx.layout, ctx.topology, ctx.queue
+    m = topo.num_local_qubits
+    kind = gate.kind
+    if kind == "diagcost":
+        from .graphs import make_graph
+        g = gate.graph
+        phys = make_graph(ctx.num_qubits, [(L.phys[u], L.phys[v]) for u, v in g.edges])
+        q.cut_phase(phys, _angle(gate))
         return
-    ctx.queue.gates, ctx.queue.tables, ctx.queue.size, ctx.queue.edges = [], [], 0, None
-    if ctx.partition is not None:
-        sv.init_basis_state(ctx.partition, index)
-    else:
-        _native.call("qs_init_basis", ctx.pool.state.handle, index)
-    ctx.gates_applied = 0
+    if kind in ("cx", "cz", "cphase", "cu"):
+        c, t = gate.qubits
+        u = _matrix_for(gate)
+        if L.phys[t] >= m:
+            pc = L.phys[c]
+            _swap_in(ctx, t, protected=(pc,) if pc < m else ())
+        pc, pt = L.phys[c], L.phys[t]
+        L.use(pt)
+        if pc < m:
+            q.controlled(pc, pt, u)
+            return
+        # control on a rank bit: the queued gate depends on this rank's bit pc,
+        # so a later swap of pc (or pt) must not overtake it; mark both on every
+        # rank so swap decisions stay identical
+        if (ctx.comm.rank >> (pc - m)) & 1:
+            q.one_qubit(pt, u)
+        q.touched.update((pc, pt))
+        return
+    qb = gate.qubits[0]
+    u = _matrix_for(gate)
+    if L.phys[qb] >= m:
+        _swap_in(ctx, qb)
+    q.one_qubit(L.phys[qb], u)
+    L.use(L.phys[qb])
+
+
+def _swap_in(ctx: RankContext, qubit: int, protected=()) -> None:
+    """Swap logical `qubit` (on a rank bit) into a local position: flush the
+    queue, then evict the most recently used local position (in sweeps and
+    layered circuits that qubit is needed last).  Half the slice crosses to the
+    partner (k_swap_peer) instead of the whole slice of a pair exchange, and the
+    gate itself then runs locally and fuses with its successors."""
+    L, m = ctx.layout, ctx.topology.num_local_qubits
+    ctx.flush()
+    p = L.phys[qubit]
+    slot = next((l for l in reversed(L.recent) if l < m and l not in protected), None)
+    if slot is None:
+        slot = next(l for l in range(m - 1, -1, -1) if l not in protected)
+    dist.swap_global_local(ctx.partition, ctx.comm, ctx.topology, L, p, slot)
 
 
 def apply_gate(ctx: RankContext, gate) -> None:
     """Queue one gate; global-qubit gates flush and exchange (runtime.py:115-152)."""
     if ctx.is_idle:
+        return
+    if ctx.layout is not None:
+        _apply_gate_remapped(ctx, gate)
+        ctx.gates_applied += 1
+        if ctx.norm_check_interval and ctx.gates_applied % ctx.norm_check_interval == 0:
+            # the drift check needs no canonical layout (any association is fine)
+            norm_sq = measure_norm_squared(ctx, restore=False)
+            if abs(norm_sq - 1.0) >= NORM_TOL:
+                raise NormDriftError(
+                    f"norm^2 drifted to {norm_sq!r} after {ctx.gates_applied} gates")
         return
     kind = gate.kind
     topo = ctx.topology
@@ -231,9 +303,11 @@ def _group_reduce(ctx: RankContext, partial: float) -> float:
     return dist.group_reduce_sum(partial, ctx.topology, ctx.comm)
 
 
-def measure_norm_squared(ctx: RankContext):
+def measure_norm_squared(ctx: RankContext, restore: bool = True):
     if ctx.is_idle:
         return 0.0
+    if restore:
+        _restore(ctx)
     ctx.flush()
     if ctx.pool is not None:
         return ctx.pool.observable(_native.QS_OBS_NORM)
@@ -243,6 +317,7 @@ def measure_norm_squared(ctx: RankContext):
 def measure_probability(ctx: RankContext, q: int):
     if ctx.is_idle:
         return 0.0
+    _restore(ctx)
     ctx.flush()
     if ctx.pool is not None:
         return ctx.pool.observable(_native.QS_OBS_PROB, q)
@@ -252,6 +327,7 @@ def measure_probability(ctx: RankContext, q: int):
 def measure_z(ctx: RankContext, q: int):
     if ctx.is_idle:
         return 0.0
+    _restore(ctx)
     ctx.flush()
     if ctx.pool is not None:
         return ctx.pool.observable(_native.QS_OBS_Z, q)
@@ -261,6 +337,7 @@ def measure_z(ctx: RankContext, q: int):
 def measure_maxcut(ctx: RankContext, graph):
     if ctx.is_idle:
         return 0.0
+    _restore(ctx)
     ctx.flush()
     if ctx.pool is not None:
         return ctx.pool.observable(_native.QS_OBS_MAXCUT, 0, edge_array(graph))
@@ -274,6 +351,7 @@ def gather_group_state(ctx: RankContext) -> np.ndarray | None:
     if ctx.is_idle and not isinstance(ctx.comm, dist.TorchComm):
         return None
     if not ctx.is_idle:
+        _restore(ctx)
         ctx.flush()
     mine = ctx.state.download() if not ctx.is_idle else None
     comm = ctx.comm
@@ -410,12 +488,12 @@ def run_spmd(world_size: int, fn, timeout: float = 30.0, exchange_mode: str = "p
 
 def simulate_circuit(circuit, num_ranks: int = 1, bindings: dict | None = None,
                      device: int = 0, fuse: bool = True, timeout: float = 30.0,
-                     exchange_mode: str = "peer") -> np.ndarray:
+                     exchange_mode: str = "peer", remap: bool = False) -> np.ndarray:
     """Run a circuit over `num_ranks` emulated ranks and return the full state
     (runtime.py:291-302).  All emulated ranks share `device`."""
 
     def rank_fn(comm):
-        ctx = make_context(comm, circuit.num_qubits, 1, device, fuse)
+        ctx = make_context(comm, circuit.num_qubits, 1, device, fuse, remap)
         run_circuit(ctx, circuit, bindings)
         return gather_group_state(ctx)
 

@@ -508,3 +508,52 @@ def test_full_pool_512x20_sample_vs_oracle():
         expect = ocirc.run(20, prog)
         assert bits_equal(amps[s], expect)
         assert values[s] == osv.maxcut_expectation(expect, edges)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_config4_qubit_remapping_bit_exact(p):
+    """Qubit remapping (global qubits swapped into local positions, half the
+    exchange traffic) reproduces the reference's run_spmd output bit for bit
+    once the canonical layout is restored."""
+    g = golden("golden_cfg4_m10.npz")
+    P, n = 1 << p, 10 + p
+    psi0, us, ref = g[f"psi0_p{p}"], g[f"us_p{p}"], g[f"out_p{p}"]
+    seq, k = [], 0
+    for layer in range(4):
+        for q in range(n):
+            seq.append(GateSpec("custom", (q,), matrix=us[k]))
+            k += 1
+        for q in range(n // 2):
+            seq.append(GateSpec("cx", (q, n - 1 - q)))
+    circ = Circuit(n, tuple(seq))
+
+    def rank_fn(comm):
+        ctx = runtime.make_context(comm, n, 1, 0, fuse=True, remap=True)
+        m = ctx.topology.num_local_qubits
+        ctx.partition.amplitudes = psi0[comm.rank << m:(comm.rank + 1) << m]
+        runtime.run_circuit(ctx, circ)
+        moved = ctx.state.counters()[1]
+        full = runtime.gather_group_state(ctx)
+        return full, moved, ctx.layout.is_identity()
+
+    res = runtime.run_spmd(P, rank_fn, timeout=120.0)
+    assert bits_equal(res[0][0], ref)
+    assert all(r[2] for r in res)  # layout restored on read
+
+
+def test_remapped_observables_match_plain():
+    g = golden("golden_cfg1_n12.npz")
+    circ = Circuit(12, tuple(decode(g["gates"])))
+    graph = make_graph(12, [(0, 11), (3, 10), (5, 6)])
+
+    def rank_fn(comm):
+        ctx = runtime.make_context(comm, 12, 1, 0, remap=True)
+        runtime.run_circuit(ctx, circ)
+        probs = [runtime.measure_probability(ctx, q) for q in (0, 9, 10, 11)]
+        return probs, runtime.measure_maxcut(ctx, graph), runtime.measure_norm_squared(ctx)
+
+    out = runtime.run_spmd(4, rank_fn)
+    psi = g["state"]
+    assert out[0][0] == [osv.get_probability(psi, q) for q in (0, 9, 10, 11)]
+    assert out[0][1] == osv.maxcut_expectation(psi, graph.edges)
+    assert out[0][2] == osv.norm_squared(psi)
