@@ -271,6 +271,7 @@ constexpr bool kPingPong = false;
 constexpr bool kPingPong = kGroups > 1;
 #endif
 constexpr int kCtaThreads = kGroups * kTileThreads;
+constexpr int kDepTables = 4;  // tile index up to 32 bits (m <= 44)
 
 // PHASE: the pass has cut-phase gates; GENERIC: it has gates outside the
 // uncontrolled in-order runs (controlled gates, repeated register bits).
@@ -282,6 +283,9 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + kGroups * sizeof(double2) * kTileAmps);
     TilePass* pass_s = reinterpret_cast<TilePass*>(smem_raw + kGroups * sizeof(double2) * kTileAmps +
                                                    sizeof(uint64_t) * (kTileAmps >> 3));
+    // deposit tables: tile index byte c -> its bits spread over the non-tile qubits
+    uint64_t* dep = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(pass_s) +
+                                                sizeof(TilePass));
     {
         // the pass description (rounds, gates, shared matrices) is read once per
         // persistent CTA and then served from shared memory (uniform broadcasts)
@@ -301,6 +305,25 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
             if ((r >> k) & 1) off |= uint64_t(1) << P.tile_bits[low_run + k];
         rowoff[r] = off;
     }
+    {
+        // non-tile qubit positions, ascending: tile index bit b lands on nontile[b]
+        int nontile[64];
+        int cnt = 0;
+        for (int b = 0, k = 0; b < P.m; ++b) {
+            if (k < kTileLog2 && P.tile_bits[k] == b) {
+                ++k;
+                continue;
+            }
+            nontile[cnt++] = b;
+        }
+        for (int i = threadIdx.x; i < kDepTables * 256; i += kCtaThreads) {
+            const int c = i >> 8, v = i & 255;
+            uint64_t out = 0;
+            for (int b = 0; b < 8; ++b)
+                if (((v >> b) & 1) && 8 * c + b < cnt) out |= uint64_t(1) << nontile[8 * c + b];
+            dep[i] = out;
+        }
+    }
     __syncthreads();
 
     const int group = threadIdx.x / kTileThreads;  // warp-uniform
@@ -315,10 +338,11 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
     if (kPingPong && group == 1) named_arrive(3, kCtaThreads);  // group 0 computes first
 
     auto tile_base = [&](uint64_t t) {
-        uint64_t x = t & (P.tiles_per_state - 1);
+        const uint64_t x = t & (P.tiles_per_state - 1);
+        uint64_t out = 0;
 #pragma unroll
-        for (int k = 0; k < kTileLog2; ++k) x = insert0(x, P.tile_bits[k]);
-        return x;
+        for (int c = 0; c < kDepTables; ++c) out |= dep[(c << 8) | ((x >> (8 * c)) & 255)];
+        return out;
     };
     auto prefetch = [&](uint64_t t) {
 #ifndef QSB_NO_GMEM
@@ -550,7 +574,7 @@ void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
 
 size_t tile_smem_bytes() {
     return kGroups * sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3) +
-           sizeof(TilePass);
+           sizeof(TilePass) + sizeof(uint64_t) * 256 * kDepTables;
 }
 
 template <bool PH, bool GE>
