@@ -186,6 +186,20 @@ def make_context(comm: dist.GroupComm | None, num_qubits: int, num_states: int =
                        remap)
 
 
+def reset_state(ctx: RankContext, index: int = 0) -> None:
+    if ctx.is_idle:
+        return
+    ctx.queue.gates, ctx.queue.tables, ctx.queue.size, ctx.queue.edges = [], [], 0, None
+    ctx.queue.touched = set()
+    if ctx.layout is not None:  # a fresh basis state: back to the canonical layout
+        ctx.layout = dist.QubitLayout(ctx.num_qubits, ctx.topology.num_local_qubits)
+    if ctx.partition is not None:
+        sv.init_basis_state(ctx.partition, index)
+    else:
+        _native.call("qs_init_basis", ctx.pool.state.handle, index)
+    ctx.gates_applied = 0
+
+
 def _restore(ctx: RankContext) -> None:
     if ctx.layout is not None and not ctx.layout.is_identity():
         ctx.flush()

@@ -181,3 +181,34 @@ def test_batched_matrices_and_luts_bit_identical_to_scalar():
         assert bits_equal(gates.rotation_batch(kind, th), np.stack([fn(float(t)) for t in th]))
     assert bits_equal(graphs.phase_lut_batch(th, 30),
                       np.stack([graphs.phase_lut(float(t), 30) for t in th]))
+
+
+def test_drop_in_api_surface():
+    """The hot-path names of qpool's modules exist in the shim (reference
+    statevector.py, distribution.py, runtime.py, pool.py, gates.py)."""
+    import paper_2001_10554_b200 as qs
+    expected = {
+        "statevector": ["LocalityError", "StatePartition", "allocate_partition",
+                        "full_state_bytes", "init_basis_state", "init_uniform", "pair_update",
+                        "apply_local_one_qubit_gate", "apply_local_controlled_gate",
+                        "apply_diagonal_phase", "norm_squared", "get_probability",
+                        "z_expectation", "maxcut_expectation", "tree_sum", "combine_pair",
+                        "tree_sum_values"],
+        "distribution": ["DEFAULT_CHUNK_AMPLITUDES", "RankTopology", "rank_and_offset",
+                         "exchange_partner", "GroupComm", "single_rank_comm",
+                         "apply_one_qubit_gate", "apply_controlled_gate", "group_reduce_sum",
+                         "measure_probability", "measure_norm_squared", "measure_maxcut",
+                         "measure_z", "TransportTimeout"],
+        "runtime": ["NormDriftError", "RankContext", "make_context", "reset_state", "apply_gate",
+                    "run_circuit", "run_circuit_pool", "measure_probability", "measure_maxcut",
+                    "measure_z", "gather_group_state", "run_spmd", "simulate_circuit",
+                    "NORM_CHECK_INTERVAL", "NORM_TOL"],
+        "pool": ["PoolLayout", "build_pool"],
+        "gates": ["HADAMARD", "PAULI_X", "PAULI_Y", "PAULI_Z", "IDENTITY", "rx", "ry", "rz",
+                  "is_unitary", "gate_matrix", "FIXED_GATES", "ROTATION_GATES"],
+        "graphs": ["Graph", "make_graph", "triangle"],
+    }
+    for mod, names in expected.items():
+        m = getattr(qs, mod)
+        missing = [n for n in names if not hasattr(m, n)]
+        assert not missing, (mod, missing)
