@@ -267,6 +267,13 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     P.tiles_per_state = uint64_t(1) << (st->m - kTileLog2);
     P.num_tiles = P.tiles_per_state * uint64_t(st->num_states);
     P.rank_offset = uint64_t(st->rank) << st->m;
+    for (int k = 0; k < ct.count; ++k)
+        for (int u = 0; u < 64; ++u)
+            if ((ct.mask[k] >> u) & 1) {
+                const int v = u + ct.shift[k];
+                P.nbr[u] |= uint64_t(1) << v;
+                P.nbr[v] |= uint64_t(1) << u;
+            }
     auto pos_of = [&](int qubit) {
         for (int p = 0; p < kTileLog2; ++p)
             if (P.tile_bits[p] == qubit) return p;

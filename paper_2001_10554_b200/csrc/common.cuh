@@ -114,6 +114,7 @@ struct alignas(16) TilePass {
     uint64_t tiles_per_state;  // 2^(m - kTileLog2)
     uint64_t num_tiles;        // num_states * tiles_per_state
     uint64_t rank_offset;      // rank_index << m (global index of local offset 0)
+    uint64_t nbr[64];          // cut-phase graph: neighbour mask of each vertex (qubit)
     Round rounds[kMaxRounds];
     TileGate gates[kMaxPassGates];
 };

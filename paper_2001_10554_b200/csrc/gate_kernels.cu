@@ -135,6 +135,8 @@ constexpr int kLoadsPerThread = kTileAmps / kTileThreads;
 
 static_assert(kRegLog2 >= 3 && kRegLog2 <= 5, "register paths cover 3..5 register qubits");
 
+__host__ __device__ constexpr int ctz_c(int x) { return (x & 1) ? 0 : 1 + ctz_c(x >> 1); }
+
 // 2x2 update on register bit J of the 16 amplitudes a thread holds.  C < 0:
 // uncontrolled; C >= 0: only pairs whose register bit C is 1.  Both are
 // compile-time, so the 8 (or 4) pair updates form one basic block the
@@ -403,12 +405,24 @@ __global__ void __launch_bounds__(kCtaThreads, 1)
                     if (PHASE && G.kind == QS_KIND_CUTPHASE) {
                         const double2* lut =
                             reinterpret_cast<const double2*>(mats + G.offset + s * G.stride);
+                        // cut of the k=0 amplitude in full, then walk the 16 register
+                        // indices in Gray-code order: flipping qubit r changes the cut
+                        // by deg(r) - 2 * (edges of r currently cut)
+                        uint64_t i = P.rank_offset | (base_local + rowoff[eb >> low_run] +
+                                                      (uint64_t(eb) & lowmask));
+                        int cut = cut_of(i, ct);
+                        a[0] = cmul(a[0], __ldg(lut + cut));
 #pragma unroll
-                        for (int k = 0; k < kRegAmps; ++k) {
-                            const int e = eb | R.dk[k];
-                            uint64_t local =
-                                base_local + rowoff[e >> low_run] + (uint64_t(e) & lowmask);
-                            a[k] = cmul(a[k], __ldg(lut + cut_of(P.rank_offset | local, ct)));
+                        for (int step = 1; step < kRegAmps; ++step) {
+                            const int j = ctz_c(step);           // bit flipped by Gray step
+                            const int gray = step ^ (step >> 1);  // register index reached
+                            const int r = P.tile_bits[__ffs(R.dk[1 << j]) - 1];
+                            const uint64_t nb = P.nbr[r];
+                            const uint64_t bitr = (i >> r) & 1;
+                            const int now_cut = __popcll((i ^ (uint64_t(0) - bitr)) & nb);
+                            cut += __popcll(nb) - 2 * now_cut;
+                            i ^= uint64_t(1) << r;
+                            a[gray] = cmul(a[gray], __ldg(lut + cut));
                         }
                         continue;
                     }
