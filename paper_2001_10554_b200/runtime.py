@@ -246,10 +246,13 @@ def _apply_gate_remapped(ctx: RankContext, gate) -> None:
 
 def _swap_in(ctx: RankContext, qubit: int, protected=()) -> None:
     """Swap logical `qubit` (on a rank bit) into a local position: flush the
-    queue, then evict the most recently used local position (in sweeps and
-    layered circuits that qubit is needed last).  Half the slice crosses to the
-    partner (k_swap_peer) instead of the whole slice of a pair exchange, and the
-    gate itself then runs locally and fuses with its successors."""
+    queue, then evict the most recently used local position.  Repeated sweeps
+    and layered circuits touch qubits cyclically, where the most recently used
+    qubit is the one needed last (MRU is the optimal eviction for cyclic use).
+    Half the slice crosses to the partner (k_swap_peer) instead of the whole
+    slice of a pair exchange, and the gate itself then runs locally and fuses
+    with the gates that follow.  (Swapping into an untouched slot without a
+    flush was measured to double the swaps in sweeps, tools/exp/remap_policy.py.)"""
     L, m = ctx.layout, ctx.topology.num_local_qubits
     ctx.flush()
     p = L.phys[qubit]
