@@ -136,6 +136,11 @@ int qs_last_program_passes(const qs_state* st, int32_t* passes);
 int qs_observable(qs_state* st, int32_t kind, int32_t q, const int32_t* edges,
                   int32_t num_edges, double* out);
 
+/* All per-qubit probabilities P(q=1), q < n, of every state in one pass
+ * (cmd_run's report, cli.py:161-172); out has num_states*n doubles, each
+ * bit-identical to qs_observable(QS_OBS_PROB, q). */
+int qs_marginals(qs_state* st, double* out);
+
 /* ---- global-qubit path: distribution.py:121-230 ----------------------- */
 /* Pairwise exchange gate for a target on a global qubit, computed in one
  * kernel over NVLink peer memory: this rank updates half of the pairs it

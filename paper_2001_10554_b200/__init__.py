@@ -21,7 +21,7 @@ from .distribution import (RankTopology, rank_and_offset, exchange_partner, sing
                            ThreadFabric, TorchComm, apply_one_qubit_gate, apply_controlled_gate,
                            group_reduce_sum, TransportTimeout)
 from .runtime import (NormDriftError, make_context, run_circuit, run_circuit_pool, apply_gate,
-                      measure_probability, measure_maxcut, measure_z, measure_norm_squared,
+                      measure_probability, measure_probabilities, measure_maxcut, measure_z, measure_norm_squared,
                       gather_group_state, run_spmd, simulate_circuit, PoolState)
 from .pool import build_pool, PoolLayout
 

@@ -27,7 +27,7 @@ EXPORTS = (
     "qs_synchronize", "qs_state_upload", "qs_state_download",
     "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
     "qs_apply_1q", "qs_apply_controlled", "qs_apply_cut_phase", "qs_apply_program",
-    "qs_plan_program", "qs_last_program_passes", "qs_observable",
+    "qs_plan_program", "qs_last_program_passes", "qs_observable", "qs_marginals",
     "qs_exchange_gate_peer", "qs_exchange_gate_nccl", "qs_swap_qubits_peer",
     "qs_swap_qubits_local", "qs_state_ipc_handle", "qs_peer_open",
     "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
@@ -90,6 +90,7 @@ _SIGNATURES = {
     "qs_plan_program": ([_I, ctypes.POINTER(QsGate), _I, _I, _IP, _I, _IP], ctypes.c_int),
     "qs_last_program_passes": ([_P, _IP], ctypes.c_int),
     "qs_observable": ([_P, _I, _I, _IP, _I, _DP], ctypes.c_int),
+    "qs_marginals": ([_P, _DP], ctypes.c_int),
     "qs_exchange_gate_peer": ([_P, _P, _I, _DP, _I], ctypes.c_int),
     "qs_exchange_gate_nccl": ([_P, _I, _I, _DP, _I, _U], ctypes.c_int),
     "qs_swap_qubits_peer": ([_P, _P, _I, _I], ctypes.c_int),
@@ -265,6 +266,12 @@ class DeviceState:
             e = np.zeros(2, dtype=np.int32)
         call("qs_observable", self.handle, kind, q, iptr(e), ne, dptr(out))
         return out
+
+    def marginals(self) -> np.ndarray:
+        """[num_states, n] probabilities P(q=1) in one pass (qs_marginals)."""
+        out = np.empty(self.num_states * self.num_qubits, dtype=np.float64)
+        call("qs_marginals", self.handle, dptr(out))
+        return out.reshape(self.num_states, self.num_qubits)
 
     def launch_log(self, enable: bool) -> None:
         call("qs_launch_log", self.handle, 1 if enable else 0)

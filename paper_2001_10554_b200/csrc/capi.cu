@@ -809,6 +809,53 @@ int qs_observable(qs_state* st, int32_t kind, int32_t q, const int32_t* edges, i
     return QS_OK;
 }
 
+// All per-qubit probabilities P(q=1) of every state in one pass over the slice
+// (cmd_run's "prob q" report, cli.py:161-172): out[num_states * n], each value
+// identical to qs_observable(QS_OBS_PROB, q).
+int qs_marginals(qs_state* st, double* out) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (int rc = ensure_device(st)) return rc;
+    const int n = st->n, m = st->m, S = st->num_states;
+    if (m < 12) {  // small slices: one reduction per qubit
+        std::vector<double> tmp(S);
+        for (int q = 0; q < n; ++q) {
+            if (int rc = qs_observable(st, QS_OBS_PROB, q, nullptr, 0, tmp.data())) return rc;
+            for (int s = 0; s < S; ++s) out[size_t(s) * n + q] = tmp[s];
+        }
+        return QS_OK;
+    }
+    size_t need = marginal_scratch_doubles(m, S) + size_t(S) * m + size_t(S);
+    if (int rc = grow(&st->d_scratch, &st->scratch_cap, need)) return rc;
+    double* dev_out = st->d_scratch + marginal_scratch_doubles(m, S);
+    {
+        LaunchScope ls(st, kLaunchReduce);
+        launch_marginals(st->psi, m, S, st->d_scratch, dev_out, st->stream);
+    }
+    CHECK_LAUNCH();
+    std::vector<double> local(size_t(S) * m);
+    CUDA_TRY(cudaMemcpyAsync(local.data(), dev_out, sizeof(double) * local.size(),
+                             cudaMemcpyDeviceToHost, st->stream));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    std::vector<double> norms;
+    if (n > m) {  // global qubits: the whole slice or nothing (statevector.py:225-228)
+        norms.resize(S);
+        if (int rc = qs_observable(st, QS_OBS_NORM, 0, nullptr, 0, norms.data())) return rc;
+    }
+    for (int s = 0; s < S; ++s)
+        for (int q = 0; q < n; ++q) {
+            double v;
+            if (q < m) {
+                // device layout: [S][11] for q < 11, then [S][m-11] for q >= 11
+                v = q < 11 ? local[size_t(s) * 11 + q]
+                           : local[size_t(S) * 11 + size_t(s) * (m - 11) + (q - 11)];
+            } else {
+                v = ((st->rank >> (q - m)) & 1) ? norms[s] : 0.0;
+            }
+            out[size_t(s) * n + q] = v;
+        }
+    return QS_OK;
+}
+
 // ---- global-qubit path --------------------------------------------------------
 int qs_exchange_gate_peer(qs_state* st, void* peer_amps, int32_t is_lower, const double* u,
                           int32_t control_local) {

@@ -141,6 +141,10 @@ void launch_observable(const double2* psi, int m, int num_states, int kind, int 
                        uint64_t rank_offset, const CutTerms& ct, double* scratch, double* out_dev,
                        cudaStream_t s);
 
+uint64_t marginal_scratch_doubles(int m, int num_states);
+void launch_marginals(const double2* psi, int m, int num_states, double* scratch, double* out_dev,
+                      cudaStream_t s);
+
 void launch_exchange_peer(double2* mine, double2* peer, int m, bool is_lower, const double* u_dev,
                           int control_local, cudaStream_t s);
 void launch_swap_peer(double2* mine, double2* peer, int m, int l, int rank_bit, cudaStream_t s);

@@ -117,6 +117,69 @@ __global__ void __launch_bounds__(kThreads)
     }
 }
 
+// All marginals P(q=1), q < m, in one pass (states with m >= 11).  A block
+// builds the full tree of one aligned 2048-amplitude chunk in shared memory
+// (levels 0..11).  For q < 11 the amplitudes with bit q set form the odd nodes
+// of level q, so their tree inside the chunk is a tree over those nodes; for
+// q >= 11 the chunk is either wholly selected (its root) or not at all.  The
+// per-chunk partials are aligned subtrees of each q's selected list, so the
+// second level (k_tree over partials) reproduces get_probability's tree_sum.
+constexpr int kMargChunkLog2 = 11;
+__global__ void __launch_bounds__(kThreads)
+    k_marginals(const double2* __restrict__ psi, int m, uint64_t total_chunks,
+                double* __restrict__ low_out, double* __restrict__ high_out) {
+    __shared__ double lev[2 << kMargChunkLog2];                // levels 0..11
+    __shared__ double tmp[(1 << kMargChunkLog2) - 1];          // odd-node trees, q = 0..10
+    const int chunk = 1 << kMargChunkLog2;
+    const uint64_t cps = uint64_t(1) << (m - kMargChunkLog2);  // chunks per state
+    const int nlow = kMargChunkLog2;                           // q < 11
+    const int nhigh = m - kMargChunkLog2;                      // 11 <= q < m
+    for (uint64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
+        const uint64_t st = c / cps, cl = c - st * cps;
+        const double2* src = psi + (st << m) + (cl << kMargChunkLog2);
+        for (int i = threadIdx.x; i < chunk; i += kThreads) lev[i] = abs2(src[i]);
+        __syncthreads();
+        // level l lives at offset (2^12 - 2^(12-l)), size 2^(11-l)
+        for (int l = 1; l <= kMargChunkLog2; ++l) {
+            const int in = (2 << kMargChunkLog2) - (2 << (kMargChunkLog2 - l + 1));
+            const int out = (2 << kMargChunkLog2) - (2 << (kMargChunkLog2 - l));
+            for (int i = threadIdx.x; i < (chunk >> l); i += kThreads)
+                lev[out + i] = __dadd_rn(lev[in + 2 * i], lev[in + 2 * i + 1]);
+            __syncthreads();
+        }
+        // odd nodes of level q -> tmp segment of q (size 2^(10-q)), then trees
+        for (int q = 0; q < nlow; ++q) {
+            const int lvl = (2 << kMargChunkLog2) - (2 << (kMargChunkLog2 - q));
+            const int cnt = chunk >> (q + 1);
+            const int seg = chunk - (chunk >> q);  // sum of earlier segment sizes
+            for (int i = threadIdx.x; i < cnt; i += kThreads) tmp[seg + i] = lev[lvl + 2 * i + 1];
+        }
+        __syncthreads();
+        for (int w = 1; w < (chunk >> 1); w <<= 1) {
+            for (int q = 0; q < nlow; ++q) {
+                const int cnt = chunk >> (q + 1);
+                const int seg = chunk - (chunk >> q);
+                for (int i = threadIdx.x; i * 2 * w < cnt; i += kThreads)
+                    if (i * 2 * w + w < cnt)
+                        tmp[seg + i * 2 * w] = __dadd_rn(tmp[seg + i * 2 * w], tmp[seg + i * 2 * w + w]);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x < nlow) {
+            const int q = threadIdx.x;
+            low_out[(st * nlow + q) * cps + cl] = tmp[chunk - (chunk >> q)];
+        }
+        if (threadIdx.x >= 32 && threadIdx.x < 32 + nhigh) {
+            const int h = threadIdx.x - 32;  // q = 11 + h
+            if ((cl >> h) & 1) {
+                const uint64_t idx = ((cl >> (h + 1)) << h) | (cl & ((uint64_t(1) << h) - 1));
+                high_out[(st * nhigh + h) * (cps >> 1) + idx] = lev[(2 << kMargChunkLog2) - 2];
+            }
+        }
+        __syncthreads();
+    }
+}
+
 inline unsigned grid_cap(uint64_t n) {
     uint64_t cap = 148ull * 16;
     return unsigned(n < cap ? (n ? n : 1) : cap);
@@ -128,6 +191,59 @@ uint64_t reduce_scratch_doubles(int m, int num_states) {
     uint64_t per_state = uint64_t(1) << m;
     uint64_t first = (per_state + kChunk - 1) / kChunk;
     return 2 * (first * uint64_t(num_states) + 1);
+}
+
+// Reduce `lists` lists of `len` partials (power of two, contiguous) to one value
+// each, with the same tree: level after level of k_tree over partials.
+void tree_lists(const double* src, double* scratch_a, double* scratch_b, uint64_t len,
+                uint64_t lists, double* out, cudaStream_t s) {
+    CutTerms ct;
+    ct.count = 0;
+    const double* cur = src;
+    int level = 0;
+    while (true) {
+        int lg = 0;
+        while ((uint64_t(1) << lg) < len) ++lg;
+        const bool wide = lg >= kWideLog2;
+        const int chunk_log2 = wide ? kWideLog2 : lg;
+        const uint64_t per = len >> chunk_log2;
+        const uint64_t total = per * lists;
+        double* dst = per == 1 ? out : (level & 1 ? scratch_b : scratch_a);
+        if (wide)
+            k_tree_wide<<<grid_cap(total), kThreads, 0, s>>>(nullptr, cur, dst, 0, 0, 0, 0, ct, len,
+                                                             total);
+        else
+            k_tree<<<grid_cap(total), kThreads, 0, s>>>(nullptr, cur, dst, 0, 0, 0, 0, ct, len,
+                                                        chunk_log2, total);
+        if (per == 1) break;
+        cur = dst;
+        len = per;
+        ++level;
+    }
+}
+
+uint64_t marginal_scratch_doubles(int m, int num_states) {
+    const uint64_t cps = uint64_t(1) << (m - kMargChunkLog2);
+    const uint64_t partials = uint64_t(num_states) * uint64_t(m) * cps;
+    return 3 * partials + 2 * uint64_t(num_states) * m + 16;
+}
+
+// out_dev: [num_states][m] marginals of the local qubits (m >= 12)
+void launch_marginals(const double2* psi, int m, int num_states, double* scratch, double* out_dev,
+                      cudaStream_t s) {
+    const uint64_t cps = uint64_t(1) << (m - kMargChunkLog2);
+    const int nlow = kMargChunkLog2, nhigh = m - kMargChunkLog2;
+    const uint64_t S = uint64_t(num_states);
+    double* low = scratch;                                     // [S][11][cps]
+    double* high = low + S * nlow * cps;                       // [S][nhigh][cps/2]
+    double* sa = high + S * nhigh * (cps >> 1) + 8;
+    double* sb = sa + S * uint64_t(m) * cps;
+    double* low_res = out_dev;                                 // [S][11] then [S][nhigh]
+    double* high_res = out_dev + S * nlow;
+    const uint64_t total = S * cps;
+    k_marginals<<<grid_cap(total), kThreads, 0, s>>>(psi, m, total, low, high);
+    tree_lists(low, sa, sb, cps, S * nlow, low_res, s);
+    if (nhigh > 0) tree_lists(high, sa, sb, cps >> 1, S * nhigh, high_res, s);
 }
 
 void launch_observable(const double2* psi, int m, int num_states, int kind, int q,

@@ -52,6 +52,9 @@ class QubitRegister:
             return fn(float(a))
         if a.shape != (self.num_states,):
             raise ValueError(f"expected {self.num_states} angles")
+        kind = {G.rx: "rx", G.ry: "ry", G.rz: "rz"}.get(fn)
+        if kind is not None:
+            return G.rotation_batch(kind, a)
         return np.stack([fn(float(x)) for x in a])
 
     # ---- one-qubit gates -----------------------------------------------------------
@@ -111,6 +114,12 @@ class QubitRegister:
 
     def GetProbability(self, q: int):
         return self._obs(_native.QS_OBS_PROB, self._q(q))
+
+    def GetProbabilities(self):
+        """P(q=1) for every qubit, one pass over the state."""
+        self.queue.flush()
+        v = self.state.marginals()
+        return v[0] if self.num_states == 1 else v
 
     def ExpectationValueZ(self, q: int):
         return self._obs(_native.QS_OBS_Z, self._q(q))

@@ -341,6 +341,21 @@ def measure_probability(ctx: RankContext, q: int):
     return _group_reduce(ctx, sv.get_probability(ctx.partition, q))
 
 
+def measure_probabilities(ctx: RankContext) -> np.ndarray:
+    """P(q=1) for every qubit in one pass over the slice (qs_marginals); each
+    value equals measure_probability(ctx, q).  Pools: [num_states, n]."""
+    if ctx.is_idle:
+        return np.zeros(ctx.num_qubits)
+    _restore(ctx)
+    ctx.flush()
+    if ctx.pool is not None:
+        return ctx.pool.state.marginals()
+    if ctx.partition is not None:
+        ctx.partition.sync_in()
+    partial = ctx.state.marginals()[0]
+    return np.array([_group_reduce(ctx, float(v)) for v in partial])
+
+
 def measure_z(ctx: RankContext, q: int):
     if ctx.is_idle:
         return 0.0

@@ -557,3 +557,33 @@ def test_remapped_observables_match_plain():
     assert out[0][0] == [osv.get_probability(psi, q) for q in (0, 9, 10, 11)]
     assert out[0][1] == osv.maxcut_expectation(psi, graph.edges)
     assert out[0][2] == osv.norm_squared(psi)
+
+
+@pytest.mark.parametrize("n,m,rank,S", [(20, 20, 0, 1), (14, 12, 3, 1), (13, 13, 0, 5), (10, 10, 0, 2)])
+def test_marginals_one_pass_bit_identical(n, m, rank, S):
+    from paper_2001_10554_b200 import _native as N
+    rng = np.random.default_rng(n + m + rank)
+    st = N.DeviceState(n, m, rank, S)
+    st.upload(np.concatenate([ogates.random_state(m, rng) for _ in range(S)]))
+    marg = st.marginals()
+    host = st.download().reshape(S, -1)
+    for s in range(S):
+        for q in range(n):
+            assert marg[s, q] == st.observable(N.QS_OBS_PROB, q)[s]
+            assert marg[s, q] == osv.get_probability(host[s], q, n=n, rank=rank)
+
+
+def test_measure_probabilities_matches_reference_report():
+    g = golden("golden_cfg1_n20.npz")
+    circ = Circuit(20, tuple(decode(g["gates"])))
+    ctx = runtime.make_context(None, 20)
+    runtime.run_circuit(ctx, circ)
+    assert list(runtime.measure_probabilities(ctx)) == list(g["probs"])
+
+    def rank_fn(comm):
+        c = runtime.make_context(comm, 20, 1, 0)
+        runtime.run_circuit(c, circ)
+        return runtime.measure_probabilities(c)
+
+    out = runtime.run_spmd(4, rank_fn)
+    assert list(out[0]) == list(g["probs"])
