@@ -321,7 +321,7 @@ def run_ours(args):
 
     # e2e through the public API with host buffers (upload + sweep + download)
     if m <= 31:
-        e2e = run_e2e(args, ctx, st, sweeps, step, m, n, dist)
+        e2e = run_e2e(args, ctx, st, sweeps, step, m, n, dist, gates_per_step)
     else:
         e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                "note": f"skipped: a 2^{m}-amplitude pinned host copy does not fit beside the "
@@ -413,27 +413,30 @@ def per_target_table(st, m, seed):
             "min_frac_of_8tbs": min(r["frac_of_8tbs"] for r in rows)}
 
 
-def run_e2e(args, ctx, st, sweeps, step, m, n, dist):
-    """Same metric through the public API with host (pinned) buffers: every step
-    uploads the state, runs the sweep and downloads the result."""
+def run_e2e(args, ctx, st, sweeps, step, m, n, dist, gates_per_step):
+    """Same metric through the public API with pinned host buffers: every step
+    uploads the state (StatePartition.amplitudes = host), runs the gates
+    (runtime.apply_gate) and reads the result back (read_amplitudes)."""
     import torch
+
+    from paper_2001_10554_b200 import statevector as sv
 
     k = max(1, args.e2e_steps)
     host = torch.empty(2 << m, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
-    st.download(host)
-    st.synchronize()
+    sv.read_amplitudes(ctx.partition, host)
     barrier(dist)
     t0 = time.perf_counter()
     for s in range(k):
-        st.upload(host)
+        ctx.partition.amplitudes = host
         step(sweeps[s % len(sweeps)])
-        st.download(host)
+        sv.read_amplitudes(ctx.partition, host)
     dt = time.perf_counter() - t0
     dt = max_over_ranks(dist, dt)
-    units = n * (2.0 ** n) / 2.0 ** 30
+    units = gates_per_step * (2.0 ** n) / 2.0 ** 30
     return {"value": units * k / dt, "unit": UNIT, "h2d_bytes_per_step": 16 * (2 ** m),
             "d2h_bytes_per_step": 16 * (2 ** m), "steps": k,
-            "note": "per GPU bytes; wall clock around upload + sweep + download"}
+            "note": "per GPU bytes; wall clock around upload + gates + download, public API "
+                    "(StatePartition.amplitudes setter, runtime.apply_gate, read_amplitudes)"}
 
 
 QAOA_N, QAOA_P, QAOA_POOL = 20, 4, 512

@@ -20,7 +20,7 @@ from ._native import LocalityError, DeviceState
 from .graphs import edge_array, phase_lut
 
 __all__ = [
-    "LocalityError", "StatePartition", "allocate_partition", "full_state_bytes",
+    "LocalityError", "StatePartition", "allocate_partition", "full_state_bytes", "read_amplitudes",
     "init_basis_state", "init_uniform", "pair_update", "apply_local_one_qubit_gate",
     "apply_local_controlled_gate", "apply_diagonal_phase", "apply_cut_phase", "CutPhase",
     "norm_squared", "get_probability", "z_expectation", "maxcut_expectation",
@@ -133,6 +133,13 @@ class StatePartition:
         return (f"StatePartition(num_qubits={self.num_qubits}, "
                 f"num_local_qubits={self.num_local_qubits}, rank_index={self.rank_index}, "
                 f"device={self.device})")
+
+
+def read_amplitudes(partition: StatePartition, out: np.ndarray | None = None) -> np.ndarray:
+    """Copy the slice into `out` (e.g. a pinned host buffer) or a new array;
+    unlike ``.amplitudes`` no host mirror is kept."""
+    st = partition.sync_in()
+    return st.download(out)
 
 
 def allocate_partition(num_qubits: int, num_local_qubits: int | None = None,
