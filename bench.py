@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--workload", default="sweep", choices=["sweep", "qaoa", "cfg4"])
     ap.add_argument("--seed", type=int, default=20260809)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--no-per-target", action="store_true")
@@ -422,21 +422,28 @@ def run_e2e(args, ctx, st, sweeps, step, m, n, dist, gates_per_step):
     from paper_2001_10554_b200 import statevector as sv
 
     k = max(1, args.e2e_steps)
-    host = torch.empty(2 << m, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
-    sv.read_amplitudes(ctx.partition, host)
+    host_in = torch.empty(2 << m, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+    host_out = torch.empty(2 << m, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+    sv.read_amplitudes(ctx.partition, host_in)
     barrier(dist)
     t0 = time.perf_counter()
+    ctx.partition.amplitudes = host_in                      # step 0 input
     for s in range(k):
-        ctx.partition.amplitudes = host
         step(sweeps[s % len(sweeps)])
-        sv.read_amplitudes(ctx.partition, host)
+        if s + 1 < k:
+            # step s result out while step s+1 input comes in (full duplex)
+            sv.exchange_amplitudes(ctx.partition, host_in, host_out)
+        else:
+            sv.read_amplitudes(ctx.partition, host_out)
     dt = time.perf_counter() - t0
     dt = max_over_ranks(dist, dt)
     units = gates_per_step * (2.0 ** n) / 2.0 ** 30
     return {"value": units * k / dt, "unit": UNIT, "h2d_bytes_per_step": 16 * (2 ** m),
             "d2h_bytes_per_step": 16 * (2 ** m), "steps": k,
-            "note": "per GPU bytes; wall clock around upload + gates + download, public API "
-                    "(StatePartition.amplitudes setter, runtime.apply_gate, read_amplitudes)"}
+            "note": "per GPU bytes; wall clock around every step's input upload, gates and "
+                    "result download through the public API (amplitudes setter / "
+                    "exchange_amplitudes, runtime.apply_gate, read_amplitudes); a step's "
+                    "download and the next step's upload share one full-duplex transfer"}
 
 
 QAOA_N, QAOA_P, QAOA_POOL = 20, 4, 512

@@ -95,6 +95,13 @@ int qs_synchronize(qs_state* st);
 int qs_state_upload(qs_state* st, const double* host, uint64_t offset, uint64_t count);
 int qs_state_download(qs_state* st, double* host, uint64_t offset, uint64_t count);
 
+/* Step boundary for streamed workloads: download the whole handle into
+ * host_out while uploading host_in in its place, pipelined in `chunk`-
+ * amplitude pieces on two streams (full-duplex PCIe).  Both host buffers
+ * should be pinned and must not alias. */
+int qs_state_exchange_host(qs_state* st, const double* host_in, double* host_out,
+                           uint64_t chunk);
+
 /* ---- initialisation: statevector.py:123-141 --------------------------- */
 int qs_init_zero(qs_state* st);
 int qs_init_basis(qs_state* st, uint64_t global_index);            /* init_basis_state */

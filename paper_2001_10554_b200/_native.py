@@ -24,7 +24,7 @@ QS_OBS_NORM, QS_OBS_PROB, QS_OBS_Z, QS_OBS_MAXCUT = 0, 1, 2, 3
 EXPORTS = (
     "qs_abi_version", "qs_last_error", "qs_device_count", "qs_counters",
     "qs_state_create", "qs_state_destroy", "qs_state_info", "qs_state_device_ptr",
-    "qs_synchronize", "qs_state_upload", "qs_state_download",
+    "qs_synchronize", "qs_state_upload", "qs_state_download", "qs_state_exchange_host",
     "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
     "qs_apply_1q", "qs_apply_controlled", "qs_apply_cut_phase", "qs_apply_program",
     "qs_plan_program", "qs_last_program_passes", "qs_observable", "qs_marginals",
@@ -78,6 +78,7 @@ _SIGNATURES = {
     "qs_synchronize": ([_P], ctypes.c_int),
     "qs_state_upload": ([_P, _DP, _U, _U], ctypes.c_int),
     "qs_state_download": ([_P, _DP, _U, _U], ctypes.c_int),
+    "qs_state_exchange_host": ([_P, _DP, _DP, _U], ctypes.c_int),
     "qs_init_zero": ([_P], ctypes.c_int),
     "qs_init_basis": ([_P, _U], ctypes.c_int),
     "qs_init_constant": ([_P, _D, _D], ctypes.c_int),
@@ -223,6 +224,10 @@ class DeviceState:
             out = np.empty(count, dtype=np.complex128)
         call("qs_state_download", self.handle, dptr(out), offset, count)
         return out
+
+    def exchange_host(self, host_in: np.ndarray, host_out: np.ndarray, chunk: int = 1 << 24) -> None:
+        """Download into host_out while uploading host_in (full duplex, chunked)."""
+        call("qs_state_exchange_host", self.handle, dptr(host_in), dptr(host_out), chunk)
 
     def synchronize(self) -> None:
         call("qs_synchronize", self.handle)

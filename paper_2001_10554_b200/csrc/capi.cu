@@ -629,6 +629,43 @@ int qs_state_download(qs_state* st, double* host, uint64_t offset, uint64_t coun
     return QS_OK;
 }
 
+// Full-duplex step boundary: read the whole slice into host_out while the
+// next input streams in from host_in, chunk by chunk -- D2H of chunk i+1 runs
+// on the comm stream while H2D of chunk i runs on the compute stream (PCIe is
+// full duplex).  Chunk i is overwritten only after its own D2H completed.
+int qs_state_exchange_host(qs_state* st, const double* host_in, double* host_out,
+                           uint64_t chunk) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (int rc = ensure_device(st)) return rc;
+    const uint64_t total = st->amps_per_state * uint64_t(st->num_states);
+    if (chunk == 0) chunk = uint64_t(1) << 24;
+    cudaEvent_t start, done;
+    CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(start, st->stream));
+    CUDA_TRY(cudaStreamWaitEvent(st->comm_stream, start, 0));
+    std::vector<cudaEvent_t> evs;
+    for (uint64_t off = 0; off < total; off += chunk) {
+        const uint64_t len = std::min(chunk, total - off);
+        CUDA_TRY(cudaMemcpyAsync(host_out + 2 * off, st->psi + off, len * sizeof(double2),
+                                 cudaMemcpyDeviceToHost, st->comm_stream));
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(ev, st->comm_stream));
+        evs.push_back(ev);
+        CUDA_TRY(cudaStreamWaitEvent(st->stream, ev, 0));
+        CUDA_TRY(cudaMemcpyAsync(st->psi + off, host_in + 2 * off, len * sizeof(double2),
+                                 cudaMemcpyHostToDevice, st->stream));
+    }
+    CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(done, st->comm_stream));
+    CUDA_TRY(cudaStreamWaitEvent(st->stream, done, 0));
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    for (auto e : evs) cudaEventDestroy(e);
+    cudaEventDestroy(start);
+    cudaEventDestroy(done);
+    return QS_OK;
+}
+
 int qs_init_zero(qs_state* st) {
     if (int rc = ensure_device(st)) return rc;
     CUDA_TRY(cudaMemsetAsync(st->psi, 0,

@@ -21,6 +21,7 @@ from .graphs import edge_array, phase_lut
 
 __all__ = [
     "LocalityError", "StatePartition", "allocate_partition", "full_state_bytes", "read_amplitudes",
+    "exchange_amplitudes",
     "init_basis_state", "init_uniform", "pair_update", "apply_local_one_qubit_gate",
     "apply_local_controlled_gate", "apply_diagonal_phase", "apply_cut_phase", "CutPhase",
     "norm_squared", "get_probability", "z_expectation", "maxcut_expectation",
@@ -140,6 +141,15 @@ def read_amplitudes(partition: StatePartition, out: np.ndarray | None = None) ->
     unlike ``.amplitudes`` no host mirror is kept."""
     st = partition.sync_in()
     return st.download(out)
+
+
+def exchange_amplitudes(partition: StatePartition, new: np.ndarray, out: np.ndarray) -> None:
+    """Read the slice into `out` while `new` replaces it -- one full-duplex,
+    chunked transfer (pinned buffers recommended; they must not alias)."""
+    partition.sync_in()
+    if new.shape != (1 << partition.num_local_qubits,) or out.shape != new.shape:
+        raise ValueError("amplitude buffers have the wrong length")
+    partition.state.exchange_host(np.ascontiguousarray(new, dtype=np.complex128), out)
 
 
 def allocate_partition(num_qubits: int, num_local_qubits: int | None = None,

@@ -587,3 +587,16 @@ def test_measure_probabilities_matches_reference_report():
 
     out = runtime.run_spmd(4, rank_fn)
     assert list(out[0]) == list(g["probs"])
+
+
+def test_exchange_amplitudes_full_duplex():
+    rng = np.random.default_rng(12)
+    n = 16
+    a, b = ogates.random_state(n, rng), ogates.random_state(n, rng)
+    p = sv.StatePartition(n, n, 0, a.copy())
+    out = np.empty_like(a)
+    p.state.exchange_host(b, out, chunk=1000)  # ragged last chunk
+    assert bits_equal(out, a)
+    assert bits_equal(sv.read_amplitudes(p), b)
+    sv.exchange_amplitudes(p, a, out)
+    assert bits_equal(out, b) and bits_equal(p.amplitudes, a)
