@@ -277,8 +277,11 @@ constexpr int kDepTables = 4;  // tile index up to 32 bits (m <= 44)
 
 // PHASE: the pass has cut-phase gates; GENERIC: it has gates outside the
 // uncontrolled in-order runs (controlled gates, repeated register bits).
+#ifndef QSB_TILE_MINB
+#define QSB_TILE_MINB 1
+#endif
 template <bool PHASE, bool GENERIC>
-__global__ void __launch_bounds__(kCtaThreads, 1)
+__global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
     k_tile(double2* __restrict__ psi, const TilePass* __restrict__ pass_dev,
            const double* __restrict__ mats, const __grid_constant__ CutTerms ct) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
