@@ -148,6 +148,16 @@ int qs_observable(qs_state* st, int32_t kind, int32_t q, const int32_t* edges,
  * bit-identical to qs_observable(QS_OBS_PROB, q). */
 int qs_marginals(qs_state* st, double* out);
 
+/* ---- host parameter preparation: noise trajectories (noise.py:70-80) ----
+ * out[s] = a[s] @ b[s] for `count` complex128 2x2 matrices (row-major,
+ * interleaved re/im).  Each entry is the FMA chain
+ *   re = fma(-ai1,bi1, fma(ar1,br1, fma(-ai0,bi0, fma(ar0,br0, 0))))
+ *   im = fma( ai1,br1, fma(ar1,bi1, fma( ai0,br0, fma(ar0,bi0, 0))))
+ * -- the association numpy's `@` (OpenBLAS zgemm) used when the reference's
+ * golden noise trajectories were generated -- so noise matrices, and the
+ * noisy states built from them, are bit-identical on any host.  Host-only. */
+int qs_compose_2x2(const double* a, const double* b, int64_t count, double* out);
+
 /* ---- global-qubit path: distribution.py:121-230 ----------------------- */
 /* Pairwise exchange gate for a target on a global qubit, computed in one
  * kernel over NVLink peer memory: this rank updates half of the pairs it

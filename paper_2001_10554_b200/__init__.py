@@ -10,7 +10,7 @@ from __future__ import annotations
 
 from . import _native
 from ._native import LocalityError, TransportError, device_count
-from . import gates, graphs, statevector, distribution, runtime, circuit, pool  # noqa: E402
+from . import gates, graphs, statevector, distribution, runtime, circuit, pool, noise  # noqa: E402
 from .register import QubitRegister
 from .statevector import (StatePartition, allocate_partition, full_state_bytes, init_basis_state,
                           init_uniform, apply_local_one_qubit_gate, apply_local_controlled_gate,
@@ -22,7 +22,9 @@ from .distribution import (RankTopology, rank_and_offset, exchange_partner, sing
                            group_reduce_sum, TransportTimeout)
 from .runtime import (NormDriftError, make_context, run_circuit, run_circuit_pool, apply_gate,
                       measure_probability, measure_probabilities, measure_maxcut, measure_z, measure_norm_squared,
-                      gather_group_state, run_spmd, simulate_circuit, PoolState)
+                      gather_group_state, run_spmd, simulate_circuit, PoolState,
+                      run_noise_ensemble, noise_ensemble_csv)
+from .noise import NoiseModel, NOISELESS, schedule_noise, trajectory_stream
 from .pool import build_pool, PoolLayout
 
 __version__ = "0.1.0"

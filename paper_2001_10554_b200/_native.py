@@ -32,6 +32,7 @@ EXPORTS = (
     "qs_swap_qubits_local", "qs_state_ipc_handle", "qs_peer_open",
     "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
     "qs_event_record", "qs_event_elapsed_ms", "qs_launch_log", "qs_launch_log_read",
+    "qs_compose_2x2",
 )
 
 
@@ -92,6 +93,7 @@ _SIGNATURES = {
     "qs_last_program_passes": ([_P, _IP], ctypes.c_int),
     "qs_observable": ([_P, _I, _I, _IP, _I, _DP], ctypes.c_int),
     "qs_marginals": ([_P, _DP], ctypes.c_int),
+    "qs_compose_2x2": ([_DP, _DP, ctypes.c_int64, _DP], ctypes.c_int),
     "qs_exchange_gate_peer": ([_P, _P, _I, _DP, _I], ctypes.c_int),
     "qs_exchange_gate_nccl": ([_P, _I, _I, _DP, _I, _U], ctypes.c_int),
     "qs_swap_qubits_peer": ([_P, _P, _I, _I], ctypes.c_int),

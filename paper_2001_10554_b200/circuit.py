@@ -15,7 +15,8 @@ import numpy as np
 ONE_QUBIT_KINDS = frozenset({"h", "x", "y", "z", "rx", "ry", "rz", "custom"})
 ROTATION_KINDS = frozenset({"rx", "ry", "rz"})
 TWO_QUBIT_KINDS = frozenset({"cx", "cz", "cphase", "cu"})
-ALL_KINDS = ONE_QUBIT_KINDS | TWO_QUBIT_KINDS | {"diagcost"}
+ALL_KINDS = ONE_QUBIT_KINDS | TWO_QUBIT_KINDS | {"diagcost", "noise"}
+DEFAULT_GATE_DURATION = 1.0  # circuit.py:31 (noise scheduling, noise.py:92-139)
 
 
 class UnboundParameterError(ValueError):
@@ -29,6 +30,7 @@ class GateSpec:
     param: float | str | None = None
     matrix: np.ndarray | None = field(default=None, repr=False, compare=False)
     graph: object | None = None
+    duration: float = DEFAULT_GATE_DURATION
 
     def __post_init__(self) -> None:
         if self.kind not in ALL_KINDS:

@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -843,6 +844,35 @@ int qs_observable(qs_state* st, int32_t kind, int32_t q, const int32_t* edges, i
                              cudaMemcpyDeviceToHost, st->stream));
     CUDA_TRY(cudaStreamSynchronize(st->stream));
     memcpy(out, st->h_out, sizeof(double) * st->num_states);
+    return QS_OK;
+}
+
+// Host-side 2x2 products for noise matrices (qsb200.h; noise.py:70-80).
+int qs_compose_2x2(const double* a, const double* b, int64_t count, double* out) {
+    if (count < 0 || (count && (!a || !b || !out))) return fail(QS_ERR_VALUE, "bad compose args");
+    for (int64_t s = 0; s < count; ++s) {
+        const double* x = a + 8 * s;
+        const double* y = b + 8 * s;
+        double z[8];
+        for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) {
+                const double ar0 = x[4 * i + 0], ai0 = x[4 * i + 1];
+                const double ar1 = x[4 * i + 2], ai1 = x[4 * i + 3];
+                const double br0 = y[2 * j + 0], bi0 = y[2 * j + 1];
+                const double br1 = y[4 + 2 * j], bi1 = y[4 + 2 * j + 1];
+                double re = std::fma(ar0, br0, 0.0);
+                re = std::fma(-ai0, bi0, re);
+                re = std::fma(ar1, br1, re);
+                re = std::fma(-ai1, bi1, re);
+                double im = std::fma(ar0, bi0, 0.0);
+                im = std::fma(ai0, br0, im);
+                im = std::fma(ar1, bi1, im);
+                im = std::fma(ai1, br1, im);
+                z[4 * i + 2 * j] = re;
+                z[4 * i + 2 * j + 1] = im;
+            }
+        memcpy(out + 8 * s, z, sizeof z);
+    }
     return QS_OK;
 }
 

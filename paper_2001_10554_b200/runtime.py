@@ -27,6 +27,7 @@ from . import distribution as dist
 from . import gates as gates_mod
 from . import statevector as sv
 from .graphs import edge_array, phase_lut, phase_lut_batch
+from . import noise as noise_mod
 
 NORM_CHECK_INTERVAL = 100
 NORM_TOL = 1e-10
@@ -135,12 +136,16 @@ class RankContext:
     fuse: bool = True
     remap: bool = False
     norm_check_interval: int = NORM_CHECK_INTERVAL
+    seed: int = 0
+    noise_model: "noise_mod.NoiseModel | None" = None
+    state_offset: int = 0  # global index of this context's first pool state
     topology: dist.RankTopology = field(init=False)
     layout: "dist.QubitLayout | None" = field(init=False, default=None)
     partition: sv.StatePartition | None = field(init=False, default=None)
     pool: "PoolState | None" = field(init=False, default=None)
     queue: GateQueue | None = field(init=False, default=None)
     gates_applied: int = field(init=False, default=0)
+    _state_stream: object = field(init=False, default=None, repr=False)
 
     def __post_init__(self) -> None:
         size = self.comm.size if self.num_states == 1 else 1
@@ -167,6 +172,20 @@ class RankContext:
         return self.queue is None
 
     @property
+    def state_stream(self):
+        """The state-scope stream of this context's state (runtime.py:79);
+        pools get a StreamBatch with one stream per state."""
+        if self._state_stream is None:
+            if self.pool is None:
+                self._state_stream = noise_mod.RandomStream(self.seed, noise_mod.SCOPE_STATE,
+                                                            self.state_offset)
+            else:
+                self._state_stream = noise_mod.StreamBatch(
+                    noise_mod.RandomStream(self.seed, noise_mod.SCOPE_STATE, self.state_offset + s)
+                    for s in range(self.num_states))
+        return self._state_stream
+
+    @property
     def state(self) -> _native.DeviceState:
         return self.partition.state if self.partition is not None else self.pool.state
 
@@ -178,12 +197,15 @@ class RankContext:
 
 
 def make_context(comm: dist.GroupComm | None, num_qubits: int, num_states: int = 1,
-                 device: int = 0, fuse: bool = True, remap: bool = False) -> RankContext:
+                 device: int = 0, fuse: bool = True, remap: bool = False, *, seed: int = 0,
+                 noise_model=None, state_offset: int = 0) -> RankContext:
     """remap=True: gates on global qubits first swap the qubit into a local
     position (half the traffic of the reference's exchange, and the gate then
-    fuses with its neighbours); reads restore the canonical layout."""
+    fuses with its neighbours); reads restore the canonical layout.
+    seed/noise_model as the reference's make_context (runtime.py:90-99);
+    state_offset: global index of the first pool state (split_pool)."""
     return RankContext(comm or dist.single_rank_comm(), num_qubits, num_states, device, fuse,
-                       remap)
+                       remap, seed=seed, noise_model=noise_model, state_offset=state_offset)
 
 
 def reset_state(ctx: RankContext, index: int = 0) -> None:
@@ -262,10 +284,37 @@ def _swap_in(ctx: RankContext, qubit: int, protected=()) -> None:
     dist.swap_global_local(ctx.partition, ctx.comm, ctx.topology, L, p, slot)
 
 
-def apply_gate(ctx: RankContext, gate) -> None:
-    """Queue one gate; global-qubit gates flush and exchange (runtime.py:115-152)."""
+def _noise_matrix(ctx: RankContext, gate, noise_stream):
+    """The noise gate's matrix (noise.py:70-80): (2,2) for one state, (S,2,2)
+    for a pool whose states draw from their own streams (runtime.py:122-126)."""
+    if ctx.noise_model is None:
+        raise ValueError("noise gate requires a noise model on the context")
+    stream = ctx.state_stream if noise_stream is None else noise_stream
+    if ctx.pool is not None:
+        if not isinstance(stream, noise_mod.StreamBatch):
+            stream = noise_mod.StreamBatch(stream)
+        if len(stream) != ctx.num_states:
+            raise ValueError(f"{len(stream)} noise streams for {ctx.num_states} states")
+        return noise_mod.noise_gate_matrices(gate.duration, ctx.noise_model, stream)
+    if isinstance(stream, noise_mod.StreamBatch):
+        raise ValueError("a single-state context takes one noise stream")
+    return noise_mod.noise_gate_matrix(gate.duration, ctx.noise_model, stream)
+
+
+def apply_gate(ctx: RankContext, gate, noise_stream=None) -> None:
+    """Queue one gate; global-qubit gates flush and exchange (runtime.py:115-152).
+    Noise gates draw their matrix from `noise_stream` (default: the context's
+    state stream) and then run as one-qubit gates."""
     if ctx.is_idle:
         return
+    if gate.kind == "noise":
+        u = _noise_matrix(ctx, gate, noise_stream)
+        if u.ndim == 3:  # pool: per-state table, every qubit is local
+            ctx.queue.one_qubit(gate.qubits[0], u)
+            ctx.gates_applied += 1
+            return
+        from .circuit import GateSpec
+        gate = GateSpec("custom", gate.qubits, matrix=u)
     if ctx.layout is not None:
         _apply_gate_remapped(ctx, gate)
         ctx.gates_applied += 1
@@ -308,11 +357,12 @@ def apply_gate(ctx: RankContext, gate) -> None:
             raise NormDriftError(f"norm^2 drifted to {norm_sq!r} after {ctx.gates_applied} gates")
 
 
-def run_circuit(ctx: RankContext, circuit, bindings: dict | None = None) -> None:
+def run_circuit(ctx: RankContext, circuit, bindings: dict | None = None,
+                noise_stream=None) -> None:
     bound = circuit.bind(bindings) if bindings else circuit
     bound.require_bound()
     for gate in bound.gates:
-        apply_gate(ctx, gate)
+        apply_gate(ctx, gate, noise_stream=noise_stream)
     ctx.flush()
 
 
@@ -428,11 +478,14 @@ class PoolState:
         return self.state.download().reshape(self.num_states, -1)
 
 
-def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None) -> None:
+def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
+                     noise_stream=None) -> None:
     """Every pool state runs `circuit`; state s binds slot_tables[name][s]
-    (runtime.py:192-209).  Per-state matrices/LUTs go to the device as tables."""
+    (runtime.py:192-209).  Per-state matrices/LUTs go to the device as tables;
+    noise gates draw state s's matrix from stream s of `noise_stream` (a
+    StreamBatch or a list of streams; default: the states' own streams)."""
     if not slot_tables:
-        run_circuit(ctx, circuit)
+        run_circuit(ctx, circuit, noise_stream=noise_stream)
         return
     if ctx.is_idle:
         return
@@ -445,8 +498,8 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None)
     for gate in circuit.gates:
         slot = gate.slot if isinstance(getattr(gate, "param", None), str) else None
         if slot is None:
-            if ctx.pool is None:
-                apply_gate(ctx, gate)
+            if ctx.pool is None or gate.kind == "noise":
+                apply_gate(ctx, gate, noise_stream=noise_stream)
                 continue
             _queue_fixed(q, gate)
             continue
@@ -456,7 +509,7 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None)
         if ctx.pool is None:
             # single state: bind value 0 (run_circuit semantics)
             from dataclasses import replace
-            apply_gate(ctx, replace(gate, param=float(vals[0])))
+            apply_gate(ctx, replace(gate, param=float(vals[0])), noise_stream=noise_stream)
             continue
         if gate.kind == "diagcost":
             q.cut_phase(gate.graph, vals)
@@ -468,6 +521,72 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None)
         else:
             raise ValueError(f"gate kind {gate.kind} takes no parameter")
     q.flush()
+
+
+def run_noise_ensemble(ctx: RankContext, circuit, model, trajectories: int, observe,
+                       seed: int | None = None, num_groups: int | None = None):
+    """Noisy-trajectory ensemble (cli.py:288-339) on this context.
+
+    Trajectory t runs on pool group t mod num_groups in round t div
+    num_groups, drawing its noise from trajectory_stream(seed, t) -- so every
+    trajectory is bit-identical to a serial single-state run with the same
+    index, however the ensemble is spread.  A pool context runs all of its S
+    states as one fused program per round.  `observe(ctx)` returns one value
+    (single state) or S values (pool).  Circuits without noise gates get
+    schedule_noise() first, as the CLI does.
+
+    Returns (reference, values): the noiseless value (computed with the
+    NOISELESS model and trajectory 0's stream) and a float array of length
+    `trajectories` holding this context's trajectories (NaN elsewhere)."""
+    if trajectories < 1:
+        raise ValueError("--trajectories must be >= 1")
+    if not any(g.kind == "noise" for g in circuit.gates):
+        circuit = noise_mod.schedule_noise(circuit)
+    seed = ctx.seed if seed is None else seed
+    S = ctx.num_states if ctx.pool is not None else 1
+    groups = S if num_groups is None else num_groups
+    values = np.full(trajectories, np.nan)
+    if ctx.is_idle:
+        return None, values
+
+    def streams(first: int):
+        if ctx.pool is None:
+            return noise_mod.trajectory_stream(seed, first)
+        return noise_mod.StreamBatch(noise_mod.trajectory_stream(seed, first + s)
+                                     for s in range(S))
+
+    def run(model_, first, stream_fn):
+        ctx.noise_model = model_
+        reset_state(ctx)
+        run_circuit(ctx, circuit, noise_stream=stream_fn(first))
+        return np.atleast_1d(np.asarray(observe(ctx), dtype=np.float64))
+
+    saved = ctx.noise_model
+    try:
+        if ctx.pool is None:
+            ref = float(run(noise_mod.NOISELESS, 0, streams)[0])
+        else:  # every state runs trajectory 0's (noiseless) draws
+            ref = float(run(noise_mod.NOISELESS, 0, lambda _f: noise_mod.StreamBatch(
+                noise_mod.trajectory_stream(seed, 0) for _ in range(S)))[0])
+        for k in range(-(-trajectories // groups)):
+            first = k * groups + ctx.state_offset
+            if first >= trajectories:
+                continue
+            vals = run(model, first, streams)
+            count = min(S, trajectories - first)
+            values[first:first + count] = vals[:count]
+    finally:
+        ctx.noise_model = saved
+    return ref, values
+
+
+def noise_ensemble_csv(values, reference: float) -> str:
+    """The noise-ensemble report (cli.py:329-334): running mean per count."""
+    values = np.asarray(values, dtype=np.float64)
+    running = np.cumsum(values) / np.arange(1, values.size + 1)
+    lines = ["trajectories,running_mean,reference"]
+    lines.extend(f"{i + 1},{float(running[i])!r},{reference!r}" for i in range(values.size))
+    return "\n".join(lines) + "\n"
 
 
 def _queue_fixed(q: GateQueue, gate) -> None:

@@ -314,11 +314,42 @@ def gen_accounting():
     save("golden_accounting_state.npz", u=u, out=np.concatenate([r[1] for r in res]))
 
 
+def gen_noise():
+    """Noise trajectories (noise.py): a 12-qubit circuit with scheduled T1/T2
+    noise, trajectories 0..3 of the reference's trajectory streams."""
+    from qpool.noise import NoiseModel, schedule_noise, trajectory_stream
+    n = 12
+    rng = np.random.default_rng(SEED + 7)
+    specs = []
+    for layer in range(3):
+        for q in range(n):
+            k = ("h", "rx", "ry")[int(rng.integers(3))]
+            specs.append(GateSpec(k, (q,)) if k == "h" else
+                         GateSpec(k, (q,), float(rng.uniform(0, 2 * np.pi))))
+        for q in range(layer % 2, n - 1, 2):
+            specs.append(GateSpec("cx", (q, q + 1)))
+    circ = schedule_noise(Circuit(n, tuple(specs)))
+    model = NoiseModel(20.0, 15.0)
+    states = []
+    for t in range(4):
+        ctx = runtime.make_context(None, n, 1, 0, model)
+        runtime.run_circuit(ctx, circ, noise_stream=trajectory_stream(SEED, t))
+        states.append(ctx.partition.amplitudes.copy())
+    enc = []
+    kinds = {"h": 0, "rx": 1, "ry": 2, "cx": 3, "noise": 4}
+    for g in circ.gates:
+        q = g.qubits
+        enc.append((kinds[g.kind], q[0], q[1] if len(q) > 1 else -1,
+                    g.param if g.param is not None else 0.0, g.duration))
+    save("golden_noise.npz", gates=np.array(enc), states=np.stack(states),
+         t1=np.array(20.0), t2=np.array(15.0), seed=np.array(SEED))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["1q", "ctrl", "phase_obs", "cfg1", "cfg3", "cfg4", "cfg5", "acct"]
     table = {"1q": gen_1q, "ctrl": gen_ctrl, "phase_obs": gen_phase_obs, "cfg1": gen_cfg1,
              "cfg3": gen_cfg3_small, "cfg4": gen_cfg4_small, "cfg5": gen_cfg5,
-             "acct": gen_accounting}
+             "acct": gen_accounting, "noise": lambda: gen_noise()}
     for w in which:
         t0 = time.perf_counter()
         table[w]()
