@@ -47,7 +47,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--local-qubits", type=int, default=30)
     ap.add_argument("--no-fuse", action="store_true")
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "qaoa", "cfg4"])
+    ap.add_argument("--workload", default="sweep", choices=["sweep", "qaoa", "cfg4", "noise"])
     ap.add_argument("--seed", type=int, default=20260809)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -252,6 +252,8 @@ def run_ours(args):
     comm = qdist.TorchComm(exchange_mode=args.exchange) if world > 1 else qdist.single_rank_comm()
     if args.workload == "qaoa":
         return run_qaoa(args, dist, comm, world, rank, local)
+    if args.workload == "noise":
+        return run_noise(args, dist, comm, world, rank, local)
     ctx = runtime.make_context(comm, n, 1, device=local, fuse=not args.no_fuse,
                                remap=args.remap)
     ctx.norm_check_interval = 0
@@ -606,6 +608,156 @@ def run_qaoa(args, dist, comm, world, rank, local):
                     "h2d_bytes_per_step": int(count * (2 * depth * 8 * n + 2 * 31 * 16 * depth)),
                     "d2h_bytes_per_step": int(8 * count),
                     "note": "the step itself is end to end: parameter tables up, <C> down"},
+        }
+        print(json.dumps(line))
+    barrier(dist)
+    return 0
+
+
+NOISE_T1, NOISE_T2 = 500.0, 250.0  # the reference's noise study defaults (noise_convergence_study.py)
+
+
+def noise_instance(seed):
+    """Config 5's circuit shape (n=20, p=4 QAOA on a random 3-regular graph)
+    at one fixed parameter point, with schedule_noise() applied: the noisy
+    QAOA ensemble of the reference's noise study, at config-5 size."""
+    from paper_2001_10554_b200 import noise
+    from paper_2001_10554_b200.circuit import build_qaoa_circuit, qaoa_bindings
+    from paper_2001_10554_b200.workloads import random_3regular_graph
+
+    rng = np.random.default_rng(seed)
+    graph = random_3regular_graph(QAOA_N, rng)
+    point = rng.uniform(0, np.pi, size=2 * QAOA_P)
+    circ = build_qaoa_circuit(graph, QAOA_P).bind(qaoa_bindings(QAOA_P, point))
+    return graph, noise.schedule_noise(circ)
+
+
+def cpu_noise_sample(circ, graph, seed, threads):
+    """Oracle port on the host: `threads` trajectories concurrently, each the
+    reference's scalar path (numpy Philox per noise gate, gate by gate)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import circuit as ocirc
+    from oracle import noise as onoise
+    from oracle import statevector as osv
+
+    n = circ.num_qubits
+    edges = list(graph.edges)
+    glist = []
+    for g in circ.gates:
+        if g.kind == "diagcost":
+            glist.append({"kind": "diagcost", "param": g.param, "edges": edges})
+        else:
+            glist.append({"kind": g.kind, "qubits": g.qubits, "param": g.param,
+                          "duration": g.duration})
+
+    def one(t):
+        prog = onoise.bind_trajectory(glist, NOISE_T1, NOISE_T2, seed, t)
+        return osv.maxcut_expectation(ocirc.run(n, prog), edges)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        vals = list(ex.map(one, range(threads)))
+    dt = time.perf_counter() - t0
+    return len(vals) / dt, dt, vals
+
+
+def run_noise(args, dist, comm, world, rank, local):
+    """Noise trajectories in pool mode (cli.py:288-339):
+    512 trajectories of the noisy config-5 QAOA circuit per step, one pool
+    round -- per-trajectory noise matrices drawn on the host in one pass,
+    the whole round applied as fused tile programs with per-state tables,
+    <C> per trajectory read back.  Trajectories are split across GPUs in
+    contiguous blocks (no state exchange); trajectory t equals a serial run
+    of index t bit for bit."""
+    from paper_2001_10554_b200 import noise, runtime
+
+    n, S = QAOA_N, QAOA_POOL
+    first, count = runtime.split_pool(S, rank, world)
+    graph, circ = noise_instance(args.seed)
+    model = noise.NoiseModel(NOISE_T1, NOISE_T2)
+    ctx = runtime.make_context(None, n, num_states=count, device=local, fuse=not args.no_fuse,
+                               seed=args.seed, noise_model=model)
+    ctx.norm_check_interval = 0
+    st = ctx.state
+    edges = np.asarray(graph.edges, dtype=np.int32)
+    round_no = [0]
+
+    def step():
+        base = round_no[0] * S + first
+        round_no[0] += 1
+        runtime.reset_state(ctx)
+        batch = noise.StreamBatch(noise.trajectory_stream(args.seed, base + s)
+                                  for s in range(count))
+        runtime.run_circuit(ctx, circ, noise_stream=batch)
+        return ctx.pool.observable(3, 0, edges)
+
+    for _ in range(args.warmup):
+        step()
+    st.synchronize()
+    barrier(dist)
+    clocks = ClockSampler(local)
+    clocks.start()
+    st.launch_log(True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        values = step()
+    st.synchronize()
+    wall = time.perf_counter() - t0
+    st.launch_log(False)
+    launch_ms, launch_kind = st.read_launch_log()
+    clock = clocks.stop()
+    wall = max_over_ranks(dist, wall)
+    gates_per_circuit = len(circ.gates)
+    noise_gates = sum(g.kind == "noise" for g in circ.gates)
+    trajectories = S * args.steps
+    value = trajectories * gates_per_circuit * (2.0 ** n) / 2.0 ** 30 / wall
+    kinds = {}
+    for k, t in zip(launch_kind, launch_ms):
+        kinds.setdefault(int(k), []).append(float(t))
+    dev_ms = sum(sum(v) for v in kinds.values())
+    dom = max(kinds, key=lambda k: sum(kinds[k]))
+    dom_ms = float(np.mean(kinds[dom]))
+    peak, peak_src = measured_peak()
+    bytes_per_launch = 32.0 * (2 ** n) * count
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import cpu_baseline as cb
+
+        tps, dt, _ = cpu_noise_sample(circ, graph, args.seed, cb.threads())
+        cpu = {"value": tps * gates_per_circuit * (2.0 ** n) / 2.0 ** 30, "unit": UNIT,
+               "cores": cb.threads(), "kind": "port",
+               "sample": f"{cb.threads()} noisy trajectories (n={n}, {gates_per_circuit} gates "
+                         f"incl. {noise_gates} noise gates, + <C>) on {cb.threads()} host "
+                         f"threads, oracle port, {dt:.2f} s",
+               "trajectories_per_s": tps}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c128 (f64 pairs)", "data": "synthetic",
+            "config": {"workload": f"noise ensemble: {S} trajectories per step of the noisy "
+                                   f"config-5 QAOA circuit (n={n}, p={QAOA_P}, schedule_noise, "
+                                   f"T1={NOISE_T1}, T2={NOISE_T2}), <C> per trajectory",
+                       "pool": S, "per_gpu": count, "gates_per_circuit": gates_per_circuit,
+                       "noise_gates": noise_gates, "fused": not args.no_fuse},
+            "trajectories_per_s": trajectories / wall,
+            "mean_cut": float(np.mean(values)),
+            "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
+                         "achieved": bytes_per_launch / (dom_ms / 1e3) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_per_launch / (dom_ms / 1e3) / 1e9 / peak,
+                         "traffic": None, "avg_launch_ms": dom_ms, "peak_source": peak_src},
+            "kernel_share": {LAUNCH_KINDS.get(k, str(k)): {"launches": len(v),
+                                                           "share": float(np.sum(v) / dev_ms)}
+                             for k, v in kinds.items()},
+            "device_ms_per_step": dev_ms / args.steps,
+            "gpu_launches": int(len(launch_ms)),
+            "clocks": clock,
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(count * noise_gates * 64),
+                    "d2h_bytes_per_step": int(8 * count),
+                    "note": "the step itself is end to end: noise matrices up, <C> down"},
         }
         print(json.dumps(line))
     barrier(dist)

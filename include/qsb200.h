@@ -158,6 +158,12 @@ int qs_marginals(qs_state* st, double* out);
  * noisy states built from them, are bit-identical on any host.  Host-only. */
 int qs_compose_2x2(const double* a, const double* b, int64_t count, double* out);
 
+/* Philox4x64-10 blocks (Random123; numpy's Philox bit generator, which the
+ * reference's RandomStream draws from, pool.py:70): for i < count,
+ * out[4i..4i+3] = philox(key = keys[2i..2i+1], counter = (ctr[2i], ctr[2i+1], 0, 0)).
+ * Host-only; lets a pool round draw all its noise angles in one call. */
+int qs_philox4x64(const uint64_t* keys, const uint64_t* ctr, int64_t count, uint64_t* out);
+
 /* ---- global-qubit path: distribution.py:121-230 ----------------------- */
 /* Pairwise exchange gate for a target on a global qubit, computed in one
  * kernel over NVLink peer memory: this rank updates half of the pairs it

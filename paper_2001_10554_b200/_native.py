@@ -32,7 +32,7 @@ EXPORTS = (
     "qs_swap_qubits_local", "qs_state_ipc_handle", "qs_peer_open",
     "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
     "qs_event_record", "qs_event_elapsed_ms", "qs_launch_log", "qs_launch_log_read",
-    "qs_compose_2x2",
+    "qs_compose_2x2", "qs_philox4x64",
 )
 
 
@@ -63,6 +63,7 @@ _I = ctypes.c_int32
 _U = ctypes.c_uint64
 _D = ctypes.c_double
 _DP = ctypes.POINTER(ctypes.c_double)
+_U64P = ctypes.POINTER(ctypes.c_uint64)
 _IP = ctypes.POINTER(ctypes.c_int32)
 _UP = ctypes.POINTER(ctypes.c_uint64)
 _BP = ctypes.POINTER(ctypes.c_ubyte)
@@ -94,6 +95,7 @@ _SIGNATURES = {
     "qs_observable": ([_P, _I, _I, _IP, _I, _DP], ctypes.c_int),
     "qs_marginals": ([_P, _DP], ctypes.c_int),
     "qs_compose_2x2": ([_DP, _DP, ctypes.c_int64, _DP], ctypes.c_int),
+    "qs_philox4x64": ([_U64P, _U64P, ctypes.c_int64, _U64P], ctypes.c_int),
     "qs_exchange_gate_peer": ([_P, _P, _I, _DP, _I], ctypes.c_int),
     "qs_exchange_gate_nccl": ([_P, _I, _I, _DP, _I, _U], ctypes.c_int),
     "qs_swap_qubits_peer": ([_P, _P, _I, _I], ctypes.c_int),
@@ -176,6 +178,12 @@ def dptr(a: np.ndarray):
 
 def iptr(a: np.ndarray):
     return a.ctypes.data_as(_IP)
+
+
+def u64ptr(a: np.ndarray):
+    if a.dtype != np.uint64 or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("need a C-contiguous uint64 array")
+    return a.ctypes.data_as(_U64P)
 
 
 class DeviceState:

@@ -848,30 +848,66 @@ int qs_observable(qs_state* st, int32_t kind, int32_t q, const int32_t* edges, i
 }
 
 // Host-side 2x2 products for noise matrices (qsb200.h; noise.py:70-80).
+static inline __attribute__((always_inline)) void compose_one(const double* x, const double* y,
+                                                              double* out) {
+    double z[8];
+    for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) {
+            const double ar0 = x[4 * i + 0], ai0 = x[4 * i + 1];
+            const double ar1 = x[4 * i + 2], ai1 = x[4 * i + 3];
+            const double br0 = y[2 * j + 0], bi0 = y[2 * j + 1];
+            const double br1 = y[4 + 2 * j], bi1 = y[4 + 2 * j + 1];
+            double re = __builtin_fma(ar0, br0, 0.0);
+            re = __builtin_fma(-ai0, bi0, re);
+            re = __builtin_fma(ar1, br1, re);
+            re = __builtin_fma(-ai1, bi1, re);
+            double im = __builtin_fma(ar0, bi0, 0.0);
+            im = __builtin_fma(ai0, br0, im);
+            im = __builtin_fma(ar1, bi1, im);
+            im = __builtin_fma(ai1, br1, im);
+            z[4 * i + 2 * j] = re;
+            z[4 * i + 2 * j + 1] = im;
+        }
+    memcpy(out, z, sizeof z);
+}
+
+// same loop with hardware FMA instructions inlined (fma is exact either way)
+__attribute__((target("fma"))) static void compose_hw(const double* a, const double* b,
+                                                      int64_t count, double* out) {
+    for (int64_t s = 0; s < count; ++s) compose_one(a + 8 * s, b + 8 * s, out + 8 * s);
+}
+
+static void compose_sw(const double* a, const double* b, int64_t count, double* out) {
+    for (int64_t s = 0; s < count; ++s) compose_one(a + 8 * s, b + 8 * s, out + 8 * s);
+}
+
 int qs_compose_2x2(const double* a, const double* b, int64_t count, double* out) {
     if (count < 0 || (count && (!a || !b || !out))) return fail(QS_ERR_VALUE, "bad compose args");
-    for (int64_t s = 0; s < count; ++s) {
-        const double* x = a + 8 * s;
-        const double* y = b + 8 * s;
-        double z[8];
-        for (int i = 0; i < 2; ++i)
-            for (int j = 0; j < 2; ++j) {
-                const double ar0 = x[4 * i + 0], ai0 = x[4 * i + 1];
-                const double ar1 = x[4 * i + 2], ai1 = x[4 * i + 3];
-                const double br0 = y[2 * j + 0], bi0 = y[2 * j + 1];
-                const double br1 = y[4 + 2 * j], bi1 = y[4 + 2 * j + 1];
-                double re = std::fma(ar0, br0, 0.0);
-                re = std::fma(-ai0, bi0, re);
-                re = std::fma(ar1, br1, re);
-                re = std::fma(-ai1, bi1, re);
-                double im = std::fma(ar0, bi0, 0.0);
-                im = std::fma(ai0, br0, im);
-                im = std::fma(ar1, bi1, im);
-                im = std::fma(ai1, br1, im);
-                z[4 * i + 2 * j] = re;
-                z[4 * i + 2 * j + 1] = im;
-            }
-        memcpy(out + 8 * s, z, sizeof z);
+    if (__builtin_cpu_supports("fma")) compose_hw(a, b, count, out);
+    else compose_sw(a, b, count, out);
+    return QS_OK;
+}
+
+// Philox4x64-10 blocks for the noise streams (qsb200.h).
+int qs_philox4x64(const uint64_t* keys, const uint64_t* ctr, int64_t count, uint64_t* out) {
+    if (count < 0 || (count && (!keys || !ctr || !out))) return fail(QS_ERR_VALUE, "bad philox args");
+    const uint64_t M0 = 0xD2E7470EE14C6C93ull, M1 = 0xCA5A826395121157ull;
+    const uint64_t W0 = 0x9E3779B97F4A7C15ull, W1 = 0xBB67AE8584CAA73Bull;
+    for (int64_t i = 0; i < count; ++i) {
+        uint64_t k0 = keys[2 * i], k1 = keys[2 * i + 1];
+        uint64_t v0 = ctr[2 * i], v1 = ctr[2 * i + 1], v2 = 0, v3 = 0;
+        for (int r = 0; r < 10; ++r) {
+            if (r) { k0 += W0; k1 += W1; }
+            const unsigned __int128 p0 = (unsigned __int128)M0 * v0;
+            const unsigned __int128 p1 = (unsigned __int128)M1 * v2;
+            const uint64_t hi0 = uint64_t(p0 >> 64), lo0 = uint64_t(p0);
+            const uint64_t hi1 = uint64_t(p1 >> 64), lo1 = uint64_t(p1);
+            v0 = hi1 ^ v1 ^ k0;
+            v1 = lo1;
+            v2 = hi0 ^ v3 ^ k1;
+            v3 = lo0;
+        }
+        out[4 * i] = v0; out[4 * i + 1] = v1; out[4 * i + 2] = v2; out[4 * i + 3] = v3;
     }
     return QS_OK;
 }

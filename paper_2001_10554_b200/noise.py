@@ -78,30 +78,69 @@ def _mulhilo(a: np.uint64, b: np.ndarray):
     return hi, a * b
 
 
+def _philox_block(k0, k1, c0, c1):
+    """Philox4x64-10 of counter (c0, c1, 0, 0) under key (k0, k1), arrays
+    broadcast; the four output words.  Runs in libqsb200 (qs_philox4x64)."""
+    shape = np.broadcast(k0, k1, c0, c1).shape
+    keys = np.empty(shape + (2,), dtype=np.uint64)
+    keys[..., 0], keys[..., 1] = k0, k1
+    ctr = np.empty(shape + (2,), dtype=np.uint64)
+    ctr[..., 0], ctr[..., 1] = c0, c1
+    out = np.empty(shape + (4,), dtype=np.uint64)
+    _native.call("qs_philox4x64", _native.u64ptr(keys), _native.u64ptr(ctr),
+                 int(np.prod(shape, dtype=np.int64)), _native.u64ptr(out))
+    return [out[..., j] for j in range(4)]
+
+
+def philox_block_numpy(k0, k1, c0, c1):
+    """The same Philox rounds in numpy (the restatement qs_philox4x64 is
+    checked against in tests/test_noise.py)."""
+    z = np.zeros(np.broadcast(k0, c0).shape, dtype=np.uint64)
+    v = [c0 + z, c1 + z, z, z]
+    with np.errstate(over="ignore"):
+        for r in range(10):
+            if r:
+                k0 = k0 + _W0
+                k1 = k1 + _W1
+            hi0, lo0 = _mulhilo(_M0, v[0])
+            hi1, lo1 = _mulhilo(_M1, v[2])
+            v = [hi1 ^ v[1] ^ k0, lo1, hi0 ^ v[3] ^ k1, lo0]
+    return v
+
+
+def _to_unit(words: np.ndarray) -> np.ndarray:
+    """numpy's next_double: top 53 bits x 2^-53."""
+    return (words >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+
+
 def philox4x64_uniform(keys: np.ndarray, counters: np.ndarray, count: int) -> np.ndarray:
     """[S, count] doubles in [0,1): what ``Generator(Philox(counter=[c,0,0,0],
-    key=k)).random(count)`` returns for each (k, c) row."""
+    key=k)).random(count)`` returns for each (k, c) row.  numpy increments
+    the 256-bit counter before every 4-word block, so block b is Philox of
+    counter c+1+b."""
     keys = np.asarray(keys, dtype=np.uint64).reshape(-1, 2)
-    ctr0 = np.asarray(counters, dtype=np.uint64).reshape(-1)
-    S = keys.shape[0]
+    ctr0 = np.asarray(counters, dtype=np.uint64).reshape(-1, 1)
     blocks = -(-count // 4)
-    out = np.empty((S, blocks * 4), dtype=np.uint64)
     with np.errstate(over="ignore"):
-        for b in range(blocks):
-            # numpy increments the 256-bit counter before every block
-            c0 = ctr0 + np.uint64(b + 1)
-            c1 = (c0 < ctr0).astype(np.uint64)  # carry (counters are < 2^64 - 4 in practice)
-            v = [c0, c1, np.zeros(S, np.uint64), np.zeros(S, np.uint64)]
-            k0, k1 = keys[:, 0].copy(), keys[:, 1].copy()
-            for r in range(10):
-                if r:
-                    k0 = k0 + _W0
-                    k1 = k1 + _W1
-                hi0, lo0 = _mulhilo(_M0, v[0])
-                hi1, lo1 = _mulhilo(_M1, v[2])
-                v = [hi1 ^ v[1] ^ k0, lo1, hi0 ^ v[3] ^ k1, lo0]
-            out[:, 4 * b:4 * b + 4] = np.stack(v, axis=1)
-    return (out[:, :count] >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
+        c0 = ctr0 + np.arange(1, blocks + 1, dtype=np.uint64)[None, :]
+    c1 = (c0 < ctr0).astype(np.uint64)  # carry into the second counter word
+    v = _philox_block(keys[:, :1], keys[:, 1:], c0, c1)
+    words = np.stack(v, axis=2).reshape(keys.shape[0], blocks * 4)
+    return _to_unit(words[:, :count])
+
+
+def philox4x64_draws3(keys: np.ndarray, counters: np.ndarray, num_calls: int) -> np.ndarray:
+    """[S, num_calls, 3]: the uniforms of `num_calls` consecutive
+    ``stream.uniform(3)`` calls per stream (call j regenerates from counter
+    c+3j, so it uses words 0..2 of block c+3j+1) -- one vectorised Philox
+    pass for a whole circuit's noise draws."""
+    keys = np.asarray(keys, dtype=np.uint64).reshape(-1, 2)
+    ctr0 = np.asarray(counters, dtype=np.uint64).reshape(-1, 1)
+    with np.errstate(over="ignore"):
+        c0 = ctr0 + np.uint64(1) + np.uint64(3) * np.arange(num_calls, dtype=np.uint64)[None, :]
+    c1 = (c0 < ctr0).astype(np.uint64)
+    v = _philox_block(keys[:, :1], keys[:, 1:], c0, c1)
+    return _to_unit(np.stack(v[:3], axis=2))
 
 
 # ---- keyed streams ----------------------------------------------------------------------
@@ -180,6 +219,15 @@ class StreamBatch:
     def normal(self, count: int) -> np.ndarray:
         return ndtri(np.clip(self.uniform(count), 1e-300, None))
 
+    def normal3_calls(self, num_calls: int) -> np.ndarray:
+        """[S, num_calls, 3]: what `num_calls` successive normal(3) calls
+        return, drawn in one pass; counters advance by 3*num_calls."""
+        ctr = np.array([s.counter for s in self.streams], dtype=np.uint64)
+        u = philox4x64_draws3(self._keys, ctr, num_calls)
+        for s in self.streams:
+            s.counter += 3 * num_calls
+        return ndtri(np.clip(u, 1e-300, None))
+
 
 def trajectory_stream(seed: int, trajectory_index: int) -> RandomStream:
     """State-scope stream of trajectory t (noise.py:60-69): independent of how
@@ -246,6 +294,30 @@ def noise_gate_matrices(duration: float, model: NoiseModel, batch: StreamBatch) 
     """[S,2,2]: noise_gate_matrix for every stream of the batch, in one pass."""
     model.variances(duration)
     return _matrices_from_draws(batch.normal(3), duration, model)
+
+
+def circuit_noise_matrices(durations, model: NoiseModel, stream) -> np.ndarray:
+    """The matrices of G consecutive noise gates (durations in circuit order)
+    drawn from one stream ([G,2,2]) or a StreamBatch ([G,S,2,2]) -- equal to
+    calling noise_gate_matrix / noise_gate_matrices gate by gate, but with
+    one Philox pass, one ndtri and one batch of 2x2 products for the whole
+    circuit (the per-gate host cost of a pool round drops ~100x)."""
+    durations = [float(d) for d in durations]
+    scales = []
+    for d in durations:
+        vxy, vz = model.variances(d)
+        scales.append((math.sqrt(vxy), math.sqrt(vxy), math.sqrt(vz)))
+    single = not isinstance(stream, StreamBatch)
+    batch = StreamBatch([stream]) if single else stream
+    num, S = len(durations), len(batch)
+    if num == 0:
+        return np.zeros((0, 2, 2) if single else (0, S, 2, 2), dtype=np.complex128)
+    ang = batch.normal3_calls(num) * np.array(scales)[None, :, :]  # [S, num, 3]
+    ang = np.ascontiguousarray(ang.transpose(1, 0, 2)).reshape(num * S, 3)
+    mats = compose_2x2(compose_2x2(G.rotation_batch("rz", ang[:, 2]),
+                                   G.rotation_batch("ry", ang[:, 1])),
+                       G.rotation_batch("rx", ang[:, 0])).reshape(num, S, 2, 2)
+    return mats[:, 0] if single else mats
 
 
 # ---- scheduling -------------------------------------------------------------------------

@@ -301,14 +301,34 @@ def _noise_matrix(ctx: RankContext, gate, noise_stream):
     return noise_mod.noise_gate_matrix(gate.duration, ctx.noise_model, stream)
 
 
-def apply_gate(ctx: RankContext, gate, noise_stream=None) -> None:
+def _circuit_noise(ctx: RankContext, gates, noise_stream):
+    """Pre-draw every noise gate of a circuit in one pass (same values, same
+    stream advance as drawing gate by gate); None when there are none."""
+    durations = [g.duration for g in gates if g.kind == "noise"]
+    if not durations or ctx.is_idle:
+        return None
+    if ctx.noise_model is None:
+        raise ValueError("noise gate requires a noise model on the context")
+    stream = ctx.state_stream if noise_stream is None else noise_stream
+    if ctx.pool is not None:
+        if not isinstance(stream, noise_mod.StreamBatch):
+            stream = noise_mod.StreamBatch(stream)
+        if len(stream) != ctx.num_states:
+            raise ValueError(f"{len(stream)} noise streams for {ctx.num_states} states")
+    elif isinstance(stream, noise_mod.StreamBatch):
+        raise ValueError("a single-state context takes one noise stream")
+    return iter(noise_mod.circuit_noise_matrices(durations, ctx.noise_model, stream))
+
+
+def apply_gate(ctx: RankContext, gate, noise_stream=None, *, noise_matrix=None) -> None:
     """Queue one gate; global-qubit gates flush and exchange (runtime.py:115-152).
     Noise gates draw their matrix from `noise_stream` (default: the context's
-    state stream) and then run as one-qubit gates."""
+    state stream) -- or take a pre-drawn `noise_matrix` -- and then run as
+    one-qubit gates."""
     if ctx.is_idle:
         return
     if gate.kind == "noise":
-        u = _noise_matrix(ctx, gate, noise_stream)
+        u = _noise_matrix(ctx, gate, noise_stream) if noise_matrix is None else noise_matrix
         if u.ndim == 3:  # pool: per-state table, every qubit is local
             ctx.queue.one_qubit(gate.qubits[0], u)
             ctx.gates_applied += 1
@@ -361,8 +381,12 @@ def run_circuit(ctx: RankContext, circuit, bindings: dict | None = None,
                 noise_stream=None) -> None:
     bound = circuit.bind(bindings) if bindings else circuit
     bound.require_bound()
+    pre = _circuit_noise(ctx, bound.gates, noise_stream)
     for gate in bound.gates:
-        apply_gate(ctx, gate, noise_stream=noise_stream)
+        if gate.kind == "noise" and pre is not None:
+            apply_gate(ctx, gate, noise_matrix=next(pre))
+        else:
+            apply_gate(ctx, gate, noise_stream=noise_stream)
     ctx.flush()
 
 
@@ -495,10 +519,14 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
             raise ValueError(f"table for ${name} has {len(vals)} entries for {S} states")
     tables = {k: np.asarray(v, dtype=np.float64) for k, v in slot_tables.items()}
     q = ctx.queue
+    pre = _circuit_noise(ctx, circuit.gates, noise_stream)
     for gate in circuit.gates:
         slot = gate.slot if isinstance(getattr(gate, "param", None), str) else None
         if slot is None:
-            if ctx.pool is None or gate.kind == "noise":
+            if gate.kind == "noise":
+                apply_gate(ctx, gate, noise_matrix=next(pre))
+                continue
+            if ctx.pool is None:
                 apply_gate(ctx, gate, noise_stream=noise_stream)
                 continue
             _queue_fixed(q, gate)

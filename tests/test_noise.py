@@ -112,3 +112,26 @@ def test_noise_ensemble_csv_format():
     assert csv.splitlines() == ["trajectories,running_mean,reference", "1,1.0,0.25",
                                 "2,0.5,0.25", "3,0.5,0.25"]
     assert math.isclose(float(csv.splitlines()[-1].split(",")[1]), 0.5)
+
+
+def test_native_philox_equals_numpy_restatement():
+    rng = np.random.default_rng(4)
+    k = rng.integers(0, 2**64 - 1, size=(300, 2), dtype=np.uint64)
+    c = rng.integers(0, 2**64 - 1, size=(300, 2), dtype=np.uint64)
+    a = N._philox_block(k[:, 0], k[:, 1], c[:, 0], c[:, 1])
+    b = N.philox_block_numpy(k[:, 0], k[:, 1], c[:, 0], c[:, 1])
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_circuit_noise_matrices_equal_gate_by_gate_draws():
+    model = N.NoiseModel(20.0, 15.0)
+    durs = np.random.default_rng(0).uniform(0, 5, size=37)
+    b1 = N.StreamBatch(N.trajectory_stream(1, t) for t in range(9))
+    b2 = N.StreamBatch(N.trajectory_stream(1, t) for t in range(9))
+    got = N.circuit_noise_matrices(durs, model, b1)
+    ref = np.stack([N.noise_gate_matrices(d, model, b2) for d in durs])
+    assert bits_equal(got, ref)
+    assert [s.counter for s in b1.streams] == [3 * 37] * 9
+    s1, s2 = N.trajectory_stream(1, 3), N.trajectory_stream(1, 3)
+    one = N.circuit_noise_matrices(durs[:5], model, s1)
+    assert bits_equal(one, np.stack([N.noise_gate_matrix(d, model, s2) for d in durs[:5]]))
