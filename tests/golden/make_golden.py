@@ -345,11 +345,93 @@ def gen_noise():
          t1=np.array(20.0), t2=np.array(15.0), seed=np.array(SEED))
 
 
+def gen_cli():
+    """Reports of the reference CLI (cli.py) on small circuit/graph files,
+    for the format-compatibility tests (tests/test_gpu_cli.py).  The input
+    files are written next to the reports in tests/golden/cli/."""
+    import contextlib
+    import io
+
+    from qpool import cli
+    from qpool.circuit import serialize_circuit
+    from qpool.graphs import serialize_graph
+
+    d = os.path.join(OUT, "cli")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(SEED + 11)
+    with open(os.path.join(d, "ring.graph"), "w") as fh:
+        fh.write(serialize_graph(make_graph(4, [(0, 1), (1, 2), (2, 3), (3, 0)])))
+    g6 = random_3regular_graph(6, RandomStream(SEED, "pool", 3))
+    with open(os.path.join(d, "cubic6.graph"), "w") as fh:
+        fh.write(serialize_graph(g6))
+    # mixed gates, noise and a cut phase on 4 qubits
+    mix = ("qubits 4\nh 0\nh 1\nh 2\nh 3\nnoise 2 1.5\ndiagcost ring.graph 0.61\n"
+           "cx 3 1\nrz 0 0.9\nnoise 0 0.5\nry 2 -1.25\ncz 0 3\n")
+    with open(os.path.join(d, "mix.qc"), "w") as fh:
+        fh.write(mix)
+    # QAOA with slots on the 6-vertex cubic graph
+    lines = ["qubits 6"] + [f"h {q}" for q in range(6)]
+    for k in (1, 2):
+        lines.append(f"diagcost cubic6.graph $gamma{k}")
+        lines += [f"rx {q} $beta{k}" for q in range(6)]
+    with open(os.path.join(d, "qaoa6.qc"), "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+    # 12 qubits: random layers (no amplitude lines in the report)
+    lines = ["qubits 12"]
+    for layer in range(3):
+        for q in range(12):
+            k = ("h", "rx", "ry", "rz")[int(rng.integers(4))]
+            lines.append(f"{k} {q}" if k == "h" else f"{k} {q} {float(rng.uniform(0, 6.2))!r}")
+        lines += [f"cx {q} {q + 1}" for q in range(layer % 2, 11, 2)]
+    with open(os.path.join(d, "layers12.qc"), "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+    cases = {
+        "run_mix": ["run", "mix.qc", "--seed", "777777", "--t1", "30", "--t2", "15"],
+        "run_mix_r4": ["run", "mix.qc", "--seed", "777777", "--t1", "30", "--t2", "15",
+                       "--ranks", "4"],
+        "run_mix_s2": ["run", "mix.qc", "--seed", "5", "--t1", "30", "--t2", "15",
+                       "--ranks", "4", "--states", "2"],
+        "run_qaoa6": ["run", "qaoa6.qc", "--bind", "gamma1=0.3", "--bind", "beta1=1.1",
+                      "--bind", "$gamma2=2.2", "--bind", "beta2=0.4", "--maxcut", "cubic6.graph",
+                      "--ranks", "2"],
+        "run_layers12": ["run", "layers12.qc", "--ranks", "8"],
+        "noise_mix": ["noise-ensemble", "mix.qc", "--t1", "30", "--t2", "15",
+                      "--trajectories", "8", "--seed", "9", "--states", "2", "--ranks", "2"],
+        "noise_qaoa6": ["noise-ensemble", "qaoa6.qc", "--t1", "40", "--t2", "20",
+                        "--trajectories", "11", "--seed", "3", "--states", "3", "--ranks", "6",
+                        "--observable", "maxcut:cubic6.graph", "--bind", "gamma1=0.3",
+                        "--bind", "beta1=1.1", "--bind", "gamma2=2.2", "--bind", "beta2=0.4"],
+        "bench_gate": ["bench-gate", "--n", "7", "--ranks", "4", "--repetitions", "2"],
+    }
+    meta = {}
+    cwd = os.getcwd()
+    os.chdir(d)
+    try:
+        for name, argv in cases.items():
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                rc = cli.main(argv)
+            assert rc == 0, (name, rc)
+            text = buf.getvalue()
+            if name == "bench_gate":  # timings vary: keep qubit,messages,bytes,ranks,n
+                rows = [r.split(",") for r in text.splitlines()]
+                text = "\n".join(",".join(r[i] for i in (0, 2, 3, 4, 5)) for r in rows) + "\n"
+            with open(name + ".txt", "w") as fh:
+                fh.write(text)
+            meta[name] = argv
+    finally:
+        os.chdir(cwd)
+    with open(os.path.join(d, "cases.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+    print("wrote", len(cases), "CLI reports")
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["1q", "ctrl", "phase_obs", "cfg1", "cfg3", "cfg4", "cfg5", "acct"]
     table = {"1q": gen_1q, "ctrl": gen_ctrl, "phase_obs": gen_phase_obs, "cfg1": gen_cfg1,
              "cfg3": gen_cfg3_small, "cfg4": gen_cfg4_small, "cfg5": gen_cfg5,
-             "acct": gen_accounting, "noise": lambda: gen_noise()}
+             "acct": gen_accounting, "noise": lambda: gen_noise(), "cli": lambda: gen_cli()}
     for w in which:
         t0 = time.perf_counter()
         table[w]()
