@@ -119,7 +119,8 @@ def load(path: str | None = None):
     with _lock:
         if _lib is not None:
             return _lib
-        path = path or LIB_PATH
+        # QSB_LIB: an alternative build of the same library (tools/exp variants)
+        path = path or os.environ.get("QSB_LIB") or LIB_PATH
         if not os.path.exists(path):
             raise ImportError(
                 f"{path} is missing: build it with `python -m paper_2001_10554_b200.build` "

@@ -392,8 +392,10 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
             ++i;
         }
     }
-    if (int rc = grow(&st->d_pass, &st->pass_cap, 1)) return rc;
-    CUDA_TRY(cudaMemcpyAsync(st->d_pass, &P, sizeof(P), cudaMemcpyHostToDevice, st->stream));
+    if (!tile_pass_in_params()) {  // QSB_PASS_SMEM builds read the pass from a device copy
+        if (int rc = grow(&st->d_pass, &st->pass_cap, 1)) return rc;
+        CUDA_TRY(cudaMemcpyAsync(st->d_pass, &P, sizeof(P), cudaMemcpyHostToDevice, st->stream));
+    }
     {
         LaunchScope ls(st, kLaunchTile);
         launch_tile_pass(st->psi, P, st->d_pass, st->d_mats, ct, st->stream);

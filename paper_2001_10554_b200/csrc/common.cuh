@@ -127,6 +127,7 @@ void launch_controlled(double2* psi, int m, int num_states, int c, int t, const 
 void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
                       const CutTerms& ct, const double* mats, uint64_t offset, uint64_t stride,
                       cudaStream_t s);
+bool tile_pass_in_params();  // k_tile takes the pass as a kernel parameter
 void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                       const double* mats, const CutTerms& ct, cudaStream_t s);
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s);

@@ -152,9 +152,12 @@ __device__ __forceinline__ void reg_gate(double2 (&a)[kRegAmps], const double2 u
 }
 
 
+// TABLES: the pass has per-state matrix tables; without them every matrix is
+// the shared copy in the pass descriptor and no table load is compiled in.
+template <bool TABLES>
 __device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, const double* mats,
                                             uint64_t s) {
-    if (G.stride == 0) {
+    if (!TABLES || G.stride == 0) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) u[q] = G.u[q];  // shared memory (LDS.128 broadcast)
     } else {
@@ -165,22 +168,23 @@ __device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, con
 // Fast path: n (1..kRegLog2) uncontrolled gates on register bits 0..n-1 in
 // program order; later gates are skipped by uniform branches, so one copy of
 // the code serves every run length.
+template <bool TABLES>
 __device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* G, int n,
                                         const double* mats, uint64_t s) {
     double2 u[4];
-    gate_matrix(u, G[0], mats, s);
+    gate_matrix<TABLES>(u, G[0], mats, s);
     reg_gate<0, -1>(a, u);
     if (n > 1) {
-        gate_matrix(u, G[1], mats, s);
+        gate_matrix<TABLES>(u, G[1], mats, s);
         reg_gate<1, -1>(a, u);
         if (n > 2) {
-            gate_matrix(u, G[2], mats, s);
+            gate_matrix<TABLES>(u, G[2], mats, s);
             reg_gate<2, -1>(a, u);
             if (kRegLog2 > 3 && n > 3) {
-                gate_matrix(u, G[3], mats, s);
+                gate_matrix<TABLES>(u, G[3], mats, s);
                 reg_gate<(kRegLog2 > 3 ? 3 : 0), -1>(a, u);
                 if (kRegLog2 > 4 && n > 4) {
-                    gate_matrix(u, G[4], mats, s);
+                    gate_matrix<TABLES>(u, G[4], mats, s);
                     reg_gate<(kRegLog2 > 4 ? 4 : 0), -1>(a, u);
                 }
             }
@@ -190,21 +194,22 @@ __device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* 
 
 // The common case, a full run of kRegLog2 gates: straight-line code with no
 // branch between gates, so one gate's tail overlaps the next gate's head.
+template <bool TABLES>
 __device__ __forceinline__ void reg_seq_full(double2 (&a)[kRegAmps], const TileGate* G,
                                              const double* mats, uint64_t s) {
     double2 u[4];
-    gate_matrix(u, G[0], mats, s);
+    gate_matrix<TABLES>(u, G[0], mats, s);
     reg_gate<0, -1>(a, u);
-    gate_matrix(u, G[1], mats, s);
+    gate_matrix<TABLES>(u, G[1], mats, s);
     reg_gate<1, -1>(a, u);
-    gate_matrix(u, G[2], mats, s);
+    gate_matrix<TABLES>(u, G[2], mats, s);
     reg_gate<2, -1>(a, u);
     if (kRegLog2 > 3) {
-        gate_matrix(u, G[3], mats, s);
+        gate_matrix<TABLES>(u, G[3], mats, s);
         reg_gate<(kRegLog2 > 3 ? 3 : 0), -1>(a, u);
     }
     if (kRegLog2 > 4) {
-        gate_matrix(u, G[4], mats, s);
+        gate_matrix<TABLES>(u, G[4], mats, s);
         reg_gate<(kRegLog2 > 4 ? 4 : 0), -1>(a, u);
     }
 }
@@ -257,14 +262,16 @@ __device__ unsigned long long g_prof[8];
 #define PROF_T(v)
 #define PROF_ADD(i, a, b)
 #endif
-// Persistent CTA, one per SM, of two warp groups ("ping-pong").  Each group
-// owns a 2^12-amplitude tile buffer and walks its own tiles; the FP64 sections
-// of the two groups alternate through a pair of named barriers, so one
-// group's arithmetic always runs while the other group moves data (cp.async
-// tile loads, the shared-memory round trips between register rounds and the
-// write-back to HBM).  Barrier ids: 1,2 group-local; 3,4 "turn of group g".
+// Persistent CTAs, two per SM (QSB_TILE_MINB), each one warp group of 256
+// threads owning a 2^12-amplitude tile buffer and walking its own tiles: while
+// one CTA runs FP64 sections the other moves data (cp.async tile loads, the
+// shared-memory round trips between register rounds, the write-back to HBM),
+// interleaved by the warp schedulers.  This measured faster than one CTA of
+// two ping-pong groups handing FP64 turns over named barriers (QSB_TILE_GROUPS=2
+// QSB_TILE_MINB=1: sweep 38.1 vs 35.1 ms, QAOA step 95 vs 86 ms).
+// Barrier ids: 1,2 group-local; 3,4 "turn of group g" (ping-pong builds only).
 #ifndef QSB_TILE_GROUPS
-#define QSB_TILE_GROUPS 2
+#define QSB_TILE_GROUPS 1
 #endif
 constexpr int kGroups = QSB_TILE_GROUPS;
 #ifdef QSB_NO_PINGPONG
@@ -278,10 +285,27 @@ constexpr int kDepTables = 4;  // tile index up to 32 bits (m <= 44)
 // PHASE: the pass has cut-phase gates; GENERIC: it has gates outside the
 // uncontrolled in-order runs (controlled gates, repeated register bits).
 #ifndef QSB_TILE_MINB
-#define QSB_TILE_MINB 1
+#define QSB_TILE_MINB 2
 #endif
-template <bool PHASE, bool GENERIC>
+// The pass descriptor is a __grid_constant__ kernel parameter (~12.5 KB of
+// the 32 KB parameter space): its fields are uniform constant-bank loads, which
+// frees the registers the shared-memory copy needed (spills 136 -> 24 bytes;
+// sweep 33.6 -> 29.6 ms).  QSB_PASS_SMEM restores the shared-memory staging.
+#ifndef QSB_PASS_SMEM
+#define QSB_PASS_PARAM 1
+#endif
+template <bool PHASE, bool GENERIC, bool TABLES>
 __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
+#ifdef QSB_PASS_PARAM
+    k_tile(double2* __restrict__ psi, const __grid_constant__ TilePass pass_param,
+           const double* __restrict__ mats, const __grid_constant__ CutTerms ct) {
+    // the pass description lives in the kernel's parameter space: every field
+    // read is a uniform constant-bank load and needs no shared memory
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + kGroups * sizeof(double2) * kTileAmps);
+    uint64_t* dep = rowoff + (kTileAmps >> 3);
+    const TilePass& P = pass_param;
+#else
     k_tile(double2* __restrict__ psi, const TilePass* __restrict__ pass_dev,
            const double* __restrict__ mats, const __grid_constant__ CutTerms ct) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -300,6 +324,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
         __syncthreads();
     }
     const TilePass& P = *pass_s;
+#endif
     const int low_run = P.low_run;
     const int nrows = kTileAmps >> low_run;
     const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
@@ -349,15 +374,20 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
         for (int c = 0; c < kDepTables; ++c) out |= dep[(c << 8) | ((x >> (8 * c)) & 255)];
         return out;
     };
+    // Tile element e -> HBM offset is linear over disjoint bit sets (a
+    // deposit): off(e | f) = off(e) + off(f), and so is the smem swizzle.  The
+    // load/store element e = tid | i*kTileThreads therefore splits into a
+    // per-thread part computed once and a uniform part per i.
+    auto goff = [&](int e) { return rowoff[e >> low_run] + (uint64_t(e) & lowmask); };
+    const uint64_t goff_tid = goff(tid);
+    const int swz_tid = swz(tid);
     auto prefetch = [&](uint64_t t) {
 #ifndef QSB_NO_GMEM
         if (t < P.num_tiles) {
-            const double2* g = psi + (((t >> tps_log2) << m) | tile_base(t));
+            const double2* g = psi + (((t >> tps_log2) << m) | tile_base(t)) + goff_tid;
 #pragma unroll
-            for (int i = 0; i < kLoadsPerThread; ++i) {
-                const int e = tid + i * kTileThreads;
-                cp_async16(tile + swz(e), g + rowoff[e >> low_run] + (e & lowmask));
-            }
+            for (int i = 0; i < kLoadsPerThread; ++i)
+                cp_async16(tile + (swz_tid ^ swz(i * kTileThreads)), g + goff(i * kTileThreads));
         }
 #endif
         cp_async_commit();
@@ -384,13 +414,25 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
             const bool last = r == P.num_rounds - 1;
             const int eb = R.dlo[tid & 15] | R.dhi[tid >> kLaneLoBits];
             const int sb = R.slo[tid & 15] ^ R.shi[tid >> kLaneLoBits];
+            // register k sits at tile element eb | dk[k]; dk and its swizzle sk
+            // are linear in k's bits, so 4 basis values give all 16 positions
+            int skb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) skb[j] = R.sk[1 << j];
+            auto sk_of = [&](int k) {
+                int v = 0;
+#pragma unroll
+                for (int j = 0; j < kRegLog2; ++j)
+                    if ((k >> j) & 1) v ^= skb[j];
+                return v;
+            };
             double2 a[kRegAmps];
 #ifdef QSB_NO_SMEM_ROUND
 #pragma unroll
             for (int k = 0; k < kRegAmps; ++k) a[k] = make_double2(sb * 1e-3 + k, eb * 1e-3);
 #else
 #pragma unroll
-            for (int k = 0; k < kRegAmps; ++k) a[k] = tile[sb ^ R.sk[k]];
+            for (int k = 0; k < kRegAmps; ++k) a[k] = tile[sb ^ sk_of(k)];
 #endif
             if (last && direct) {
                 // the tile now lives in registers: the buffer is free for the next tile
@@ -430,12 +472,12 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                         continue;
                     }
                     if (G.seq == kRegLog2) {
-                        reg_seq_full(a, &G, mats, s);
+                        reg_seq_full<TABLES>(a, &G, mats, s);
                         g += kRegLog2 - 1;
                         continue;
                     }
                     if (G.seq > 0) {
-                        reg_seq(a, &G, G.seq, mats, s);
+                        reg_seq<TABLES>(a, &G, G.seq, mats, s);
                         g += G.seq - 1;
                         continue;
                     }
@@ -443,7 +485,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                         if (G.ctype == 2 && !((eb >> G.cval) & 1)) continue;
                         if (G.ctype == 3 && !((base_local >> G.cval) & 1)) continue;
                         double2 u[4];
-                        gate_matrix(u, G, mats, s);
+                        gate_matrix<TABLES>(u, G, mats, s);
                         // register control c: only pairs whose register index has bit c set
                         unsigned mask = (kRegAmps >= 32) ? 0xffffffffu : ((1u << kRegAmps) - 1);
                         if (G.ctype == 1) {
@@ -463,10 +505,17 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                 // positions 0,1,2 (128-byte rows), so every warp store is 4 full rows
 #ifndef QSB_NO_GMEM
                 if (valid) {
+                    uint64_t okb[kRegLog2];
+#pragma unroll
+                    for (int j = 0; j < kRegLog2; ++j) okb[j] = goff(R.dk[1 << j]);
+                    double2* gb = gbase + goff(eb);
 #pragma unroll
                     for (int k = 0; k < kRegAmps; ++k) {
-                        const int e = eb | R.dk[k];
-                        gbase[rowoff[e >> low_run] + (e & lowmask)] = a[k];
+                        uint64_t o = 0;
+#pragma unroll
+                        for (int j = 0; j < kRegLog2; ++j)
+                            if ((k >> j) & 1) o += okb[j];
+                        gb[o] = a[k];
                     }
                 }
 #endif
@@ -485,8 +534,14 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                 if (acc.x == 12345.678) tile[sb] = acc;  // keep the arithmetic alive
             }
 #else
+            {
+                // recompute the 16 positions instead of keeping the load
+                // addresses live across the FP64 section (they would spill)
+                int sbs = sb;
+                asm volatile("" : "+r"(sbs));
 #pragma unroll
-            for (int k = 0; k < kRegAmps; ++k) tile[sb ^ R.sk[k]] = a[k];
+                for (int k = 0; k < kRegAmps; ++k) tile[sbs ^ sk_of(k)] = a[k];
+            }
 #endif
             named_sync(gbar, kTileThreads);
             PROF_T(r4);
@@ -499,11 +554,10 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
             PROF_T(s0);
 #ifndef QSB_NO_GMEM
             if (valid) {
+                double2* gb = gbase + goff_tid;
 #pragma unroll
-                for (int i = 0; i < kLoadsPerThread; ++i) {
-                    const int e = tid + i * kTileThreads;
-                    gbase[rowoff[e >> low_run] + (e & lowmask)] = tile[swz(e)];
-                }
+                for (int i = 0; i < kLoadsPerThread; ++i)
+                    gb[goff(i * kTileThreads)] = tile[swz_tid ^ swz(i * kTileThreads)];
             }
 #endif
             named_sync(gbar, kTileThreads);
@@ -589,52 +643,83 @@ void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
                                                                        ct, mats, offset, stride);
 }
 
-size_t tile_smem_bytes() {
-    return kGroups * sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3) +
-           sizeof(TilePass) + sizeof(uint64_t) * 256 * kDepTables;
+bool tile_pass_in_params() {
+#ifdef QSB_PASS_PARAM
+    return true;
+#else
+    return false;
+#endif
 }
 
-template <bool PH, bool GE>
-void launch_tile_variant(double2* psi, const TilePass* pass_dev, const double* mats,
+size_t tile_smem_bytes() {
+#ifdef QSB_PASS_PARAM
+    const size_t pass_bytes = 0;
+#else
+    const size_t pass_bytes = sizeof(TilePass);
+#endif
+    return kGroups * sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3) +
+           pass_bytes + sizeof(uint64_t) * 256 * kDepTables;
+}
+
+template <bool PH, bool GE, bool TB>
+void launch_tile_variant(double2* psi, const TilePass& pass, const TilePass* pass_dev,
+                         const double* mats,
                          const CutTerms& ct, uint64_t num_tiles, cudaStream_t s) {
     static bool configured = false;
     static int sms = 148, per_sm = 1;
     const size_t smem = tile_smem_bytes();
     if (!configured) {
-        cudaFuncSetAttribute(k_tile<PH, GE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_tile<PH, GE, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<PH, GE>, kCtaThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<PH, GE, TB>, kCtaThreads, smem);
         if (per_sm < 1) per_sm = 1;
         configured = true;
     }
     uint64_t grid = uint64_t(sms) * per_sm;
     const uint64_t need = (num_tiles + kGroups - 1) / kGroups;
     if (grid > need) grid = need;
-    k_tile<PH, GE><<<unsigned(grid), kCtaThreads, smem, s>>>(psi, pass_dev, mats, ct);
+#ifdef QSB_PASS_PARAM
+    (void)pass_dev;
+    k_tile<PH, GE, TB><<<unsigned(grid), kCtaThreads, smem, s>>>(psi, pass, mats, ct);
+#else
+    (void)pass;
+    k_tile<PH, GE, TB><<<unsigned(grid), kCtaThreads, smem, s>>>(psi, pass_dev, mats, ct);
+#endif
 }
 
 void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                       const double* mats, const CutTerms& ct, cudaStream_t s) {
-    bool phase = false, generic = false;
+    bool phase = false, generic = false, tables = false;
     for (int r = 0; r < pass.num_rounds; ++r) {
         const Round& R = pass.rounds[r];
         for (int g = R.first_gate; g < R.first_gate + R.num_gates; ++g) {
             const TileGate& G = pass.gates[g];
             if (G.kind == QS_KIND_CUTPHASE) {
                 phase = true;
-            } else if (G.seq > 0) {
-                g += G.seq - 1;
             } else {
-                generic = true;
+                // a sequence run covers G.seq gates; any of them may use a table
+                const int run = G.seq > 0 ? G.seq : 1;
+                for (int j = 0; j < run; ++j) tables |= pass.gates[g + j].stride != 0;
+                if (G.seq > 0) g += G.seq - 1;
+                else generic = true;
             }
         }
     }
-    if (phase && generic) launch_tile_variant<true, true>(psi, pass_dev, mats, ct, pass.num_tiles, s);
-    else if (phase) launch_tile_variant<true, false>(psi, pass_dev, mats, ct, pass.num_tiles, s);
-    else if (generic) launch_tile_variant<false, true>(psi, pass_dev, mats, ct, pass.num_tiles, s);
-    else launch_tile_variant<false, false>(psi, pass_dev, mats, ct, pass.num_tiles, s);
+    const uint64_t nt = pass.num_tiles;
+#define QSB_TILE_CASE(PH, GE, TB) \
+    if (phase == PH && generic == GE && tables == TB) \
+        return launch_tile_variant<PH, GE, TB>(psi, pass, pass_dev, mats, ct, nt, s);
+    QSB_TILE_CASE(false, false, false)
+    QSB_TILE_CASE(false, false, true)
+    QSB_TILE_CASE(false, true, false)
+    QSB_TILE_CASE(false, true, true)
+    QSB_TILE_CASE(true, false, false)
+    QSB_TILE_CASE(true, false, true)
+    QSB_TILE_CASE(true, true, false)
+    QSB_TILE_CASE(true, true, true)
+#undef QSB_TILE_CASE
 }
 
 int prof_read(unsigned long long* out) {
