@@ -152,16 +152,18 @@ __device__ __forceinline__ void reg_gate(double2 (&a)[kRegAmps], const double2 u
 }
 
 
-// TABLES: the pass has per-state matrix tables; without them every matrix is
-// the shared copy in the pass descriptor and no table load is compiled in.
+// TABLES: the pass has per-state matrix tables.  The tile's rows of those
+// tables are staged into shared memory with the tile itself (tm: this gate's
+// 4 entries there); without tables every matrix is the shared copy in the
+// pass descriptor and no table access is compiled in.
 template <bool TABLES>
-__device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, const double* mats,
-                                            uint64_t s) {
+__device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, const double2* tm) {
     if (!TABLES || G.stride == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) u[q] = G.u[q];  // shared memory (LDS.128 broadcast)
+        for (int q = 0; q < 4; ++q) u[q] = G.u[q];  // parameter space (uniform)
     } else {
-        load_u(u, mats + G.offset + s * G.stride);  // per-state table in global memory
+#pragma unroll
+        for (int q = 0; q < 4; ++q) u[q] = tm[q];   // staged row (LDS.128 broadcast)
     }
 }
 
@@ -170,21 +172,21 @@ __device__ __forceinline__ void gate_matrix(double2 u[4], const TileGate& G, con
 // the code serves every run length.
 template <bool TABLES>
 __device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* G, int n,
-                                        const double* mats, uint64_t s) {
+                                        const double2* tm) {
     double2 u[4];
-    gate_matrix<TABLES>(u, G[0], mats, s);
+    gate_matrix<TABLES>(u, G[0], tm);
     reg_gate<0, -1>(a, u);
     if (n > 1) {
-        gate_matrix<TABLES>(u, G[1], mats, s);
+        gate_matrix<TABLES>(u, G[1], tm + 4);
         reg_gate<1, -1>(a, u);
         if (n > 2) {
-            gate_matrix<TABLES>(u, G[2], mats, s);
+            gate_matrix<TABLES>(u, G[2], tm + 8);
             reg_gate<2, -1>(a, u);
             if (kRegLog2 > 3 && n > 3) {
-                gate_matrix<TABLES>(u, G[3], mats, s);
+                gate_matrix<TABLES>(u, G[3], tm + 12);
                 reg_gate<(kRegLog2 > 3 ? 3 : 0), -1>(a, u);
                 if (kRegLog2 > 4 && n > 4) {
-                    gate_matrix<TABLES>(u, G[4], mats, s);
+                    gate_matrix<TABLES>(u, G[4], tm + 16);
                     reg_gate<(kRegLog2 > 4 ? 4 : 0), -1>(a, u);
                 }
             }
@@ -196,20 +198,20 @@ __device__ __forceinline__ void reg_seq(double2 (&a)[kRegAmps], const TileGate* 
 // branch between gates, so one gate's tail overlaps the next gate's head.
 template <bool TABLES>
 __device__ __forceinline__ void reg_seq_full(double2 (&a)[kRegAmps], const TileGate* G,
-                                             const double* mats, uint64_t s) {
+                                             const double2* tm) {
     double2 u[4];
-    gate_matrix<TABLES>(u, G[0], mats, s);
+    gate_matrix<TABLES>(u, G[0], tm);
     reg_gate<0, -1>(a, u);
-    gate_matrix<TABLES>(u, G[1], mats, s);
+    gate_matrix<TABLES>(u, G[1], tm + 4);
     reg_gate<1, -1>(a, u);
-    gate_matrix<TABLES>(u, G[2], mats, s);
+    gate_matrix<TABLES>(u, G[2], tm + 8);
     reg_gate<2, -1>(a, u);
     if (kRegLog2 > 3) {
-        gate_matrix<TABLES>(u, G[3], mats, s);
+        gate_matrix<TABLES>(u, G[3], tm + 12);
         reg_gate<(kRegLog2 > 3 ? 3 : 0), -1>(a, u);
     }
     if (kRegLog2 > 4) {
-        gate_matrix<TABLES>(u, G[4], mats, s);
+        gate_matrix<TABLES>(u, G[4], tm + 16);
         reg_gate<(kRegLog2 > 4 ? 4 : 0), -1>(a, u);
     }
 }
@@ -325,6 +327,23 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
     }
     const TilePass& P = *pass_s;
 #endif
+    // per-round thread -> tile element deposits (dlo|slo<<16, dhi|shi<<16) in
+    // shared memory: indexed by thread id they would be divergent (serialised)
+    // constant-bank reads
+    uint32_t* rlo = reinterpret_cast<uint32_t*>(dep + 256 * kDepTables);
+    uint32_t* rhi = rlo + kMaxRounds * (1 << kLaneLoBits);
+    // two buffers of staged per-state matrix rows (tile it uses buffer it & 1)
+    double2* tmat = reinterpret_cast<double2*>(rhi + kMaxRounds * (1 << kLaneHiBits));
+    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneLoBits); i += kCtaThreads) {
+        const Round& R = P.rounds[i >> kLaneLoBits];
+        const int v = i & ((1 << kLaneLoBits) - 1);
+        rlo[i] = uint32_t(R.dlo[v]) | (uint32_t(R.slo[v]) << 16);
+    }
+    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneHiBits); i += kCtaThreads) {
+        const Round& R = P.rounds[i >> kLaneHiBits];
+        const int v = i & ((1 << kLaneHiBits) - 1);
+        rhi[i] = uint32_t(R.dhi[v]) | (uint32_t(R.shi[v]) << 16);
+    }
     const int low_run = P.low_run;
     const int nrows = kTileAmps >> low_run;
     const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
@@ -381,19 +400,30 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
     auto goff = [&](int e) { return rowoff[e >> low_run] + (uint64_t(e) & lowmask); };
     const uint64_t goff_tid = goff(tid);
     const int swz_tid = swz(tid);
-    auto prefetch = [&](uint64_t t) {
+    const int ngates = P.rounds[P.num_rounds - 1].first_gate + P.rounds[P.num_rounds - 1].num_gates;
+    auto prefetch = [&](uint64_t t, int buf) {
 #ifndef QSB_NO_GMEM
         if (t < P.num_tiles) {
-            const double2* g = psi + (((t >> tps_log2) << m) | tile_base(t)) + goff_tid;
+            const uint64_t st = t >> tps_log2;
+            const double2* g = psi + ((st << m) | tile_base(t)) + goff_tid;
 #pragma unroll
             for (int i = 0; i < kLoadsPerThread; ++i)
                 cp_async16(tile + (swz_tid ^ swz(i * kTileThreads)), g + goff(i * kTileThreads));
+            if (TABLES) {
+                // this state's row of every per-state matrix table: 4 x 16 B per gate
+                double2* tm = tmat + buf * (4 * kMaxPassGates);
+                for (int c = tid; c < 4 * ngates; c += kTileThreads) {
+                    const TileGate& G = P.gates[c >> 2];
+                    if (G.stride != 0 && G.kind != QS_KIND_CUTPHASE)
+                        cp_async16(tm + c, mats + G.offset + st * G.stride + 2 * (c & 3));
+                }
+            }
         }
 #endif
         cp_async_commit();
     };
     const bool direct = P.direct_store != 0;
-    prefetch(uint64_t(blockIdx.x) * kGroups + group);
+    prefetch(uint64_t(blockIdx.x) * kGroups + group, 0);
 
     for (uint64_t it = 0; it < iters; ++it) {
         const uint64_t tile_id = it * stride_tiles + uint64_t(blockIdx.x) * kGroups + group;
@@ -402,6 +432,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
         const uint64_t s = tile_id >> tps_log2;
         const uint64_t base_local = tile_base(tile_id);
         double2* gbase = psi + ((s << m) | base_local);
+        const double2* tm_cur = tmat + int(it & 1) * (4 * kMaxPassGates);
         PROF_T(t0);
         cp_async_wait_all();
         named_sync(gbar, kTileThreads);
@@ -412,8 +443,10 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
             PROF_T(r0);
             const Round& R = P.rounds[r];
             const bool last = r == P.num_rounds - 1;
-            const int eb = R.dlo[tid & 15] | R.dhi[tid >> kLaneLoBits];
-            const int sb = R.slo[tid & 15] ^ R.shi[tid >> kLaneLoBits];
+            const uint32_t lo = rlo[(r << kLaneLoBits) | (tid & ((1 << kLaneLoBits) - 1))];
+            const uint32_t hi = rhi[(r << kLaneHiBits) | (tid >> kLaneLoBits)];
+            const int eb = int((lo | hi) & 0xffff);
+            const int sb = int((lo ^ hi) >> 16);
             // register k sits at tile element eb | dk[k]; dk and its swizzle sk
             // are linear in k's bits, so 4 basis values give all 16 positions
             int skb[kRegLog2];
@@ -437,7 +470,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
             if (last && direct) {
                 // the tile now lives in registers: the buffer is free for the next tile
                 named_sync(gbar, kTileThreads);
-                prefetch(next_id);
+                prefetch(next_id, int((it + 1) & 1));
             }
 
             PROF_T(r1);
@@ -472,12 +505,12 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                         continue;
                     }
                     if (G.seq == kRegLog2) {
-                        reg_seq_full<TABLES>(a, &G, mats, s);
+                        reg_seq_full<TABLES>(a, &G, tm_cur + 4 * g);
                         g += kRegLog2 - 1;
                         continue;
                     }
                     if (G.seq > 0) {
-                        reg_seq<TABLES>(a, &G, G.seq, mats, s);
+                        reg_seq<TABLES>(a, &G, G.seq, tm_cur + 4 * g);
                         g += G.seq - 1;
                         continue;
                     }
@@ -485,7 +518,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                         if (G.ctype == 2 && !((eb >> G.cval) & 1)) continue;
                         if (G.ctype == 3 && !((base_local >> G.cval) & 1)) continue;
                         double2 u[4];
-                        gate_matrix<TABLES>(u, G, mats, s);
+                        gate_matrix<TABLES>(u, G, tm_cur + 4 * g);
                         // register control c: only pairs whose register index has bit c set
                         unsigned mask = (kRegAmps >= 32) ? 0xffffffffu : ((1u << kRegAmps) - 1);
                         if (G.ctype == 1) {
@@ -561,7 +594,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
             }
 #endif
             named_sync(gbar, kTileThreads);
-            prefetch(next_id);
+            prefetch(next_id, int((it + 1) & 1));
             PROF_T(s1);
             PROF_ADD(5, s0, s1);
         }
@@ -658,7 +691,9 @@ size_t tile_smem_bytes() {
     const size_t pass_bytes = sizeof(TilePass);
 #endif
     return kGroups * sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3) +
-           pass_bytes + sizeof(uint64_t) * 256 * kDepTables;
+           pass_bytes + sizeof(uint64_t) * 256 * kDepTables +
+           sizeof(uint32_t) * kMaxRounds * ((1 << kLaneLoBits) + (1 << kLaneHiBits)) +
+           2 * sizeof(double2) * 4 * kMaxPassGates;
 }
 
 template <bool PH, bool GE, bool TB>
