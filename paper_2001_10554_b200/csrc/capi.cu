@@ -253,7 +253,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
                 const double* mats_host) {
     if (count > kMaxPassGates) return fail(QS_ERR_VALUE, "planner: pass too long");
     // tile bits: the targets, plus qubits 0..2 for 128-byte rows, filled upward
-    uint64_t need = 0x7;
+    uint64_t need = kLowMask;
     for (int i = 0; i < count; ++i)
         if (prog[first + i].kind != QS_KIND_CUTPHASE) need |= uint64_t(1) << prog[first + i].target;
     for (int b = 0; __builtin_popcountll(need) < kTileLog2 && b < st->m; ++b) need |= uint64_t(1) << b;
@@ -345,7 +345,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         bool low_free = true;
         for (int p : all_pos.back())
             if (p < 3) low_free = false;
-        P.direct_store = (low_free && P.low_run >= 3) ? 1 : 0;
+        P.direct_store = (low_free && P.low_run >= 3 && kLowBits >= 3) ? 1 : 0;
     }
     for (int i = 0; i < count; ++i) {
         const qs_gate& g = prog[first + i];
@@ -421,7 +421,7 @@ std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool f
     while (i < count) {
         int j = i + 1;
         if (tile_ok) {
-            uint64_t need = 0x7;
+            uint64_t need = kLowMask;
             if (gates[i].kind != QS_KIND_CUTPHASE) need |= uint64_t(1) << gates[i].target;
             uint64_t round_set = gates[i].kind != QS_KIND_CUTPHASE ? (uint64_t(1) << gates[i].target) : 0;
             int rounds = 1;

@@ -70,6 +70,13 @@ __device__ __forceinline__ int cut_of(uint64_t i, const CutTerms& ct) {
 constexpr int kTileLog2 = QSB_TILE_LOG2;  // 2^12 amplitudes = 64 KiB of shared memory
 constexpr int kRegLog2 = QSB_REG_LOG2;    // 16 amplitudes per thread = 4 register qubits
 constexpr int kTileThreads = 1 << (kTileLog2 - kRegLog2);
+// low qubits every tile keeps (2^kLowBits contiguous amplitudes = 16 << kLowBits
+// bytes per HBM row segment)
+#ifndef QSB_LOW_BITS
+#define QSB_LOW_BITS 3
+#endif
+constexpr int kLowBits = QSB_LOW_BITS;
+constexpr uint64_t kLowMask = (uint64_t(1) << kLowBits) - 1;
 constexpr int kLaneLoBits = 4;
 constexpr int kLaneHiBits = kTileLog2 - kRegLog2 - kLaneLoBits;
 constexpr int kMaxRounds = 24;

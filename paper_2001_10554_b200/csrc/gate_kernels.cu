@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
     // read is a uniform constant-bank load and needs no shared memory
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + kGroups * sizeof(double2) * kTileAmps);
-    uint64_t* dep = rowoff + (kTileAmps >> 3);
+    uint64_t* dep = rowoff + (kTileAmps >> kLowBits);
     const TilePass& P = pass_param;
 #else
     k_tile(double2* __restrict__ psi, const TilePass* __restrict__ pass_dev,
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + kGroups * sizeof(double2) * kTileAmps);
     TilePass* pass_s = reinterpret_cast<TilePass*>(smem_raw + kGroups * sizeof(double2) * kTileAmps +
-                                                   sizeof(uint64_t) * (kTileAmps >> 3));
+                                                   sizeof(uint64_t) * (kTileAmps >> kLowBits));
     // deposit tables: tile index byte c -> its bits spread over the non-tile qubits
     uint64_t* dep = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(pass_s) +
                                                 sizeof(TilePass));
@@ -490,16 +490,23 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                                                       (uint64_t(eb) & lowmask));
                         int cut = cut_of(i, ct);
                         a[0] = cmul(a[0], __ldg(lut + cut));
+                        // per register bit j (uniform): its qubit, neighbour mask, degree
+                        int rq[kRegLog2], degq[kRegLog2];
+                        uint64_t nbq[kRegLog2];
+#pragma unroll
+                        for (int j = 0; j < kRegLog2; ++j) {
+                            rq[j] = P.tile_bits[__ffs(R.dk[1 << j]) - 1];
+                            nbq[j] = P.nbr[rq[j]];
+                            degq[j] = __popcll(nbq[j]);
+                        }
 #pragma unroll
                         for (int step = 1; step < kRegAmps; ++step) {
                             const int j = ctz_c(step);           // bit flipped by Gray step
                             const int gray = step ^ (step >> 1);  // register index reached
-                            const int r = P.tile_bits[__ffs(R.dk[1 << j]) - 1];
-                            const uint64_t nb = P.nbr[r];
-                            const uint64_t bitr = (i >> r) & 1;
-                            const int now_cut = __popcll((i ^ (uint64_t(0) - bitr)) & nb);
-                            cut += __popcll(nb) - 2 * now_cut;
-                            i ^= uint64_t(1) << r;
+                            const uint64_t bitr = (i >> rq[j]) & 1;
+                            const int now_cut = __popcll((i ^ (uint64_t(0) - bitr)) & nbq[j]);
+                            cut += degq[j] - 2 * now_cut;
+                            i ^= uint64_t(1) << rq[j];
                             a[gray] = cmul(a[gray], __ldg(lut + cut));
                         }
                         continue;
@@ -690,7 +697,7 @@ size_t tile_smem_bytes() {
 #else
     const size_t pass_bytes = sizeof(TilePass);
 #endif
-    return kGroups * sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> 3) +
+    return kGroups * sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> kLowBits) +
            pass_bytes + sizeof(uint64_t) * 256 * kDepTables +
            sizeof(uint32_t) * kMaxRounds * ((1 << kLaneLoBits) + (1 << kLaneHiBits)) +
            2 * sizeof(double2) * 4 * kMaxPassGates;

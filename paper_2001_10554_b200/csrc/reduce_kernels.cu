@@ -92,15 +92,48 @@ __global__ void __launch_bounds__(kThreads)
     __shared__ double wsum[kThreads / 32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t chunks_per_state = elems_per_state >> kWideLog2;
+    // MAXCUT: a thread's 8 elements differ in qubits 5,6,7 only, so after one
+    // full cut_of the other 7 cuts follow by a Gray-code walk (flipping qubit
+    // r changes the cut by deg(r) - 2 * (edges of r currently cut))
+    const bool walk = psi != nullptr && kind == QS_OBS_MAXCUT;
+    uint64_t nbq[3] = {0, 0, 0};
+    int degq[3] = {0, 0, 0};
+    if (walk) {
+        for (int b = 0; b < 3; ++b) {
+            const int r = 5 + b;
+            for (int k = 0; k < ct.count; ++k) {
+                const int sh = ct.shift[k];
+                if ((ct.mask[k] >> r) & 1) nbq[b] |= uint64_t(1) << (r + sh);
+                if (r >= sh && ((ct.mask[k] >> (r - sh)) & 1)) nbq[b] |= uint64_t(1) << (r - sh);
+            }
+            degq[b] = __popcll(nbq[b]);
+        }
+    }
     for (uint64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
         const uint64_t s = c / chunks_per_state;
         const uint64_t first = ((c - s * chunks_per_state) << kWideLog2) + warp * 256 + lane;
         double v[8];
+        if (walk) {
+            const double2* p = psi + (s << m) + first;
+            uint64_t i = rank_offset | first;
+            int cut = cut_of(i, ct);
+            v[0] = __dmul_rn(double(cut), abs2(p[0]));
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const uint64_t j = first + i * 32;
-            v[i] = psi ? obs_value(psi, m, kind, q, rank_offset, ct, s, j)
-                       : src[s * elems_per_state + j];
+            for (int step = 1; step < 8; ++step) {
+                const int b = step & 1 ? 0 : (step & 2 ? 1 : 2);  // bit flipped
+                const int gray = step ^ (step >> 1);               // element reached
+                const uint64_t bit = (i >> (5 + b)) & 1;
+                cut += degq[b] - 2 * __popcll((i ^ (uint64_t(0) - bit)) & nbq[b]);
+                i ^= uint64_t(1) << (5 + b);
+                v[gray] = __dmul_rn(double(cut), abs2(p[gray * 32]));
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint64_t j = first + i * 32;
+                v[i] = psi ? obs_value(psi, m, kind, q, rank_offset, ct, s, j)
+                           : src[s * elems_per_state + j];
+            }
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = warp_tree(v[i]);
