@@ -466,13 +466,13 @@ def pso_step(pos, vel, best_pos, best_val, gbest, values, rng, lo=0.0, hi=np.pi)
 
 
 def qaoa_tables(positions, depth):
-    from paper_2001_10554_b200.circuit import qaoa_bindings
-
-    S = positions.shape[0]
+    """Per-state slot tables: qaoa_bindings (circuit.py) for every row, as
+    columns (gamma_k = x[k-1], beta_k = 2 * x[p+k-1]; same IEEE products)."""
+    pos = np.asarray(positions, dtype=np.float64)
     tables = {}
-    for s in range(S):
-        for name, v in qaoa_bindings(depth, positions[s]).items():
-            tables.setdefault(name, np.empty(S))[s] = v
+    for k in range(1, depth + 1):
+        tables[f"gamma{k}"] = pos[:, k - 1].copy()
+        tables[f"beta{k}"] = 2.0 * pos[:, depth + k - 1]
     return tables
 
 
@@ -680,15 +680,28 @@ def run_noise(args, dist, comm, world, rank, local):
     ctx.norm_check_interval = 0
     st = ctx.state
     edges = np.asarray(graph.edges, dtype=np.int32)
+    durations = [g.duration for g in circ.gates if g.kind == "noise"]
+    from concurrent.futures import ThreadPoolExecutor
+
+    pool = ThreadPoolExecutor(1)
+
+    def draw(k):
+        # round k's trajectories: k*S + first .. k*S + first + count - 1
+        batch = noise.StreamBatch(noise.trajectory_stream(args.seed, k * S + first + s)
+                                  for s in range(count))
+        return noise.circuit_noise_matrices(durations, model, batch)
+
     round_no = [0]
+    pending = [pool.submit(draw, 0)]
 
     def step():
-        base = round_no[0] * S + first
+        # the next round's host draws overlap this round's device work
+        k = round_no[0]
         round_no[0] += 1
+        mats = pending[0].result()
         runtime.reset_state(ctx)
-        batch = noise.StreamBatch(noise.trajectory_stream(args.seed, base + s)
-                                  for s in range(count))
-        runtime.run_circuit(ctx, circ, noise_stream=batch)
+        runtime.run_circuit(ctx, circ, noise_matrices=mats)
+        pending[0] = pool.submit(draw, k + 1)
         return ctx.pool.observable(3, 0, edges)
 
     for _ in range(args.warmup):

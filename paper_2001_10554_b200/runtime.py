@@ -378,10 +378,14 @@ def apply_gate(ctx: RankContext, gate, noise_stream=None, *, noise_matrix=None) 
 
 
 def run_circuit(ctx: RankContext, circuit, bindings: dict | None = None,
-                noise_stream=None) -> None:
+                noise_stream=None, noise_matrices=None) -> None:
+    """Queue and flush every gate (runtime.py:155-162).  `noise_matrices`:
+    the circuit's noise gates already drawn (noise.circuit_noise_matrices),
+    e.g. by a worker thread while the previous round ran."""
     bound = circuit.bind(bindings) if bindings else circuit
     bound.require_bound()
-    pre = _circuit_noise(ctx, bound.gates, noise_stream)
+    pre = (iter(noise_matrices) if noise_matrices is not None
+           else _circuit_noise(ctx, bound.gates, noise_stream))
     for gate in bound.gates:
         if gate.kind == "noise" and pre is not None:
             apply_gate(ctx, gate, noise_matrix=next(pre))
@@ -589,6 +593,11 @@ def run_noise_ensemble(ctx: RankContext, circuit, model, trajectories: int, obse
         run_circuit(ctx, circuit, noise_stream=stream_fn(first))
         return np.atleast_1d(np.asarray(observe(ctx), dtype=np.float64))
 
+    durations = [g.duration for g in circuit.gates if g.kind == "noise"]
+
+    def draw(first):
+        return noise_mod.circuit_noise_matrices(durations, model, streams(first))
+
     saved = ctx.noise_model
     try:
         if ctx.pool is None:
@@ -596,13 +605,23 @@ def run_noise_ensemble(ctx: RankContext, circuit, model, trajectories: int, obse
         else:  # every state runs trajectory 0's (noiseless) draws
             ref = float(run(noise_mod.NOISELESS, 0, lambda _f: noise_mod.StreamBatch(
                 noise_mod.trajectory_stream(seed, 0) for _ in range(S)))[0])
-        for k in range(-(-trajectories // groups)):
-            first = k * groups + ctx.state_offset
-            if first >= trajectories:
-                continue
-            vals = run(model, first, streams)
-            count = min(S, trajectories - first)
-            values[first:first + count] = vals[:count]
+        firsts = [k * groups + ctx.state_offset for k in range(-(-trajectories // groups))]
+        firsts = [f for f in firsts if f < trajectories]
+        # round k+1's noise is drawn on a worker thread while round k runs
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(1) as ex:
+            fut = ex.submit(draw, firsts[0]) if firsts else None
+            for idx, first in enumerate(firsts):
+                mats = fut.result()
+                ctx.noise_model = model
+                reset_state(ctx)
+                run_circuit(ctx, circuit, noise_matrices=mats)
+                if idx + 1 < len(firsts):
+                    fut = ex.submit(draw, firsts[idx + 1])
+                vals = np.atleast_1d(np.asarray(observe(ctx), dtype=np.float64))
+                count = min(S, trajectories - first)
+                values[first:first + count] = vals[:count]
     finally:
         ctx.noise_model = saved
     return ref, values
