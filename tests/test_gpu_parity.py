@@ -600,3 +600,52 @@ def test_exchange_amplitudes_full_duplex():
     assert bits_equal(sv.read_amplitudes(p), b)
     sv.exchange_amplitudes(p, a, out)
     assert bits_equal(out, b) and bits_equal(p.amplitudes, a)
+
+
+@pytest.mark.slow
+def test_n33_max_single_gpu_size_layer_roundtrip():
+    """Config 4's per-GPU size (2^33 amplitudes, 128 GiB) on one GPU: a
+    single gate on the top qubit is bit-exact on sampled pairs; one fused
+    config-4 layer (Haar on all 33 qubits + CX(q, 32-q)) keeps the norm and
+    its adjoint layer returns sampled blocks to within 1e-12."""
+    from paper_2001_10554_b200 import _native as N
+    n = 33
+    st = N.DeviceState(n, n)
+    N.call("qs_init_gaussian", st.handle, 5)
+    norm = st.observable(N.QS_OBS_NORM)[0]
+    N.call("qs_scale", st.handle, 1.0 / np.sqrt(norm))
+    rng = np.random.default_rng(33)
+    blk = 1 << 12
+    offs = [int(o) * blk for o in rng.integers(0, (1 << (n - 1)) // blk, size=24)]
+
+    def read(offsets):
+        return [st.download(offset=o, count=blk).copy() for o in offsets]
+
+    # top qubit: pairs (o + i, o + i + 2^32)
+    u = ogates.random_unitary_2x2(rng)
+    lo_before, hi_before = read(offs), read([o + (1 << 32) for o in offs])
+    st.apply_program([N.QsGate(0, n - 1, -1, 0, 0, 0)], u.view(np.float64).ravel(), fuse=False)
+    lo_after, hi_after = read(offs), read([o + (1 << 32) for o in offs])
+    for lb, hb, la, ha in zip(lo_before, hi_before, lo_after, hi_after):
+        a, b = osv.pair_update(lb, hb, u)
+        assert bits_equal(la, a) and bits_equal(ha, b)
+    # one config-4 layer and its adjoint
+    samples = offs + [o + (1 << 32) for o in offs]
+    start = read(samples)
+    us = [ogates.random_unitary_2x2(rng) for _ in range(n)]
+    X = qs.gates.PAULI_X
+    q = runtime.GateQueue(st, fuse=True)
+    for k in range(n):
+        q.one_qubit(k, us[k])
+    for c in range(n // 2):
+        q.controlled(c, n - 1 - c, X)
+    q.flush()
+    assert abs(st.observable(N.QS_OBS_NORM)[0] - 1.0) < 1e-10
+    for c in reversed(range(n // 2)):
+        q.controlled(c, n - 1 - c, X)
+    for k in reversed(range(n)):
+        q.one_qubit(k, np.ascontiguousarray(us[k].conj().T))
+    q.flush()
+    back = read(samples)
+    assert max(max_dev(b, s) for b, s in zip(back, start)) <= TOL
+    del st
