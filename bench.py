@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--local-qubits", type=int, default=30)
     ap.add_argument("--no-fuse", action="store_true")
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "qaoa", "cfg4", "noise"])
+    ap.add_argument("--workload", default="sweep",
+                    choices=["sweep", "qaoa", "cfg3", "cfg4", "noise"])
     ap.add_argument("--seed", type=int, default=20260809)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -267,8 +268,27 @@ def run_ours(args):
     from paper_2001_10554_b200.circuit import GateSpec
 
     cx_pairs = [(q, n - 1 - q) for q in range(n // 2)] if args.workload == "cfg4" else []
+    cfg3 = args.workload == "cfg3"
+    if cfg3:
+        # config 3: 64 seeded (control, target) pairs, control != target, each
+        # getting CNOT, CPhase(phi ~ U[0,2pi)) and a controlled Haar 2x2
+        prng = np.random.default_rng(args.seed + 3)
+        pairs = []
+        while len(pairs) < 64:
+            c, t = (int(x) for x in prng.integers(0, n, size=2))
+            if c != t:
+                pairs.append((c, t))
+        sweeps = [[(prng.uniform(0, 2 * np.pi), haar(prng)) for _ in pairs]
+                  for _ in range(total_steps)]
 
     def step(us):
+        if cfg3:
+            for (c, t), (phi, u) in zip(pairs, us):
+                runtime.apply_gate(ctx, GateSpec("cx", (c, t)))
+                runtime.apply_gate(ctx, GateSpec("cphase", (c, t), float(phi)))
+                runtime.apply_gate(ctx, GateSpec("cu", (c, t), matrix=u))
+            ctx.flush()
+            return
         # config 2: Haar gate on every qubit; config 4 adds CX(q, n-1-q), q < n/2
         # (pairs cross the local/global boundary: routed like the reference)
         for k in range(n):
@@ -297,11 +317,15 @@ def run_ours(args):
     clock = clocks.stop()
     barrier(dist)
     ms_total = max_over_ranks(dist, ms_dev)
-    gates_per_step = n + len(cx_pairs)
+    gates_per_step = 3 * 64 if cfg3 else n + len(cx_pairs)
     units_per_step = gates_per_step * (2.0 ** n) / 2.0 ** 30
     value = units_per_step * args.steps / (ms_total / 1e3)
-    # algorithmic: every 1q gate r+w of the slice, a CX the control=1 half
-    bytes_per_step_per_gpu = 32.0 * (2 ** m) * n + 16.0 * (2 ** m) * len(cx_pairs)
+    # algorithmic: every 1q gate r+w of the slice, a CX the control=1 half,
+    # a CPhase (diag(1,z)) the control=1, target=1 quarter
+    if cfg3:
+        bytes_per_step_per_gpu = (16.0 + 8.0 + 16.0) * (2 ** m) * 64
+    else:
+        bytes_per_step_per_gpu = 32.0 * (2 ** m) * n + 16.0 * (2 ** m) * len(cx_pairs)
     hbm_gbs = bytes_per_step_per_gpu * world * args.steps / (ms_total / 1e3) / 1e9
 
     # dominant kernel and its roofline
@@ -340,7 +364,8 @@ def run_ours(args):
     passes_per_step = len(launch_ms) / max(args.steps, 1)
     actual_gbs = 32.0 * (2 ** m) * passes_per_step * args.steps / (ms_dev / 1e3) / 1e9
     # numpy-exact pair update: 20 FP64 ops per pair (a CX touches half the pairs)
-    fp64_ops = 10.0 * (2 ** m) * (n + 0.5 * len(cx_pairs)) * args.steps
+    fp64_ops = ((5.0 + 1.0 + 5.0) * (2 ** m) * 64 * args.steps if cfg3 else
+                10.0 * (2 ** m) * (n + 0.5 * len(cx_pairs)) * args.steps)
     fp64_rate = fp64_ops / (ms_dev / 1e3) / 1e12
     if rank == 0:
         line = {
@@ -351,6 +376,9 @@ def run_ours(args):
             "config": {
                 "workload": (f"config 2 sweep: Haar 2x2 on each of the {n} qubits in turn, "
                              if args.workload == "sweep" else
+                             "config 3: CNOT, CPhase(phi) and controlled Haar 2x2 on each of "
+                             "64 seeded (control, target) pairs, "
+                             if cfg3 else
                              f"config 4 layer: Haar 2x2 on each of the {n} qubits, then "
                              f"CX(q, n-1-q) for q < {n // 2}, ")
                             + f"fresh unitaries per step, normalised Gaussian state, "
