@@ -10,7 +10,7 @@ from __future__ import annotations
 
 from . import _native
 from ._native import LocalityError, TransportError, device_count
-from . import gates, graphs, statevector, distribution, runtime, circuit, pool, noise  # noqa: E402
+from . import gates, graphs, statevector, distribution, runtime, circuit, pool, noise, optimize  # noqa: E402
 from .register import QubitRegister
 from .statevector import (StatePartition, allocate_partition, full_state_bytes, init_basis_state,
                           init_uniform, apply_local_one_qubit_gate, apply_local_controlled_gate,

@@ -13,6 +13,9 @@ QubitRegister parses the ``run`` report) can drive this core unchanged:
                   counters per repetition
   noise-ensemble  running mean of a noisy circuit's observable, CSV
                   trajectories,running_mean,reference (cli.py:288-339)
+  qaoa-pso        PSO over QAOA/MaxCut on random 3-regular graphs, CSV
+                  evaluations,mean_ratio,step (cli.py:240-274); each chunk of
+                  particles is one pool program on the device
 
 Ranks are emulated on one GPU as threads (``--ranks``), exactly the
 reference's in-process transport; multi-GPU runs use torchrun + TorchComm
@@ -79,6 +82,14 @@ def build_parser() -> argparse.ArgumentParser:
     e.add_argument("--observable", default="prob:0", help="prob:<qubit> or maxcut:<graphfile>")
     e.add_argument("--bind", action="append", default=[], metavar="NAME=VALUE")
     _common(e)
+    o = sub.add_parser("qaoa-pso", help="PSO/QAOA study on random 3-regular graphs")
+    o.add_argument("--vertices", type=int, required=True)
+    o.add_argument("--graphs", type=int, default=1)
+    o.add_argument("--depth", type=int, default=1)
+    o.add_argument("--particles", type=int, default=4)
+    o.add_argument("--budget", type=int, required=True)
+    o.add_argument("--pso-sign", choices=("standard", "paper"), default="standard")
+    _common(o)
     return ap
 
 
@@ -240,7 +251,41 @@ def cmd_noise_ensemble(args) -> int:
     return EXIT_OK
 
 
-COMMANDS = {"run": cmd_run, "bench-gate": cmd_bench_gate, "noise-ensemble": cmd_noise_ensemble}
+def cmd_qaoa_pso(args) -> int:
+    import os
+
+    from .optimize import PsoHyperparams, random_3regular_graph, run_pso_qaoa, trace_csv_lines
+
+    if args.vertices % 2 or args.vertices > 20:
+        raise UsageError("--vertices must be even and <= 20 at desk scale")
+    hyper = PsoHyperparams(sign=args.pso_sign)
+    n = args.vertices
+    layout = _layout(args, n)
+    # every particle's value is layout-independent (tree-ordered reductions),
+    # so the states of the pool hold whole circuits on one device
+    S = layout.num_states
+    ctx = runtime.make_context(None, n, S, device=args.device, seed=args.seed)
+    pool_stream = RandomStream(args.seed, SCOPE_POOL, 0)
+    traces = []
+    for k in range(args.graphs):
+        graph = random_3regular_graph(n, pool_stream.split(2 * k))
+        traces.append(run_pso_qaoa(ctx, graph, args.depth, args.particles, args.budget,
+                                   pool_stream.split(2 * k + 1), hyper))
+    lines = ["evaluations,mean_ratio,step"]
+    for i, row in enumerate(traces[0]):
+        mean = sum(t[i].global_best_ratio for t in traces) / len(traces)
+        lines.append(f"{row.evaluations},{mean!r},{row.step}")
+    _emit("\n".join(lines) + "\n", args)
+    if args.out:
+        stem, ext = os.path.splitext(args.out)
+        for k, trace in enumerate(traces):
+            with open(f"{stem}_instance{k}{ext or '.csv'}", "w", encoding="utf-8") as fh:
+                fh.write("\n".join(trace_csv_lines(trace)) + "\n")
+    return EXIT_OK
+
+
+COMMANDS = {"run": cmd_run, "bench-gate": cmd_bench_gate, "noise-ensemble": cmd_noise_ensemble,
+            "qaoa-pso": cmd_qaoa_pso}
 
 
 def main(argv=None) -> int:

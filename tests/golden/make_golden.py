@@ -403,6 +403,14 @@ def gen_cli():
                         "--observable", "maxcut:cubic6.graph", "--bind", "gamma1=0.3",
                         "--bind", "beta1=1.1", "--bind", "gamma2=2.2", "--bind", "beta2=0.4"],
         "bench_gate": ["bench-gate", "--n", "7", "--ranks", "4", "--repetitions", "2"],
+        "pso_v8": ["qaoa-pso", "--vertices", "8", "--graphs", "2", "--depth", "2",
+                   "--particles", "6", "--budget", "24", "--seed", "11", "--states", "4",
+                   "--ranks", "4"],
+        "pso_v12_paper": ["qaoa-pso", "--vertices", "12", "--depth", "1", "--particles", "5",
+                          "--budget", "15", "--seed", "3", "--pso-sign", "paper",
+                          "--states", "2", "--ranks", "4"],
+        "pso_v14": ["qaoa-pso", "--vertices", "14", "--depth", "3", "--particles", "3",
+                    "--budget", "9", "--seed", "5"],
     }
     meta = {}
     cwd = os.getcwd()
@@ -427,11 +435,40 @@ def gen_cli():
     print("wrote", len(cases), "CLI reports")
 
 
+def gen_optimize():
+    """Swarm and graph pins for optimize.py: random_3regular_graph edges from
+    keyed streams, exact_maxcut, and a swarm driven by fixed values."""
+    from qpool import optimize as opt
+
+    graphs = {}
+    for n, key in ((4, 0), (8, 1), (12, 2), (20, 3)):
+        g = opt.random_3regular_graph(n, RandomStream(SEED, "pool", key))
+        graphs[f"edges_{n}"] = np.array(g.edges)
+        graphs[f"exact_{n}"] = np.array(opt.exact_maxcut(g))
+    rng = np.random.default_rng(SEED + 21)
+    out = {}
+    for sign in ("standard", "paper"):
+        sw = opt.init_swarm(5, 4, opt.PsoHyperparams(sign=sign), RandomStream(SEED, "pool", 9))
+        pos, vel, gb = [], [], []
+        vals = rng.uniform(0, 1, size=(6, 5))
+        for v in vals:
+            opt.step_swarm(sw, v)
+            pos.append(np.stack([p.position for p in sw.particles]))
+            vel.append(np.stack([p.velocity for p in sw.particles]))
+            gb.append(sw.global_best_value)
+        out[f"{sign}_values"] = vals
+        out[f"{sign}_pos"] = np.stack(pos)
+        out[f"{sign}_vel"] = np.stack(vel)
+        out[f"{sign}_gbest"] = np.array(gb)
+    save("golden_optimize.npz", **graphs, **out)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["1q", "ctrl", "phase_obs", "cfg1", "cfg3", "cfg4", "cfg5", "acct"]
     table = {"1q": gen_1q, "ctrl": gen_ctrl, "phase_obs": gen_phase_obs, "cfg1": gen_cfg1,
              "cfg3": gen_cfg3_small, "cfg4": gen_cfg4_small, "cfg5": gen_cfg5,
-             "acct": gen_accounting, "noise": lambda: gen_noise(), "cli": lambda: gen_cli()}
+             "acct": gen_accounting, "noise": lambda: gen_noise(), "cli": lambda: gen_cli(),
+             "optimize": lambda: gen_optimize()}
     for w in which:
         t0 = time.perf_counter()
         table[w]()
