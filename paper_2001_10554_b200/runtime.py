@@ -638,6 +638,47 @@ def noise_ensemble_csv(values, reference: float) -> str:
     return "\n".join(lines) + "\n"
 
 
+def apply_gate_pool(ctx: RankContext, gate, param_table=None) -> None:
+    """One gate on every pool state; state s binds param_table[s]
+    (runtime.py:175-189).  A pool context sends the per-state values as one
+    table; a single-state context binds its own entry (state_offset)."""
+    if param_table is None:
+        apply_gate(ctx, gate)
+        return
+    vals = np.asarray(param_table, dtype=np.float64)
+    if ctx.is_idle:
+        return
+    if ctx.pool is None:
+        from dataclasses import replace
+        apply_gate(ctx, replace(gate, param=float(vals[ctx.state_offset])))
+        return
+    if vals.shape != (ctx.num_states,):
+        raise ValueError(f"parameter table has {vals.size} entries for {ctx.num_states} states")
+    q = ctx.queue
+    if gate.kind == "diagcost":
+        q.cut_phase(gate.graph, vals)
+    elif gate.kind in gates_mod.ROTATION_GATES:
+        q.one_qubit(gate.qubits[0], gates_mod.rotation_batch(gate.kind, vals))
+    elif gate.kind == "cphase":
+        q.controlled(gate.qubits[0], gate.qubits[1],
+                     np.stack([gates_mod.cphase(float(v)) for v in vals]))
+    else:
+        raise ValueError(f"gate kind {gate.kind} takes no parameter")
+
+
+def pool_sum(ctx: RankContext, value) -> float:
+    """Incoherent sum over the pool's states in the reference's fixed tree
+    order (runtime.py:230-232, pool.py:131-155); `value` is the per-state
+    array a pool context's measurements return (or one state's scalar)."""
+    return sv.tree_sum_values(np.atleast_1d(np.asarray(value, dtype=np.float64)))
+
+
+def pool_gather(ctx: RankContext, value, num_groups: int | None = None) -> np.ndarray:
+    """Per-state values in state order (runtime.py:235-236)."""
+    arr = np.atleast_1d(np.asarray(value, dtype=np.float64))
+    return arr if num_groups is None else arr[:num_groups]
+
+
 def _queue_fixed(q: GateQueue, gate) -> None:
     if gate.kind == "diagcost":
         q.cut_phase(gate.graph, _angle(gate))

@@ -124,3 +124,29 @@ def test_tile_of_exactly_one_state_and_pool_of_one():
                 osv.apply_1q(exp[s], t, u)
         q.flush()
         assert bits_equal(st.download().reshape(S, -1), exp)
+
+
+def test_apply_gate_pool_binds_state_values():
+    """runtime.apply_gate_pool (runtime.py:175-189): state s binds table[s];
+    equal to running each binding on its own state."""
+    from paper_2001_10554_b200.circuit import GateSpec
+    from paper_2001_10554_b200.graphs import make_graph
+
+    n, S = 12, 3
+    rng = np.random.default_rng(12)
+    graph = make_graph(n, [(0, 3), (3, 7), (7, 11), (2, 5)])
+    gates = [GateSpec("h", (q,)) for q in range(n)]
+    gates += [GateSpec("diagcost", (), "$g", graph=graph), GateSpec("rx", (4,), "$b"),
+              GateSpec("cphase", (1, 9), "$p")]
+    tables = {"g": rng.uniform(0, 3, S), "b": rng.uniform(0, 3, S), "p": rng.uniform(0, 3, S)}
+    ctx = runtime.make_context(None, n, S)
+    for g in gates:
+        runtime.apply_gate_pool(ctx, g, None if g.slot is None else tables[g.slot])
+    got = ctx.pool.amplitudes()
+    for s in range(S):
+        one = runtime.make_context(None, n, 1)
+        for g in gates:
+            runtime.apply_gate(one, g if g.slot is None else
+                               GateSpec(g.kind, g.qubits, float(tables[g.slot][s]), graph=g.graph))
+        one.flush()
+        assert bits_equal(got[s], one.state.download())

@@ -212,3 +212,17 @@ def test_drop_in_api_surface():
         m = getattr(qs, mod)
         missing = [n for n in names if not hasattr(m, n)]
         assert not missing, (mod, missing)
+
+
+def test_pool_helpers_follow_reference_tree_order():
+    from paper_2001_10554_b200 import pool, runtime
+    from paper_2001_10554_b200.statevector import tree_sum_values
+
+    vals = np.random.default_rng(2).standard_normal(7)
+    assert pool.incoherent_sum_over_pool(vals) == tree_sum_values(vals)
+    assert runtime.pool_sum(None, vals) == tree_sum_values(vals)
+    assert runtime.pool_sum(None, 0.25) == 0.25
+    assert np.array_equal(runtime.pool_gather(None, vals, 3), vals[:3])
+    s = pool.RandomStream(3, pool.SCOPE_POOL, 0)
+    assert np.array_equal(pool.uniform_randoms(s, 4, 0.0, 2.0),
+                          pool.RandomStream(3, pool.SCOPE_POOL, 0).uniform(4, 0.0, 2.0))
