@@ -10,6 +10,8 @@
 //  k_tile        fused pass: a 2^12-amplitude tile in shared memory, gates
 //                applied in program order in register "rounds" of 4 qubits;
 //                one HBM read + write for a whole run of gates.
+#include <atomic>
+
 #include "common.cuh"
 
 namespace qsb {
@@ -707,19 +709,24 @@ template <bool PH, bool GE, bool TB>
 void launch_tile_variant(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                          const double* mats,
                          const CutTerms& ct, uint64_t num_tiles, cudaStream_t s) {
-    static bool configured = false;
-    static int sms = 148, per_sm = 1;
+    // per device: the shared-memory opt-in is a per-device function attribute
+    constexpr int kMaxDevices = 64;
+    static std::atomic<int> configured[kMaxDevices];
+    static int sms_of[kMaxDevices], per_sm_of[kMaxDevices];
     const size_t smem = tile_smem_bytes();
-    if (!configured) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (configured[dev].load(std::memory_order_acquire) == 0) {
         cudaFuncSetAttribute(k_tile<PH, GE, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        int dev = 0;
-        cudaGetDevice(&dev);
+        int sms = 148, per_sm = 1;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<PH, GE, TB>, kCtaThreads, smem);
-        if (per_sm < 1) per_sm = 1;
-        configured = true;
+        sms_of[dev] = sms;
+        per_sm_of[dev] = per_sm < 1 ? 1 : per_sm;
+        configured[dev].store(1, std::memory_order_release);
     }
-    uint64_t grid = uint64_t(sms) * per_sm;
+    uint64_t grid = uint64_t(sms_of[dev]) * per_sm_of[dev];
     const uint64_t need = (num_tiles + kGroups - 1) / kGroups;
     if (grid > need) grid = need;
 #ifdef QSB_PASS_PARAM

@@ -22,6 +22,7 @@ VARIANTS = {
     "t11g1m3": ["-DQSB_TILE_LOG2=11", "-DQSB_TILE_GROUPS=1", "-DQSB_TILE_MINB=3"],
     "pp": ["-DQSB_TILE_GROUPS=2", "-DQSB_TILE_MINB=1"],
     "low2": ["-DQSB_LOW_BITS=2"],
+    "prof": ["-DQSB_PROF"],
 }
 
 
