@@ -395,7 +395,9 @@ def run_ours(args):
                 "exchange": (None if world == 1 else
                              "qubit remapping (peer swap of half the slice)" if args.remap
                              else args.exchange),
-                "l2": "inputs larger than L2 (16 GiB state vs 126 MB)"},
+                "l2": (f"inputs larger than L2 ({16 * 2 ** m / 2 ** 30:g} GiB state per GPU "
+                       "vs 126 MB L2)" if 16 * 2 ** m > 126e6 else
+                       f"state fits in L2 ({16 * 2 ** m / 2 ** 20:g} MiB): not a roofline run")},
             "hbm_gbs": hbm_gbs,
             "hbm_gbs_note": "algorithmic: 32 B/amplitude for every gate (what an unfused "
                             "gate-by-gate simulator moves); fusion moves less, see hbm_gbs_actual",
