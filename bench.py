@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--workload", default="sweep",
                     choices=["sweep", "qaoa", "cfg3", "cfg4", "noise"])
     ap.add_argument("--seed", type=int, default=20260809)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--no-per-target", action="store_true")
