@@ -490,27 +490,34 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                         // by deg(r) - 2 * (edges of r currently cut)
                         uint64_t i = P.rank_offset | (base_local + rowoff[eb >> low_run] +
                                                       (uint64_t(eb) & lowmask));
-                        int cut = cut_of(i, ct);
-                        a[0] = cmul(a[0], __ldg(lut + cut));
-                        // per register bit j (uniform): its qubit, neighbour mask, degree
-                        int rq[kRegLog2], degq[kRegLog2];
+                        const int cut0 = cut_of(i, ct);
+                        // register bit j <-> qubit rq[j]: flipping a set F of them
+                        // changes the cut by sum_{j in F} d_j plus, per edge inside F,
+                        // (4 * cut_e - 2) (both ends flipped: the edge's status stays)
+                        int rq[kRegLog2], d[kRegLog2], bq[kRegLog2];
                         uint64_t nbq[kRegLog2];
 #pragma unroll
                         for (int j = 0; j < kRegLog2; ++j) {
                             rq[j] = P.tile_bits[__ffs(R.dk[1 << j]) - 1];
                             nbq[j] = P.nbr[rq[j]];
-                            degq[j] = __popcll(nbq[j]);
+                            bq[j] = int((i >> rq[j]) & 1);
+                            d[j] = __popcll(nbq[j]) -
+                                   2 * __popcll((i ^ (uint64_t(0) - uint64_t(bq[j]))) & nbq[j]);
+                        }
+                        int cuts[kRegAmps];
+                        cuts[0] = cut0;
+#pragma unroll
+                        for (int k = 1; k < kRegAmps; ++k) {
+                            const int h = 31 - __clz(k);  // highest bit of k (compile time)
+                            int c = cuts[k ^ (1 << h)] + d[h];
+#pragma unroll
+                            for (int j = 0; j < h; ++j)
+                                if ((k >> j) & 1)
+                                    c += ((nbq[h] >> rq[j]) & 1) ? 4 * (bq[h] ^ bq[j]) - 2 : 0;
+                            cuts[k] = c;
                         }
 #pragma unroll
-                        for (int step = 1; step < kRegAmps; ++step) {
-                            const int j = ctz_c(step);           // bit flipped by Gray step
-                            const int gray = step ^ (step >> 1);  // register index reached
-                            const uint64_t bitr = (i >> rq[j]) & 1;
-                            const int now_cut = __popcll((i ^ (uint64_t(0) - bitr)) & nbq[j]);
-                            cut += degq[j] - 2 * now_cut;
-                            i ^= uint64_t(1) << rq[j];
-                            a[gray] = cmul(a[gray], __ldg(lut + cut));
-                        }
+                        for (int k = 0; k < kRegAmps; ++k) a[k] = cmul(a[k], __ldg(lut + cuts[k]));
                         continue;
                     }
                     if (G.seq == kRegLog2) {
