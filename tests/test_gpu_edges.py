@@ -150,3 +150,14 @@ def test_apply_gate_pool_binds_state_values():
                                GateSpec(g.kind, g.qubits, float(tables[g.slot][s]), graph=g.graph))
         one.flush()
         assert bits_equal(got[s], one.state.download())
+
+
+def test_oversize_state_fails_loudly():
+    """2^36 amplitudes (1 TiB) cannot be allocated: a clean error, and the
+    device stays usable."""
+    with pytest.raises(Exception) as err:
+        N.DeviceState(36, 36)
+    assert "memory" in str(err.value).lower() or "alloc" in str(err.value).lower()
+    st = N.DeviceState(12, 12)
+    N.call("qs_init_basis", st.handle, 5)
+    assert st.download()[5] == 1.0
