@@ -23,6 +23,7 @@ VARIANTS = {
     "pp": ["-DQSB_TILE_GROUPS=2", "-DQSB_TILE_MINB=1"],
     "low2": ["-DQSB_LOW_BITS=2"],
     "prof": ["-DQSB_PROF"],
+    "dbuf1": ["-DQSB_DBUF", "-DQSB_TILE_MINB=1"],
 }
 
 
