@@ -39,9 +39,11 @@ int fail(int code, const char* fmt, ...) {
 #define CUDA_TRY(expr)                                                                    \
     do {                                                                                  \
         cudaError_t _e = (expr);                                                          \
-        if (_e != cudaSuccess)                                                            \
+        if (_e != cudaSuccess) {                                                          \
+            (void)cudaGetLastError(); /* a non-sticky error must not resurface later */   \
             return fail(_e == cudaErrorMemoryAllocation ? QS_ERR_NOMEM : QS_ERR_CUDA,    \
                         "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+        }                                                                                 \
     } while (0)
 
 #define CHECK_LAUNCH()                                                                    \
@@ -163,6 +165,7 @@ int grow(T** p, size_t* cap, size_t need) {
     size_t n = std::max(need, *cap * 2);
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
     if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // clear the (non-sticky) allocation error
         *p = nullptr;
         *cap = 0;
         return fail(QS_ERR_NOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
@@ -551,6 +554,7 @@ int qs_state_create(int32_t num_qubits, int32_t num_local_qubits, int32_t rank_i
         if ((e = cudaMemsetAsync(st->psi, 0, bytes, st->stream)) != cudaSuccess) break;
     } while (0);
     if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // clear the (non-sticky) error before later launches
         rc = fail(e == cudaErrorMemoryAllocation ? QS_ERR_NOMEM : QS_ERR_CUDA,
                   "qs_state_create(n=%d, m=%d, states=%d): %s", n, m, num_states,
                   cudaGetErrorString(e));
