@@ -158,55 +158,75 @@ __global__ void __launch_bounds__(kThreads)
 // per-chunk partials are aligned subtrees of each q's selected list, so the
 // second level (k_tree over partials) reproduces get_probability's tree_sum.
 constexpr int kMargChunkLog2 = 11;
+// A block reduces one aligned 2048-amplitude chunk; thread t holds amplitudes
+// 8t..8t+7.  With every |psi|^2 >= 0, zeroing the amplitudes whose bit q is 0
+// and summing the whole chunk in tree order gives exactly get_probability's
+// tree over the selected ones (0 + x == x), so each q is one masked tree:
+//  * q < 3: the masking happens inside the thread's 8 values (levels 0..3);
+//  * 3 <= q < 11: the thread's level-3 node is kept or zeroed by a thread-id bit;
+//  * the chunk total (q >= 11 and the norm) is the unmasked tree.
+// The 12 per-thread values go through a transpose-reduce butterfly (each
+// step halves the values a lane keeps: 8+4+2+1+1 shuffles instead of 12x5),
+// whose pairings are the tree's, then a tree over the 8 warps.
 __global__ void __launch_bounds__(kThreads)
     k_marginals(const double2* __restrict__ psi, int m, uint64_t total_chunks,
                 double* __restrict__ low_out, double* __restrict__ high_out) {
-    __shared__ double lev[2 << kMargChunkLog2];                // levels 0..11
-    __shared__ double tmp[(1 << kMargChunkLog2) - 1];          // odd-node trees, q = 0..10
-    const int chunk = 1 << kMargChunkLog2;
+    __shared__ double wsum[16][kThreads / 32];
     const uint64_t cps = uint64_t(1) << (m - kMargChunkLog2);  // chunks per state
     const int nlow = kMargChunkLog2;                           // q < 11
     const int nhigh = m - kMargChunkLog2;                      // 11 <= q < m
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
         const uint64_t st = c / cps, cl = c - st * cps;
-        const double2* src = psi + (st << m) + (cl << kMargChunkLog2);
-        for (int i = threadIdx.x; i < chunk; i += kThreads) lev[i] = abs2(src[i]);
-        __syncthreads();
-        // level l lives at offset (2^12 - 2^(12-l)), size 2^(11-l)
-        for (int l = 1; l <= kMargChunkLog2; ++l) {
-            const int in = (2 << kMargChunkLog2) - (2 << (kMargChunkLog2 - l + 1));
-            const int out = (2 << kMargChunkLog2) - (2 << (kMargChunkLog2 - l));
-            for (int i = threadIdx.x; i < (chunk >> l); i += kThreads)
-                lev[out + i] = __dadd_rn(lev[in + 2 * i], lev[in + 2 * i + 1]);
-            __syncthreads();
-        }
-        // odd nodes of level q -> tmp segment of q (size 2^(10-q)), then trees
-        for (int q = 0; q < nlow; ++q) {
-            const int lvl = (2 << kMargChunkLog2) - (2 << (kMargChunkLog2 - q));
-            const int cnt = chunk >> (q + 1);
-            const int seg = chunk - (chunk >> q);  // sum of earlier segment sizes
-            for (int i = threadIdx.x; i < cnt; i += kThreads) tmp[seg + i] = lev[lvl + 2 * i + 1];
-        }
-        __syncthreads();
-        for (int w = 1; w < (chunk >> 1); w <<= 1) {
-            for (int q = 0; q < nlow; ++q) {
-                const int cnt = chunk >> (q + 1);
-                const int seg = chunk - (chunk >> q);
-                for (int i = threadIdx.x; i * 2 * w < cnt; i += kThreads)
-                    if (i * 2 * w + w < cnt)
-                        tmp[seg + i * 2 * w] = __dadd_rn(tmp[seg + i * 2 * w], tmp[seg + i * 2 * w + w]);
+        const double2* src = psi + (st << m) + (cl << kMargChunkLog2) + 8 * tid;
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = abs2(src[j]);
+        const double l1[4] = {__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3]),
+                              __dadd_rn(v[4], v[5]), __dadd_rn(v[6], v[7])};
+        const double l2[2] = {__dadd_rn(l1[0], l1[1]), __dadd_rn(l1[2], l1[3])};
+        const double l3 = __dadd_rn(l2[0], l2[1]);
+        double x[16];
+        x[0] = __dadd_rn(__dadd_rn(v[1], v[3]), __dadd_rn(v[5], v[7]));  // q = 0
+        x[1] = __dadd_rn(l1[1], l1[3]);                                   // q = 1
+        x[2] = l2[1];                                                     // q = 2
+#pragma unroll
+        for (int q = 3; q < 11; ++q) x[q] = ((tid >> (q - 3)) & 1) ? l3 : 0.0;
+        x[11] = l3;                                                       // total
+#pragma unroll
+        for (int q = 12; q < 16; ++q) x[q] = 0.0;
+        // transpose-reduce: after step s a lane keeps 8 >> s values
+#pragma unroll
+        for (int s = 0, n = 16; s < 4; ++s, n >>= 1) {
+            const bool up = (lane >> s) & 1;
+#pragma unroll
+            for (int i = 0; i < n / 2; ++i) {
+                const double keep = up ? x[i + n / 2] : x[i];
+                const double give = up ? x[i] : x[i + n / 2];
+                x[i] = __dadd_rn(keep, __shfl_xor_sync(0xffffffffu, give, 1 << s));
             }
-            __syncthreads();
         }
-        if (threadIdx.x < nlow) {
-            const int q = threadIdx.x;
-            low_out[(st * nlow + q) * cps + cl] = tmp[chunk - (chunk >> q)];
+        x[0] = __dadd_rn(x[0], __shfl_xor_sync(0xffffffffu, x[0], 16));
+        // lane l (< 16) now holds the warp sum of slot bitrev4(l)
+        if (lane < 16) {
+            const int slot = ((lane & 1) << 3) | ((lane & 2) << 1) | ((lane & 4) >> 1) |
+                             ((lane & 8) >> 3);
+            wsum[slot][warp] = x[0];
         }
-        if (threadIdx.x >= 32 && threadIdx.x < 32 + nhigh) {
-            const int h = threadIdx.x - 32;  // q = 11 + h
-            if ((cl >> h) & 1) {
-                const uint64_t idx = ((cl >> (h + 1)) << h) | (cl & ((uint64_t(1) << h) - 1));
-                high_out[(st * nhigh + h) * (cps >> 1) + idx] = lev[(2 << kMargChunkLog2) - 2];
+        __syncthreads();
+        if (tid < 12) {
+            const double* w = wsum[tid];
+            const double b = __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3])),
+                                       __dadd_rn(__dadd_rn(w[4], w[5]), __dadd_rn(w[6], w[7])));
+            if (tid < nlow) {
+                low_out[(st * nlow + tid) * cps + cl] = b;
+            } else {
+                for (int h = 0; h < nhigh; ++h)  // q = 11 + h: the chunk if its bit h is set
+                    if ((cl >> h) & 1) {
+                        const uint64_t idx =
+                            ((cl >> (h + 1)) << h) | (cl & ((uint64_t(1) << h) - 1));
+                        high_out[(st * nhigh + h) * (cps >> 1) + idx] = b;
+                    }
             }
         }
         __syncthreads();
