@@ -29,7 +29,7 @@ class QubitRegister:
 
     # ---- initialisation ----------------------------------------------------------
     def Initialize(self, kind: str, index: int = 0) -> "QubitRegister":
-        self.queue.gates, self.queue.tables, self.queue.size = [], [], 0
+        self.queue.discard()
         if kind == "base":
             if not (0 <= index < (1 << self.num_qubits)):
                 raise ValueError(f"basis index {index} out of range")

@@ -51,22 +51,39 @@ class GateQueue:
         self.passes_total = 0
         self.gates_total = 0
         self.touched: set = set()  # physical positions the queued gates act on
+        self._keyed: dict = {}     # table key -> (offset, stride) within this program
 
     def __len__(self) -> int:
         return len(self.gates)
 
-    def _add(self, kind: int, target: int, control: int, table: np.ndarray, per_state: bool):
+    def discard(self) -> None:
+        """Drop the pending gates without running them."""
+        self.gates, self.tables, self.size, self.edges = [], [], 0, None
+        self.touched = set()
+        self._keyed = {}
+
+    def _add(self, kind: int, target: int, control: int, table: np.ndarray, per_state: bool,
+             key=None):
+        """Queue a gate whose matrix/LUT table is `table`.  Gates passing the
+        same `key` share one copy of the table in the program (e.g. the 20 RX
+        mixers of a QAOA layer bound to the same per-state beta table)."""
+        if key is not None and key in self._keyed:
+            offset, stride = self._keyed[key]
+            self.gates.append(_native.QsGate(kind, target, control, 0, offset, stride))
+            return
         table = np.ascontiguousarray(table, dtype=np.float64).reshape(-1)
         stride = table.size // self.state.num_states if per_state else 0
         g = _native.QsGate(kind, target, control, 0, self.size, stride)
+        if key is not None:
+            self._keyed[key] = (self.size, stride)
         self.gates.append(g)
         self.tables.append(table)
         self.size += table.size
 
-    def one_qubit(self, q: int, u) -> None:
-        """u: (2,2) shared or (S,2,2) per state."""
+    def one_qubit(self, q: int, u, key=None) -> None:
+        """u: (2,2) shared or (S,2,2) per state; `key` dedupes repeated tables."""
         u = np.ascontiguousarray(u, dtype=np.complex128)
-        self._add(_native.QS_KIND_1Q, q, -1, u.view(np.float64), u.ndim == 3)
+        self._add(_native.QS_KIND_1Q, q, -1, u.view(np.float64), u.ndim == 3, key)
         self.touched.add(q)
 
     def controlled(self, c: int, t: int, u) -> None:
@@ -98,6 +115,7 @@ class GateQueue:
         self.gates, self.tables, self.size = [], [], 0
         self.edges = None
         self.touched = set()
+        self._keyed = {}
         return passes
 
 
@@ -211,8 +229,7 @@ def make_context(comm: dist.GroupComm | None, num_qubits: int, num_states: int =
 def reset_state(ctx: RankContext, index: int = 0) -> None:
     if ctx.is_idle:
         return
-    ctx.queue.gates, ctx.queue.tables, ctx.queue.size, ctx.queue.edges = [], [], 0, None
-    ctx.queue.touched = set()
+    ctx.queue.discard()
     if ctx.layout is not None:  # a fresh basis state: back to the canonical layout
         ctx.layout = dist.QubitLayout(ctx.num_qubits, ctx.topology.num_local_qubits)
     if ctx.partition is not None:
@@ -526,6 +543,7 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
     tables = {k: np.asarray(v, dtype=np.float64) for k, v in slot_tables.items()}
     q = ctx.queue
     pre = _circuit_noise(ctx, circuit.gates, noise_stream)
+    rot_cache: dict = {}
     for gate in circuit.gates:
         slot = gate.slot if isinstance(getattr(gate, "param", None), str) else None
         if slot is None:
@@ -548,7 +566,12 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
         if gate.kind == "diagcost":
             q.cut_phase(gate.graph, vals)
         elif gate.kind in gates_mod.ROTATION_GATES:
-            q.one_qubit(gate.qubits[0], gates_mod.rotation_batch(gate.kind, vals))
+            # one table per (rotation, slot): every gate bound to the slot shares it
+            key = ("rot", gate.kind, slot)
+            mats = rot_cache.get(key)
+            if mats is None:
+                mats = rot_cache[key] = gates_mod.rotation_batch(gate.kind, vals)
+            q.one_qubit(gate.qubits[0], mats, key=(id(rot_cache), key))
         elif gate.kind == "cphase":
             mats = np.stack([gates_mod.cphase(float(v)) for v in vals])
             q.controlled(gate.qubits[0], gate.qubits[1], mats)
