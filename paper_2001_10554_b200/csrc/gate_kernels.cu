@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(kThreads) k_controlled(double2* __restrict__ p
             uint64_t s = p >> (m - 2), j = p & qmask;
             uint64_t x = insert0(insert0(j, lowb), highb) | cbit;
             lo[i] = (s << m) | x;
-            if (!diag_one) a[i] = psi[lo[i]];
+            a[i] = psi[lo[i]];
             b[i] = psi[lo[i] | tbit];
         }
     }
@@ -91,9 +91,16 @@ __global__ void __launch_bounds__(kThreads) k_controlled(double2* __restrict__ p
         if (p < total_pairs) {
             if (stride != 0) load_u(u, mats + offset + (p >> (m - 2)) * stride);
             if (diag_one) {
-                // u = diag(1, z): a is unchanged and b' = u11*b (the u10*a term is
-                // a signed zero); only the control=1, target=1 quarter moves.
-                psi[lo[i] | tbit] = cmul(u[3], b[i]);
+                // u = diag(1, z): a' equals a except where a signed zero meets
+                // the zero terms, so the full update is computed (bit-exact) but
+                // a is written back only when its bits changed -- the
+                // control=1, target=1 quarter is the only one that moves.
+                const double2 a0 = a[i];
+                pair_update(a[i], b[i], u);
+                if (__double_as_longlong(a[i].x) != __double_as_longlong(a0.x) ||
+                    __double_as_longlong(a[i].y) != __double_as_longlong(a0.y))
+                    psi[lo[i]] = a[i];
+                psi[lo[i] | tbit] = b[i];
             } else {
                 pair_update(a[i], b[i], u);
                 psi[lo[i]] = a[i];
