@@ -966,6 +966,29 @@ int qs_marginals(qs_state* st, double* out) {
 }
 
 // ---- global-qubit path --------------------------------------------------------
+// A partner slice on another device of this process (thread-per-rank over
+// several GPUs) needs peer access from ours; IPC-mapped slices of other
+// processes already have it (cudaIpcMemLazyEnablePeerAccess).
+static int ensure_peer_access(qs_state* st, const void* peer) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, peer) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return QS_OK;  // not a pointer the runtime knows: let the kernel report it
+    }
+    if (attr.type != cudaMemoryTypeDevice || attr.device == st->device) return QS_OK;
+    int can = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&can, st->device, attr.device));
+    if (!can)
+        return fail(QS_ERR_COMM, "device %d cannot access device %d's memory (no P2P)",
+                    st->device, attr.device);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(attr.device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(QS_ERR_COMM, "cudaDeviceEnablePeerAccess(%d): %s", attr.device,
+                    cudaGetErrorString(e));
+    (void)cudaGetLastError();
+    return QS_OK;
+}
+
 int qs_exchange_gate_peer(qs_state* st, void* peer_amps, int32_t is_lower, const double* u,
                           int32_t control_local) {
     if (!st) return fail(QS_ERR_VALUE, "null state");
@@ -973,6 +996,7 @@ int qs_exchange_gate_peer(qs_state* st, void* peer_amps, int32_t is_lower, const
     if (st->num_states != 1) return fail(QS_ERR_VALUE, "exchange needs a single-state handle");
     if (control_local >= st->m) return fail(QS_ERR_LOCALITY, "control %d is not local", control_local);
     if (int rc = ensure_device(st)) return rc;
+    if (int rc = ensure_peer_access(st, peer_amps)) return rc;
     CUDA_TRY(cudaMemcpyAsync(st->d_u, u, 8 * sizeof(double), cudaMemcpyHostToDevice, st->stream));
     {
         LaunchScope ls(st, kLaunchExchange);
@@ -996,6 +1020,7 @@ int qs_swap_qubits_peer(qs_state* st, void* peer_amps, int32_t local_qubit, int3
     if (local_qubit < 0 || local_qubit >= st->m)
         return fail(QS_ERR_LOCALITY, "qubit %d is not local", local_qubit);
     if (int rc = ensure_device(st)) return rc;
+    if (int rc = ensure_peer_access(st, peer_amps)) return rc;
     {
         LaunchScope ls(st, kLaunchExchange);
         launch_swap_peer(st->psi, reinterpret_cast<double2*>(peer_amps), st->m, local_qubit,
