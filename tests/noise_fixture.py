@@ -1,6 +1,4 @@
 """Decode tests/golden/golden_noise.npz (made by make_golden.py gen_noise)."""
-import numpy as np
-
 from conftest import golden
 
 KINDS = {0: "h", 1: "rx", 2: "ry", 3: "cx", 4: "noise"}

@@ -5,7 +5,6 @@ import os
 import re
 import subprocess
 
-import numpy as np
 import pytest
 
 from paper_2001_10554_b200 import _native as N
