@@ -221,9 +221,14 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128 (f64 pairs)", "data": "synthetic",
-        "config": {"workload": f"config 2 sample: one Haar 2x2 gate per step on a 2^{m} "
-                               f"complex128 state, targets (7*step) mod {m}",
-                   "qubits": m, "parallelism": "host threads"},
+        # our arm's workload; each reference step is a bounded sample of it
+        "config": {"workload": f"config 2 sweep: Haar 2x2 on each of the {m} qubits in turn, "
+                               f"fresh unitaries per step, normalised Gaussian state, "
+                               f"2^{m} c128 amplitudes per GPU (n={m}, 0 global qubits)",
+                   "qubits": m, "local_qubits": m,
+                   "sample": f"one Haar 2x2 gate per step, targets (7*step) mod {m}, on a "
+                             f"uniform 2^{m} state (same arithmetic per gate-update)",
+                   "parallelism": f"{cb.threads()} host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.threads(), "kind": "port",
                          "sample": f"{args.steps} single-gate steps at n={m}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
