@@ -10,20 +10,24 @@ from paper_2001_10554_b200 import build as B  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 VARIANTS = {
+    # default build: one 256-thread group per CTA, two CTAs per SM, 2^12 tiles
     "base": [],
-    "t11g2": ["-DQSB_TILE_LOG2=11"],
-    "r3t11": ["-DQSB_REG_LOG2=3", "-DQSB_TILE_LOG2=11"],
+    # the round-1 variants (results in profiles/r01_notes.md); GROUPS=2 means the
+    # ping-pong pair of groups in one CTA
+    "t11g2": ["-DQSB_TILE_LOG2=11", "-DQSB_TILE_GROUPS=2", "-DQSB_TILE_MINB=1"],
+    "r3t11": ["-DQSB_REG_LOG2=3", "-DQSB_TILE_LOG2=11", "-DQSB_TILE_GROUPS=2",
+              "-DQSB_TILE_MINB=1"],
     "t11g1m2": ["-DQSB_TILE_LOG2=11", "-DQSB_TILE_GROUPS=1", "-DQSB_TILE_MINB=2"],
-    "t11np": ["-DQSB_TILE_LOG2=11", "-DQSB_NO_PINGPONG"],
-    "t10g2": ["-DQSB_TILE_LOG2=10"],
-    "g1": ["-DQSB_TILE_GROUPS=1"],
+    "t11np": ["-DQSB_TILE_LOG2=11", "-DQSB_TILE_GROUPS=2", "-DQSB_TILE_MINB=1",
+              "-DQSB_NO_PINGPONG"],
+    "t10g2": ["-DQSB_TILE_LOG2=10", "-DQSB_TILE_GROUPS=2", "-DQSB_TILE_MINB=1"],
+    "g1": ["-DQSB_TILE_GROUPS=1", "-DQSB_TILE_MINB=1"],
     "g1m2": ["-DQSB_TILE_GROUPS=1", "-DQSB_TILE_MINB=2"],
     "t11g1m4": ["-DQSB_TILE_LOG2=11", "-DQSB_TILE_GROUPS=1", "-DQSB_TILE_MINB=4"],
     "t11g1m3": ["-DQSB_TILE_LOG2=11", "-DQSB_TILE_GROUPS=1", "-DQSB_TILE_MINB=3"],
     "pp": ["-DQSB_TILE_GROUPS=2", "-DQSB_TILE_MINB=1"],
     "low2": ["-DQSB_LOW_BITS=2"],
     "prof": ["-DQSB_PROF"],
-    "dbuf1": ["-DQSB_DBUF", "-DQSB_TILE_MINB=1"],
 }
 
 
