@@ -28,6 +28,7 @@ VARIANTS = {
     "pp": ["-DQSB_TILE_GROUPS=2", "-DQSB_TILE_MINB=1"],
     "low2": ["-DQSB_LOW_BITS=2"],
     "prof": ["-DQSB_PROF"],
+    "fmachain": ["-DQSB_FMA_CHAIN"],
     "nogmem": ["-DQSB_NO_GMEM"],
     "nogmem_nosmem": ["-DQSB_NO_GMEM", "-DQSB_NO_SMEM_ROUND"],
 }
