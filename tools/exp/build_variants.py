@@ -28,7 +28,9 @@ VARIANTS = {
     "pp": ["-DQSB_TILE_GROUPS=2", "-DQSB_TILE_MINB=1"],
     "low2": ["-DQSB_LOW_BITS=2"],
     "prof": ["-DQSB_PROF"],
-    "fmachain": ["-DQSB_FMA_CHAIN"],
+    "t11dbuf2": ["-DQSB_DBUF", "-DQSB_TILE_LOG2=11", "-DQSB_TILE_MINB=2"],
+    "t11dbuf3": ["-DQSB_DBUF", "-DQSB_TILE_LOG2=11", "-DQSB_TILE_MINB=3"],
+    "t11m3": ["-DQSB_TILE_LOG2=11", "-DQSB_TILE_MINB=3"],
     "nogmem": ["-DQSB_NO_GMEM"],
     "nogmem_nosmem": ["-DQSB_NO_GMEM", "-DQSB_NO_SMEM_ROUND"],
 }
