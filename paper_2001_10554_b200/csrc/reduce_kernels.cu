@@ -172,16 +172,25 @@ __global__ void __launch_bounds__(kThreads)
     k_marginals(const double2* __restrict__ psi, int m, uint64_t total_chunks,
                 double* __restrict__ low_out, double* __restrict__ high_out) {
     __shared__ double wsum[16][kThreads / 32];
+    // |psi|^2 of the chunk, loaded coalesced, one pad double per 8 so that
+    // thread t's 8 consecutive values read without bank conflicts
+    __shared__ double sq[(1 << kMargChunkLog2) + (1 << kMargChunkLog2) / 8];
     const uint64_t cps = uint64_t(1) << (m - kMargChunkLog2);  // chunks per state
     const int nlow = kMargChunkLog2;                           // q < 11
     const int nhigh = m - kMargChunkLog2;                      // 11 <= q < m
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (uint64_t c = blockIdx.x; c < total_chunks; c += gridDim.x) {
         const uint64_t st = c / cps, cl = c - st * cps;
-        const double2* src = psi + (st << m) + (cl << kMargChunkLog2) + 8 * tid;
+        const double2* src = psi + (st << m) + (cl << kMargChunkLog2);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int e = tid + j * kThreads;
+            sq[e + (e >> 3)] = abs2(src[e]);
+        }
+        __syncthreads();
         double v[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = abs2(src[j]);
+        for (int j = 0; j < 8; ++j) v[j] = sq[9 * tid + j];
         const double l1[4] = {__dadd_rn(v[0], v[1]), __dadd_rn(v[2], v[3]),
                               __dadd_rn(v[4], v[5]), __dadd_rn(v[6], v[7])};
         const double l2[2] = {__dadd_rn(l1[0], l1[1]), __dadd_rn(l1[2], l1[3])};
