@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
     const int swz_tid = swz(tid);
     const int ngates = P.rounds[P.num_rounds - 1].first_gate + P.rounds[P.num_rounds - 1].num_gates;
     auto prefetch = [&](uint64_t t, int buf) {
-#ifndef QSB_NO_GMEM
+#if !defined(QSB_NO_GMEM) && !defined(QSB_NO_LOADS)  // diagnostics builds
         if (t < P.num_tiles) {
             const uint64_t st = t >> tps_log2;
             const double2* g = psi + ((st << m) | tile_base(t)) + goff_tid;
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
             if (last && direct) {
                 // last round straight from registers to HBM: lanes 0-7 cover tile
                 // positions 0,1,2 (128-byte rows), so every warp store is 4 full rows
-#ifndef QSB_NO_GMEM
+#if !defined(QSB_NO_GMEM) && !defined(QSB_NO_STORES)
                 if (valid) {
                     uint64_t okb[kRegLog2];
 #pragma unroll
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
         }
         if (!direct) {
             PROF_T(s0);
-#ifndef QSB_NO_GMEM
+#if !defined(QSB_NO_GMEM) && !defined(QSB_NO_STORES)
             if (valid) {
                 double2* gb = gbase + goff_tid;
 #pragma unroll

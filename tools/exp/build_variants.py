@@ -32,6 +32,8 @@ VARIANTS = {
     "t11dbuf3": ["-DQSB_DBUF", "-DQSB_TILE_LOG2=11", "-DQSB_TILE_MINB=3"],
     "t11m3": ["-DQSB_TILE_LOG2=11", "-DQSB_TILE_MINB=3"],
     "nogmem": ["-DQSB_NO_GMEM"],
+    "noloads": ["-DQSB_NO_LOADS"],
+    "nostores": ["-DQSB_NO_STORES"],
     "nogmem_nosmem": ["-DQSB_NO_GMEM", "-DQSB_NO_SMEM_ROUND"],
 }
 
