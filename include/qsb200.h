@@ -116,8 +116,9 @@ int qs_scale(qs_state* st, double factor);
  * (`u_stride` doubles apart; 0 = one matrix for all states). */
 int qs_apply_1q(qs_state* st, int32_t q, const double* u, uint64_t u_stride);
 /* apply_local_controlled_gate (statevector.py:180-195): control-mask
- * compaction touches only the control=1 half (a quarter for CPhase-like
- * matrices diag(1, z)). */
+ * compaction touches only the control=1 half; for CPhase-like matrices
+ * diag(1, z) only the control=1, target=1 quarter is written (the target=0
+ * amplitude is written back only if a signed zero changed it). */
 int qs_apply_controlled(qs_state* st, int32_t control, int32_t target,
                         const double* u, uint64_t u_stride);
 /* apply_diagonal_phase with gamma*cut_counts (statevector.py:198-206,
