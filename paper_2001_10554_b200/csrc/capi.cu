@@ -578,8 +578,7 @@ int qs_state_destroy(qs_state* st) {
     cudaFree(st->d_pass);
     cudaFree(st->d_scratch);
     cudaFree(st->d_u);
-    cudaFree(st->d_stage[0]);
-    cudaFree(st->d_stage[1]);
+    cudaFree(st->d_stage[0]);  // d_stage[1] points into the same allocation
     if (st->h_out) cudaFreeHost(st->h_out);
     if (st->stream) cudaStreamDestroy(st->stream);
     if (st->comm_stream) cudaStreamDestroy(st->comm_stream);
@@ -1116,10 +1115,9 @@ int qs_exchange_gate_nccl(qs_state* st, int32_t peer, int32_t is_lower, const do
     if (int rc = ensure_device(st)) return rc;
     const uint64_t half = st->amps_per_state / 2;
     const uint64_t c = std::min<uint64_t>(chunk, half);
-    if (int rc = grow(&st->d_stage[0], &st->stage_cap, c)) return rc;
-    if (st->stage_cap > 0 && st->d_stage[1] == nullptr) {
-        CUDA_TRY(cudaMalloc(&st->d_stage[1], st->stage_cap * sizeof(double2)));
-    }
+    // one allocation holds both staging chunks, so they always grow together
+    if (int rc = grow(&st->d_stage[0], &st->stage_cap, 2 * c)) return rc;
+    st->d_stage[1] = st->d_stage[0] + st->stage_cap / 2;
     CUDA_TRY(cudaMemcpyAsync(st->d_u, u, 8 * sizeof(double), cudaMemcpyHostToDevice, st->stream));
     double2* mine = is_lower ? st->psi : st->psi + half;
     double2* outbound = is_lower ? st->psi + half : st->psi;

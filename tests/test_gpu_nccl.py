@@ -32,7 +32,7 @@ def nccl_state():
     N.call("qs_comm_destroy", st.handle)
 
 
-@pytest.mark.parametrize("chunk_log2", [13, 10, 7])
+@pytest.mark.parametrize("chunk_log2", [7, 10, 13, 9])  # growing, then shrinking chunks
 @pytest.mark.parametrize("control", [-1, 0, 5, 12])
 def test_self_exchange_equals_local_gate_on_top_qubit(nccl_state, chunk_log2, control):
     st, m = nccl_state
