@@ -161,3 +161,20 @@ def test_oversize_state_fails_loudly():
     st = N.DeviceState(12, 12)
     N.call("qs_init_basis", st.handle, 5)
     assert st.download()[5] == 1.0
+
+
+@pytest.mark.parametrize("a,c", [(0, 1), (2, 9), (11, 3), (0, 12)])
+def test_swap_qubits_local_is_a_permutation(a, c):
+    """qs_swap_qubits_local (remapping's local swap) exchanges qubit a and c
+    of every state: the amplitude at i moves to i with bits a and c swapped."""
+    n, S = 13, 3
+    rng = np.random.default_rng(a * 31 + c)
+    states = np.stack([ogates.random_state(n, rng) for _ in range(S)])
+    st = N.DeviceState(n, n, 0, S)
+    st.upload(states)
+    N.call("qs_swap_qubits_local", st.handle, a, c)
+    got = st.download().reshape(S, -1)
+    idx = np.arange(1 << n)
+    ba, bc = (idx >> a) & 1, (idx >> c) & 1
+    src = idx ^ ((ba ^ bc) << a) ^ ((ba ^ bc) << c)
+    assert bits_equal(got, states[:, src])
