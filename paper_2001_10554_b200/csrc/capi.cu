@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -78,7 +79,10 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
+std::mutex g_nccl_mutex;
+
 int nccl_load() {
+    std::lock_guard<std::mutex> lock(g_nccl_mutex);  // ranks may be threads
     if (g_nccl.loaded) return QS_OK;
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char* n : names) {
