@@ -34,7 +34,8 @@ KEYS = [
 
 def short(name):
     for k in ("k_tile", "k_gate1q", "k_controlled", "k_cut_phase", "k_tree_wide", "k_tree",
-              "k_exchange_peer", "k_fill", "k_gaussian", "k_scale", "k_pair_halves"):
+              "k_marginals", "k_exchange_peer", "k_swap_peer", "k_swap_local", "k_fill",
+              "k_gaussian", "k_scale", "k_pair_halves"):
         if k in name:
             return k
     return name[:40]
