@@ -36,7 +36,7 @@ METRIC = "gate-updates/s and achieved HBM GB/s (n=30 c128); weak-scaled n=33-36 
 UNIT = "gate-updates/s (n=30-equivalent: 1 unit = one 2x2 gate on 2^30 c128 amplitudes)"
 FP64_PEAK_TOPS = 62 * 148 * 1.965e9 / 1e12  # measured on B200 (tools/exp/fp64.cu)
 LAUNCH_KINDS = {1: "k_gate1q", 2: "k_controlled", 3: "k_cut_phase", 4: "k_tile",
-                5: "k_exchange_peer", 6: "k_tree"}
+                5: "k_exchange_peer", 6: "k_tree", 7: "k_fact"}
 
 
 def parse():
@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--local-qubits", type=int, default=30)
     ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--numerics", default="factored", choices=["factored", "exact"],
+                    help="factored: QS_FUSE_FACTORED (Euler-factored 1q gates, within 1e-12 "
+                         "of the reference); exact: QS_FUSE_EXACT (bit-identical)")
     ap.add_argument("--workload", default="sweep",
                     choices=["sweep", "qaoa", "cfg3", "cfg4", "noise"])
     ap.add_argument("--seed", type=int, default=20260809)
@@ -54,10 +57,17 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--no-per-target", action="store_true")
+    ap.add_argument("--no-exact-compare", action="store_true")
     ap.add_argument("--remap", action="store_true",
                     help="gates on global qubits swap the qubit into a local position "
                          "(half the NVLink traffic) instead of the pair exchange")
     return ap.parse_args()
+
+
+def fuse_mode(args):
+    if args.no_fuse:
+        return False
+    return "factored" if args.numerics == "factored" else True
 
 
 # ---- clocks -------------------------------------------------------------------------
@@ -260,7 +270,7 @@ def run_ours(args):
         return run_qaoa(args, dist, comm, world, rank, local)
     if args.workload == "noise":
         return run_noise(args, dist, comm, world, rank, local)
-    ctx = runtime.make_context(comm, n, 1, device=local, fuse=not args.no_fuse,
+    ctx = runtime.make_context(comm, n, 1, device=local, fuse=fuse_mode(args),
                                remap=args.remap)
     ctx.norm_check_interval = 0
     st = ctx.state
@@ -375,10 +385,38 @@ def run_ours(args):
                   if not args.no_per_target and args.workload == "sweep" else None)
     passes_per_step = len(launch_ms) / max(args.steps, 1)
     actual_gbs = 32.0 * (2 ** m) * passes_per_step * args.steps / (ms_dev / 1e3) / 1e9
-    # numpy-exact pair update: 20 FP64 ops per pair (a CX touches half the pairs)
-    fp64_ops = ((5.0 + 1.0 + 5.0) * (2 ** m) * 64 * args.steps if cfg3 else
-                10.0 * (2 ** m) * (n + 0.5 * len(cx_pairs)) * args.steps)
+    # numpy-exact pair update: 20 FP64 ops per pair (a CX touches half the pairs);
+    # factored: a 4-FMA shear per pair (2 per amplitude; lean passes pad every
+    # register round to 4 shears) plus two product diagonals (~13 per amplitude)
+    factored = fuse_mode(args) == "factored" and not cfg3
+    if factored:
+        fp64_per_amp = (2.0 * 4 * sum(-(-r // 4) for r in (12, 9, 9)) if n == 30 else 2.0 * n) \
+            + 26.0 + 10.0 * 0.5 * len(cx_pairs)
+        fp64_note = ("factored: 2 FP64 instructions per amplitude per shear (register rounds "
+                     "padded to 4 shears), two product diagonals ~13 each; the pass is not "
+                     "FP64-bound")
+    else:
+        fp64_per_amp = (5.0 + 1.0 + 5.0) * 64 if cfg3 else 10.0 * (n + 0.5 * len(cx_pairs))
+        fp64_note = ("10 FP64 instructions per amplitude per gate (numpy-exact complex "
+                     "arithmetic)")
+    fp64_ops = fp64_per_amp * (2 ** m) * args.steps
     fp64_rate = fp64_ops / (ms_dev / 1e3) / 1e12
+    # the bit-exact numerics on the same workload, for comparison
+    exact_cmp = None
+    if factored and not args.no_exact_compare:
+        ctx.queue.fuse = True
+        step(sweeps[0])
+        st.synchronize()
+        st.event_record(0)
+        for s in range(min(args.steps, 5)):
+            step(sweeps[args.warmup + s])
+        st.event_record(1)
+        st.synchronize()
+        ms_exact = max_over_ranks(dist, st.event_elapsed_ms(0, 1)) / min(args.steps, 5)
+        ctx.queue.fuse = "factored"
+        exact_cmp = {"value": units_per_step / (ms_exact / 1e3), "ms_per_step": ms_exact,
+                     "numerics": "exact (QS_FUSE_EXACT: bit-identical to the reference's numpy "
+                                 "arithmetic)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -396,7 +434,12 @@ def run_ours(args):
                             + f"fresh unitaries per step, normalised Gaussian state, "
                             f"2^{m} c128 amplitudes per GPU (n={n}, {p} global qubits)",
                 "qubits": n, "local_qubits": m, "gates_per_step": gates_per_step,
-                "fused": not args.no_fuse, "parallelism": f"state sharded over {world} GPU(s)",
+                "fused": not args.no_fuse,
+                "numerics": ("factored (QS_FUSE_FACTORED: Euler-factored 1q gates as 4-FMA "
+                             "shears + merged diagonals; within 1e-12 of the reference, "
+                             "tests/test_gpu_factored.py)" if factored else
+                             "exact (bit-identical to the reference's numpy arithmetic)"),
+                "parallelism": f"state sharded over {world} GPU(s)",
                 "exchange": (None if world == 1 else
                              "qubit remapping (peer swap of half the slice)" if args.remap
                              else args.exchange),
@@ -411,9 +454,9 @@ def run_ours(args):
             "passes_per_step": passes_per_step,
             "fp64": {"tera_ops_per_s": fp64_rate, "peak": FP64_PEAK_TOPS,
                      "frac": fp64_rate / FP64_PEAK_TOPS,
-                     "note": "10 FP64 instructions per amplitude per gate (numpy-exact "
-                             "complex arithmetic); peak = measured DFMA/DMUL/DADD issue rate "
+                     "note": fp64_note + "; peak = measured DFMA/DMUL/DADD issue rate "
                              "62 lanes/clk/SM x 148 SMs x 1.965 GHz (tools/exp/fp64.cu)"},
+            "exact_numerics": exact_cmp,
             "per_target_unfused": per_target,
             "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -427,8 +470,8 @@ def run_ours(args):
                          "note": "achieved = algorithmic bytes (32*2^m B per gate-update, "
                                  "SURVEY 8(d)) x gate-updates per launch / launch time; "
                                  "a fused pass moves 32*2^m B physically (traffic, "
-                                 "physical_gbs), so frac > 1 is the fusion gain; the pass "
-                                 "itself is FP64-issue-bound (see fp64)"},
+                                 "physical_gbs), so frac > 1 is the fusion gain; "
+                                 "physical_frac is the pass's own HBM rate"},
             "kernel_share": share,
             "gpu_launches": int(len(launch_ms)),
             "wall_s": wall,
@@ -606,7 +649,7 @@ def run_qaoa(args, dist, comm, world, rank, local):
     vel = rng.uniform(-0.5, 0.5, size=(S, 2 * depth))[first:first + count]
     best_pos, best_val = pos.copy(), np.full(count, -np.inf)
     gbest = pos[0].copy()
-    ctx = runtime.make_context(None, n, num_states=count, device=local, fuse=not args.no_fuse)
+    ctx = runtime.make_context(None, n, num_states=count, device=local, fuse=fuse_mode(args))
     ctx.norm_check_interval = 0
     st = ctx.state
     edges = np.asarray(graph.edges, dtype=np.int32)
@@ -764,7 +807,7 @@ def run_noise(args, dist, comm, world, rank, local):
     first, count = runtime.split_pool(S, rank, world)
     graph, circ = noise_instance(args.seed)
     model = noise.NoiseModel(NOISE_T1, NOISE_T2)
-    ctx = runtime.make_context(None, n, num_states=count, device=local, fuse=not args.no_fuse,
+    ctx = runtime.make_context(None, n, num_states=count, device=local, fuse=fuse_mode(args),
                                seed=args.seed, noise_model=model)
     ctx.norm_check_interval = 0
     st = ctx.state

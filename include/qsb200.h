@@ -126,9 +126,21 @@ int qs_apply_controlled(qs_state* st, int32_t control, int32_t target,
 int qs_apply_cut_phase(qs_state* st, const int32_t* edges, int32_t num_edges,
                        const double* lut, uint64_t lut_stride);
 /* A sequence of gates in program order (runtime.run_circuit, runtime.py:155-162).
- * With fuse != 0 the native planner groups consecutive gates into shared-
- * memory tile passes (one HBM read+write per pass); per-amplitude arithmetic
- * and order are unchanged, so results are bit-identical to fuse == 0. */
+ * fuse == QS_FUSE_NONE: one streaming kernel per gate.
+ * fuse == QS_FUSE_EXACT: the native planner groups consecutive gates into
+ *   shared-memory tile passes (one HBM read+write per pass); per-amplitude
+ *   arithmetic and order are unchanged, so results are bit-identical to
+ *   QS_FUSE_NONE and to the reference's numpy arithmetic.
+ * fuse == QS_FUSE_FACTORED: as EXACT, after a rewrite of every uncontrolled
+ *   shared-matrix 1q unitary into k*diag(1,za)*R*diag(1,zb) (R a real
+ *   rotation applied as a 4-FMA shear); the diagonals merge across the program
+ *   into neighbouring gates and two product diagonals at its ends.  Same
+ *   operator, about a quarter of the FP64 work, results within 1e-12 of the
+ *   reference (north_star tolerance) but not bit-identical.  States with
+ *   fewer than 12 local qubits run EXACT. */
+#define QS_FUSE_NONE      0
+#define QS_FUSE_EXACT     1
+#define QS_FUSE_FACTORED  2
 int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count,
                      const double* mats, uint64_t mats_len,
                      const int32_t* edges, int32_t num_edges, int32_t fuse);
@@ -138,6 +150,12 @@ int qs_plan_program(int32_t num_local_qubits, const qs_gate* gates, int32_t coun
                     int32_t* starts, int32_t cap, int32_t* npasses);
 /* Number of HBM passes the last qs_apply_program launched (planner output). */
 int qs_last_program_passes(const qs_state* st, int32_t* passes);
+/* The factorisation QS_FUSE_FACTORED applies to one 2x2 unitary u (8 doubles):
+ * u = k * diag(1, za) * R * diag(1, zb), R = [[c,-s],[s,c]] = scale *
+ * [[1,-t],[t,1]] (scale = c, t = s/c).  out[10] = k.re k.im za.re za.im zb.re
+ * zb.im 0 t scale 0.  Returns QS_ERR_VALUE when u is not unitary to 1e-12,
+ * exactly diagonal or has c < 1e-3 (those stay unfactored). */
+int qs_decompose_2x2(const double* u, double* out);
 
 /* ---- observables: per-state partial sums in the reference's tree order
  *      (statevector.py:29-45, 209-251); out has num_states doubles ------- */

@@ -32,7 +32,7 @@ EXPORTS = (
     "qs_swap_qubits_local", "qs_state_ipc_handle", "qs_peer_open",
     "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
     "qs_event_record", "qs_event_elapsed_ms", "qs_launch_log", "qs_launch_log_read",
-    "qs_compose_2x2", "qs_philox4x64",
+    "qs_compose_2x2", "qs_philox4x64", "qs_decompose_2x2",
 )
 
 
@@ -95,6 +95,7 @@ _SIGNATURES = {
     "qs_observable": ([_P, _I, _I, _IP, _I, _DP], ctypes.c_int),
     "qs_marginals": ([_P, _DP], ctypes.c_int),
     "qs_compose_2x2": ([_DP, _DP, ctypes.c_int64, _DP], ctypes.c_int),
+    "qs_decompose_2x2": ([_DP, _DP], ctypes.c_int),
     "qs_philox4x64": ([_U64P, _U64P, ctypes.c_int64, _U64P], ctypes.c_int),
     "qs_exchange_gate_peer": ([_P, _P, _I, _DP, _I], ctypes.c_int),
     "qs_exchange_gate_nccl": ([_P, _I, _I, _DP, _I, _U], ctypes.c_int),
@@ -159,13 +160,44 @@ def device_count() -> int:
     return n.value if rc == QS_OK else 0
 
 
+FUSE_NONE, FUSE_EXACT, FUSE_FACTORED = 0, 1, 2
+
+
+def fuse_code(fuse) -> int:
+    """False -> QS_FUSE_NONE, True -> QS_FUSE_EXACT (bit-identical to the
+    reference), "factored" -> QS_FUSE_FACTORED (include/qsb200.h: Euler-
+    factored 1q gates, within 1e-12 of the reference)."""
+    if isinstance(fuse, str):
+        if fuse == "factored":
+            return FUSE_FACTORED
+        if fuse == "exact":
+            return FUSE_EXACT
+        raise ValueError(f"unknown fuse mode {fuse!r}")
+    if fuse is True or fuse is False or fuse is None:
+        return FUSE_EXACT if fuse else FUSE_NONE
+    code = int(fuse)
+    if code not in (FUSE_NONE, FUSE_EXACT, FUSE_FACTORED):
+        raise ValueError(f"unknown fuse mode {fuse!r}")
+    return code
+
+
+def decompose_2x2(u) -> tuple:
+    """qs_decompose_2x2: u = k diag(1,za) R diag(1,zb) with R = scale *
+    [[1,-t],[t,1]] (form is always 0)."""
+    u = np.ascontiguousarray(u, dtype=np.complex128).reshape(2, 2)
+    out = np.zeros(10)
+    call("qs_decompose_2x2", dptr(u.view(np.float64).ravel()), dptr(out))
+    return (complex(out[0], out[1]), complex(out[2], out[3]), complex(out[4], out[5]),
+            int(out[6]), float(out[7]), float(out[8]))
+
+
 def plan_program(num_local_qubits: int, gates, fuse: bool = True) -> list[int]:
     """First gate index of every pass the native planner would launch (CPU only)."""
     n = len(gates)
     arr = gates if isinstance(gates, ctypes.Array) else (QsGate * max(n, 1))(*gates)
     starts = (ctypes.c_int32 * max(n, 1))()
     count = ctypes.c_int32(0)
-    call("qs_plan_program", num_local_qubits, arr, n, 1 if fuse else 0, starts, max(n, 1),
+    call("qs_plan_program", num_local_qubits, arr, n, fuse_code(fuse), starts, max(n, 1),
          ctypes.byref(count))
     return list(starts[:count.value])
 
@@ -268,7 +300,7 @@ class DeviceState:
             if ne == 0:
                 e = np.zeros(2, dtype=np.int32)
         call("qs_apply_program", self.handle, arr, n, dptr(mats), mats.size, iptr(e), ne,
-             1 if fuse else 0)
+             fuse_code(fuse))
         passes = ctypes.c_int32(0)
         call("qs_last_program_passes", self.handle, ctypes.byref(passes))
         return passes.value

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libqsb200.so")
-SOURCES = ["gate_kernels.cu", "reduce_kernels.cu", "exchange_kernels.cu", "capi.cu"]
+SOURCES = ["gate_kernels.cu", "reduce_kernels.cu", "exchange_kernels.cu", "factor.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-v",
          "--expt-relaxed-constexpr"]

@@ -222,7 +222,7 @@ struct LaunchScope {
 };
 
 enum { kLaunchGate1q = 1, kLaunchControlled = 2, kLaunchPhase = 3, kLaunchTile = 4,
-       kLaunchExchange = 5, kLaunchReduce = 6 };
+       kLaunchExchange = 5, kLaunchReduce = 6, kLaunchFact = 7 };
 
 bool is_diag_one(const double* e) {
     return e[0] == 1.0 && e[1] == 0.0 && e[2] == 0.0 && e[3] == 0.0 && e[4] == 0.0 && e[5] == 0.0;
@@ -262,7 +262,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     // tile bits: the targets, plus qubits 0..2 for 128-byte rows, filled upward
     uint64_t need = kLowMask;
     for (int i = 0; i < count; ++i)
-        if (prog[first + i].kind != QS_KIND_CUTPHASE) need |= uint64_t(1) << prog[first + i].target;
+        if (kind_has_target(prog[first + i].kind)) need |= uint64_t(1) << prog[first + i].target;
     for (int b = 0; __builtin_popcountll(need) < kTileLog2 && b < st->m; ++b) need |= uint64_t(1) << b;
     static thread_local TilePass P;
     memset(&P, 0, sizeof(P));
@@ -325,7 +325,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     std::vector<int> gate_round(count);
     for (int i = 0; i < count; ++i) {
         const qs_gate& g = prog[first + i];
-        int p = g.kind == QS_KIND_CUTPHASE ? -1 : pos_of(g.target);
+        int p = kind_has_target(g.kind) ? pos_of(g.target) : -1;
         bool fits = r >= 0;
         if (fits && p >= 0 &&
             std::find(round_pos.begin(), round_pos.end(), p) == round_pos.end() &&
@@ -365,6 +365,10 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         d.cval = 0;
         d.seq = 0;
         if (g.kind == QS_KIND_CUTPHASE) continue;
+        if (g.kind == kKindDiagN) {
+            d.cval = g.reserved;  // byte-table count
+            continue;
+        }
         if (g.stride == 0) memcpy(&d.u[0], mats_host + g.offset, 8 * sizeof(double));
         const std::vector<int>& rp = all_pos[gate_round[i]];
         int p = pos_of(g.target), j = 0;
@@ -386,11 +390,14 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
             }
         }
     }
-    // mark runs of uncontrolled gates on register bits 0,1,2 (in order, same round)
+    // mark runs of uncontrolled gates (or of shears) on register bits 0,1,2,..
+    // (in order, same round)
     for (int i = 0; i < count;) {
         int n = 0;
-        while (i + n < count && n < kRegLog2 && P.gates[i + n].kind == QS_KIND_1Q &&
-               P.gates[i + n].variant == n && gate_round[i + n] == gate_round[i])
+        const int kind = P.gates[i].kind;
+        while (i + n < count && n < kRegLog2 && (kind == QS_KIND_1Q || kind == kKindShear) &&
+               P.gates[i + n].kind == kind && P.gates[i + n].variant == n &&
+               gate_round[i + n] == gate_round[i])
             ++n;
         if (n >= 1) {
             P.gates[i].seq = n;
@@ -405,7 +412,8 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     }
     {
         LaunchScope ls(st, kLaunchTile);
-        launch_tile_pass(st->psi, P, st->d_pass, st->d_mats, ct, st->stream);
+        if (launch_tile_pass(st->psi, P, st->d_pass, st->d_mats, ct, st->stream))
+            ls.rec.kind = kLaunchFact;
     }
     CHECK_LAUNCH();
     return QS_OK;
@@ -429,14 +437,14 @@ std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool f
         int j = i + 1;
         if (tile_ok) {
             uint64_t need = kLowMask;
-            if (gates[i].kind != QS_KIND_CUTPHASE) need |= uint64_t(1) << gates[i].target;
-            uint64_t round_set = gates[i].kind != QS_KIND_CUTPHASE ? (uint64_t(1) << gates[i].target) : 0;
+            if (kind_has_target(gates[i].kind)) need |= uint64_t(1) << gates[i].target;
+            uint64_t round_set = kind_has_target(gates[i].kind) ? (uint64_t(1) << gates[i].target) : 0;
             int rounds = 1;
             while (j < count && j - i < kMaxPassGates) {
                 const qs_gate& g = gates[j];
                 uint64_t nn = need, rs = round_set;
                 int nr = rounds;
-                if (g.kind != QS_KIND_CUTPHASE) {
+                if (kind_has_target(g.kind)) {
                     uint64_t b = uint64_t(1) << g.target;
                     nn |= b;
                     if (!(rs & b)) {
@@ -744,6 +752,19 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
     }
     for (int i = 0; i < count; ++i)
         if (int rc = validate_gate(st, gates[i], mats_len, num_edges)) return rc;
+    if (fuse == QS_FUSE_FACTORED && st->m >= kTileLog2) {
+        // rewrite, then plan the rewritten program; its parameters and diagonal
+        // tables follow the caller's table in one upload
+        static thread_local FactoredProgram fp;
+        static thread_local std::vector<double> all;
+        factor_program(gates, count, mats, mats_len, st->m, st->num_states, &fp);
+        all.assign(mats, mats + mats_len);
+        all.insert(all.end(), fp.extra.begin(), fp.extra.end());
+        gates = fp.gates.data();
+        count = int(fp.gates.size());
+        mats = all.data();
+        mats_len = all.size();
+    }
     if (int rc = grow(&st->d_mats, &st->mats_cap, mats_len ? mats_len : 1)) return rc;
     if (mats_len)
         CUDA_TRY(cudaMemcpyAsync(st->d_mats, mats, mats_len * sizeof(double),
@@ -751,8 +772,10 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
     std::vector<PassPlan> plan = plan_passes(gates, count, st->m, fuse != 0);
     int passes = 0;
     for (const PassPlan& pp : plan) {
-        int rc = pp.count == 1 ? launch_single(st, gates[pp.first], ct, mats)
-                               : launch_tile(st, gates, pp.first, pp.count, ct, mats);
+        // the internal kinds of a factored program only exist as tile-pass gates
+        const bool single = pp.count == 1 && gates[pp.first].kind <= QS_KIND_CUTPHASE;
+        int rc = single ? launch_single(st, gates[pp.first], ct, mats)
+                        : launch_tile(st, gates, pp.first, pp.count, ct, mats);
         if (rc) return rc;
         ++passes;
     }
@@ -774,6 +797,12 @@ int qs_plan_program(int32_t num_local_qubits, const qs_gate* gates, int32_t coun
     std::vector<PassPlan> plan = plan_passes(gates, count, num_local_qubits, fuse != 0);
     for (size_t k = 0; k < plan.size() && (int)k < cap; ++k) starts[k] = plan[k].first;
     *npasses = (int32_t)plan.size();
+    return QS_OK;
+}
+
+int qs_decompose_2x2(const double* u, double* out) {
+    if (!u || !out) return fail(QS_ERR_VALUE, "null argument");
+    if (!decompose_2x2(u, out)) return fail(QS_ERR_VALUE, "not a non-diagonal unitary");
     return QS_OK;
 }
 

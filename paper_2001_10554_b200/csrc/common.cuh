@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
+#include <vector>
 
 #include "../../include/qsb200.h"
 
@@ -126,6 +127,35 @@ struct alignas(16) TilePass {
     TileGate gates[kMaxPassGates];
 };
 
+// ---- factored programs (fuse == QS_FUSE_FACTORED, factor.cu) ---------------
+// Internal gate kinds the factored rewrite emits; they never appear in a user
+// program.  Each 1q unitary U = k * diag(1, za) * R(c, s) * diag(1, zb) with R
+// the real rotation [[c,-s],[s,c]] = c*[[1,-t],[t,1]] (t = s/c), so the pair
+// update is a 4-FMA shear.  The diagonals commute with every gate not mixing
+// their qubit, so they merge into the neighbouring gates' diagonals and, at the
+// ends of the program, into one product diagonal over all qubits (D_in before
+// everything, D_out with the scalars after everything).
+constexpr int kKindShear = 16;  // params [t, 0, has_pre, 0, z.re, z.im, 0, 0]: b *= z (if
+                                // has_pre), then (a, b) <- (a - t b, b + t a) on `target`
+constexpr int kKindDiag1 = 17;  // params [0, 0, 0, 0, z.re, z.im, 0, 0]: amplitudes with bit
+                                // `target` set *= z
+constexpr int kKindDiagN = 18;  // psi_i *= prod_c T_c[byte c of i]; `reserved` = table count;
+                                // offset -> ntab*256 complex byte tables, then 64 complex z_q
+inline bool kind_has_target(int kind) { return kind != QS_KIND_CUTPHASE && kind != kKindDiagN; }
+
+struct FactoredProgram {
+    std::vector<qs_gate> gates;
+    std::vector<double> extra;  // parameters/tables, addressed at mats_len + local offset
+    int factored = 0;           // 1q gates turned into shears
+};
+// Rewrites gates[0..count) (validated, all local) into `out`.  mats_len is the
+// size of the caller's table (the extra entries are appended after it).
+void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
+                    int num_states, FactoredProgram* out);
+// U = k diag(1,za) R diag(1,zb): out = [k, za, zb] (complex), 0, t, scale (= c).
+// Returns false when U is not unitary to 1e-12, exactly diagonal or c < 1e-3.
+bool decompose_2x2(const double* u, double out[10]);
+
 // ---- launchers (gate_kernels.cu / reduce_kernels.cu / exchange.cu) ---------
 void launch_gate1q(double2* psi, int m, int num_states, int q, const double* mats,
                    uint64_t offset, uint64_t stride, cudaStream_t s);
@@ -135,7 +165,8 @@ void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
                       const CutTerms& ct, const double* mats, uint64_t offset, uint64_t stride,
                       cudaStream_t s);
 bool tile_pass_in_params();  // k_tile takes the pass as a kernel parameter
-void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
+// returns true when the pass ran on the lean factored kernel (k_fact)
+bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                       const double* mats, const CutTerms& ct, cudaStream_t s);
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s);
 void launch_gaussian(double2* psi, uint64_t count_per_state, int num_states, uint64_t rank_offset,

@@ -1,0 +1,239 @@
+// Factored programs (QS_FUSE_FACTORED): the same operator as the user's gate
+// list with about a quarter of the FP64 work per fused pass.
+//
+// Every uncontrolled 1q gate with a shared unitary matrix U is written
+//     U = k * diag(1, za) * R * diag(1, zb),   R = [[c,-s],[s,c]],  c,s >= 0,
+// and R as a shear times a scalar: c*[[1,-t],[t,1]] with t = s/c.  A shear pair
+// update is 4 FMAs (2 FP64 instructions per amplitude) against numpy's 10 per
+// amplitude for a general complex 2x2 (statevector.py:144-150).  A large t
+// costs no accuracy (fma(-t, y, x) rounds once, relative to |x - t y|, and the
+// scale c brings the result back), only growth: the amplitudes grow by at most
+// 1/c per shear until the scalar is applied, so gates with c < 1e-3 stay exact
+// and a scalar pass is inserted when the pending scale passes 2^-600.  The
+// rest is bookkeeping that costs nothing per amplitude:
+//  * scalars commute with everything: k and the shear scale multiply into one
+//    constant applied once at the end;
+//  * diag(1, z) on qubit q commutes with every gate that does not mix q
+//    (gates on other qubits, controls on q, cut phases, diagonal gates), so
+//    the za of one gate on q and the zb of the next gate on q meet and merge
+//    into one pre-diagonal of that shear (complex multiply of its b member);
+//  * the zb of the FIRST mixing gate on q moves to the program start and the
+//    za of the LAST one to the program end, where the diagonals of all qubits
+//    form one product diagonal D(i) = prod_q z_q^{bit_q(i)} (kKindDiagN),
+//    evaluated per tile from byte tables plus a walk over the register bits.
+// For a layer of 1q gates on distinct qubits (BASELINE config 2's sweep, the
+// 1q layers of configs 1 and 4) this leaves one shear per gate plus D_in and
+// D_out.  Controlled gates, per-state matrix tables, non-unitary matrices and
+// cut phases stay exact.  Errors are a few ulps per gate (the tests bound them
+// by the north_star 1e-12 on amplitudes).
+#include <cmath>
+#include <complex>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace qsb {
+
+namespace {
+using cd = std::complex<double>;
+
+cd unit(cd z) { return z / std::abs(z); }
+
+cd entry(const double* u, int i) { return cd(u[2 * i], u[2 * i + 1]); }
+
+bool is_unitary(const cd u[4]) {
+    // U^dagger U == I to 1e-12
+    const cd g00 = std::conj(u[0]) * u[0] + std::conj(u[2]) * u[2];
+    const cd g11 = std::conj(u[1]) * u[1] + std::conj(u[3]) * u[3];
+    const cd g01 = std::conj(u[0]) * u[1] + std::conj(u[2]) * u[3];
+    return std::abs(g00 - 1.0) <= 1e-12 && std::abs(g11 - 1.0) <= 1e-12 && std::abs(g01) <= 1e-12;
+}
+}  // namespace
+
+bool decompose_2x2(const double* m, double out[10]) {
+    cd u[4];
+    for (int i = 0; i < 4; ++i) u[i] = entry(m, i);
+    for (int i = 0; i < 8; ++i)
+        if (!std::isfinite(m[i])) return false;
+    if (u[1] == 0.0 && u[2] == 0.0) return false;  // diagonal: merged as a diagonal instead
+    if (!is_unitary(u)) return false;
+    const double a00 = std::abs(u[0]), a01 = std::abs(u[1]), a10 = std::abs(u[2]),
+                 a11 = std::abs(u[3]);
+    double c = std::sqrt(0.5 * (a00 * a00 + a11 * a11));
+    double s = std::sqrt(0.5 * (a01 * a01 + a10 * a10));
+    const double r = std::hypot(c, s);
+    c /= r;
+    s /= r;
+    // u00 = k c, u01 = -k s zb, u10 = k za s, u11 = k za zb c.  The phases come
+    // from the two large entries, the ratio (or product) from the two small
+    // ones, so an error in a small entry's phase only moves small entries.
+    cd k, za, zb;
+    int form;
+    double t, scale;
+    if (c >= s) {
+        k = unit(u[0]);
+        const cd P = unit(u[3]) / k;                                         // za * zb
+        const cd Q = (a01 > 0 && a10 > 0) ? -unit(u[2]) * std::conj(unit(u[1])) : cd(1.0);  // za / zb
+        za = std::sqrt(P * Q);
+        zb = P / za;
+        if (std::real(std::conj(k * za) * u[2]) < 0) za = -za, zb = -zb;  // u10 = +k za s
+    } else {
+        const cd Q = -unit(u[2]) * std::conj(unit(u[1]));                          // za / zb
+        const cd P = (a00 > 0 && a11 > 0) ? unit(u[3]) * std::conj(unit(u[0])) : cd(1.0);  // za * zb
+        za = std::sqrt(P * Q);
+        zb = P / za;
+        k = unit(u[2]) / za;  // u10 = k za s
+        if (a00 > 0 && std::real(std::conj(k) * u[0]) < 0) za = -za, zb = -zb, k = -k;  // u00 = +k c
+    }
+    if (c < 1e-3) return false;  // nearly anti-diagonal: t would exceed 1000
+    form = 0;
+    t = s / c;
+    scale = c;
+    za = unit(za);
+    zb = unit(zb);
+    out[0] = k.real(), out[1] = k.imag();
+    out[2] = za.real(), out[3] = za.imag();
+    out[4] = zb.real(), out[5] = zb.imag();
+    out[6] = form, out[7] = t, out[8] = scale, out[9] = 0;
+    return true;
+}
+
+void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
+                    int num_states, FactoredProgram* out) {
+    out->gates.clear();
+    out->extra.clear();
+    out->factored = 0;
+    std::vector<cd> pending(m, cd(1.0)), din(m, cd(1.0));
+    std::vector<char> mixed(m, 0);
+    cd K(1.0);
+    const int ntab = (m + 7) / 8;
+
+    auto params = [&](const double* p8) {
+        const uint64_t off = mats_len + out->extra.size();
+        out->extra.insert(out->extra.end(), p8, p8 + 8);
+        return off;
+    };
+    auto emit = [&](int kind, int target, uint64_t off) {
+        qs_gate g;
+        memset(&g, 0, sizeof(g));
+        g.kind = kind;
+        g.target = target;
+        g.control = -1;
+        g.offset = off;
+        g.stride = 0;
+        out->gates.push_back(g);
+    };
+    // product diagonal sum over set bits: byte tables with `scalar` in table 0
+    auto diag_tables = [&](const std::vector<cd>& z, cd scalar) {
+        while (out->extra.size() % 2) out->extra.push_back(0.0);  // 16-byte aligned entries
+        const uint64_t off = mats_len + out->extra.size();
+        std::vector<cd> T(size_t(ntab) * 256);
+        for (int c = 0; c < ntab; ++c) {
+            cd* t = T.data() + c * 256;
+            t[0] = 1.0;
+            for (int v = 1; v < 256; ++v) {
+                const int b = __builtin_ctz(v), q = 8 * c + b;
+                t[v] = t[v & (v - 1)] * (q < m ? z[q] : cd(1.0));
+            }
+        }
+        for (int v = 0; v < 256; ++v) T[v] *= scalar;
+        for (const cd& x : T) out->extra.push_back(x.real()), out->extra.push_back(x.imag());
+        for (int q = 0; q < 64; ++q) {
+            const cd x = q < m ? z[q] : cd(1.0);
+            out->extra.push_back(x.real()), out->extra.push_back(x.imag());
+        }
+        qs_gate g;
+        memset(&g, 0, sizeof(g));
+        g.kind = kKindDiagN;
+        g.target = -1;
+        g.control = -1;
+        g.reserved = ntab;
+        g.offset = off;
+        return g;
+    };
+    auto diag1 = [&](int q, cd z) {
+        const double p[8] = {0, 0, 0, 0, z.real(), z.imag(), 0, 0};
+        emit(kKindDiag1, q, params(p));
+    };
+    auto flush = [&](int q) {  // make the pending diagonal on q explicit before a mixing gate
+        if (pending[q] != 1.0) {
+            if (!mixed[q]) din[q] *= pending[q];
+            else diag1(q, pending[q]);
+            pending[q] = 1.0;
+        }
+    };
+    auto diagonal_for_all_states = [&](const qs_gate& g) {
+        for (int s = 0; s < num_states; ++s) {
+            const double* u = mats + g.offset + uint64_t(s) * g.stride;
+            if (u[2] != 0 || u[3] != 0 || u[4] != 0 || u[5] != 0) return false;
+            if (g.stride == 0) break;
+        }
+        return true;
+    };
+
+    for (int i = 0; i < count; ++i) {
+        const qs_gate& g = gates[i];
+        if (g.kind == QS_KIND_CUTPHASE) {  // diagonal: commutes with every pending diagonal
+            out->gates.push_back(g);
+            continue;
+        }
+        const int q = g.target;
+        if (g.kind == QS_KIND_CTRL) {
+            if (!diagonal_for_all_states(g)) {
+                flush(q);
+                mixed[q] = 1;
+            }
+            out->gates.push_back(g);
+            continue;
+        }
+        // QS_KIND_1Q
+        if (g.stride != 0) {
+            if (!diagonal_for_all_states(g)) {
+                flush(q);
+                mixed[q] = 1;
+            }
+            out->gates.push_back(g);
+            continue;
+        }
+        const double* u = mats + g.offset;
+        const cd u00 = entry(u, 0), u11 = entry(u, 3);
+        if (entry(u, 1) == 0.0 && entry(u, 2) == 0.0 && std::abs(std::abs(u00) - 1.0) <= 1e-12 &&
+            std::abs(std::abs(u11) - 1.0) <= 1e-12) {
+            K *= u00;  // diag(u00, u11) = u00 * diag(1, u11/u00)
+            pending[q] *= u11 / u00;
+            continue;
+        }
+        double f[10];
+        if (!decompose_2x2(u, f)) {
+            flush(q);
+            mixed[q] = 1;
+            out->gates.push_back(g);
+            continue;
+        }
+        const cd k(f[0], f[1]), za(f[2], f[3]), zb(f[4], f[5]);
+        const cd pre = pending[q] * zb;
+        K *= k * f[8];
+        bool has_pre = false;
+        if (!mixed[q]) din[q] *= pre;
+        else has_pre = pre != 1.0;
+        const double p[8] = {f[7], f[6], has_pre ? 1.0 : 0.0, 0, pre.real(), pre.imag(), 0, 0};
+        emit(kKindShear, q, params(p));
+        out->factored++;
+        pending[q] = za;
+        mixed[q] = 1;
+        // the amplitudes grow by at most sqrt(2) per shear; a scalar pass keeps
+        // them far from overflow in very long programs
+        if (std::abs(K) < 0x1p-600) {
+            out->gates.push_back(diag_tables(std::vector<cd>(m, cd(1.0)), K));
+            K = 1.0;
+        }
+    }
+    bool any_in = false;
+    for (int q = 0; q < m; ++q) any_in |= din[q] != 1.0;
+    if (any_in) out->gates.insert(out->gates.begin(), diag_tables(din, cd(1.0)));
+    bool any_out = K != 1.0;
+    for (int q = 0; q < m; ++q) any_out |= pending[q] != 1.0;
+    if (any_out) out->gates.push_back(diag_tables(pending, K));
+}
+
+}  // namespace qsb

@@ -11,6 +11,8 @@
 //                applied in program order in register "rounds" of 4 qubits;
 //                one HBM read + write for a whole run of gates.
 #include <atomic>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -248,6 +250,86 @@ __device__ __forceinline__ void reg_gate_generic(double2 (&a)[kRegAmps], const d
     }
 }
 
+// ---- factored gates (QS_FUSE_FACTORED, factor.cu) ---------------------------
+// Shear on register bit J: (a, b) <- (a - t b, b + t a), 4 FMAs per pair.
+// With a pre-diagonal the b member is first multiplied by z (diag(1, z) on the
+// same qubit).
+template <int J>
+__device__ __forceinline__ void reg_shear(double2 (&a)[kRegAmps], const TileGate& G) {
+    const double t = G.u[0].x;
+    if (G.u[1].x != 0.0) {  // has_pre (params[2])
+        const double2 z = G.u[2];
+#pragma unroll
+        for (int k = 0; k < kRegAmps; ++k)
+            if ((k >> J) & 1) a[k] = cmul(a[k], z);
+    }
+#pragma unroll
+    for (int k = 0; k < kRegAmps; ++k) {
+        if ((k >> J) & 1) continue;
+        const double2 x = a[k], y = a[k | (1 << J)];
+        a[k] = make_double2(__fma_rn(-t, y.x, x.x), __fma_rn(-t, y.y, x.y));
+        a[k | (1 << J)] = make_double2(__fma_rn(t, x.x, y.x), __fma_rn(t, x.y, y.y));
+    }
+}
+
+template <int J>
+__device__ __forceinline__ void reg_diag1(double2 (&a)[kRegAmps], const double2 z) {
+#pragma unroll
+    for (int k = 0; k < kRegAmps; ++k)
+        if ((k >> J) & 1) a[k] = cmul(a[k], z);
+}
+
+__device__ __forceinline__ void reg_fact_generic(double2 (&a)[kRegAmps], const TileGate& G) {
+    const int j = G.variant % kRegLog2;
+    if (G.kind == kKindDiag1) {
+        const double2 z = G.u[2];
+        switch (j) {
+            case 0: reg_diag1<0>(a, z); break;
+            case 1: reg_diag1<1>(a, z); break;
+            case 2: reg_diag1<2>(a, z); break;
+            case 3: reg_diag1<(kRegLog2 > 3 ? 3 : 0)>(a, z); break;
+            default: reg_diag1<(kRegLog2 > 4 ? 4 : 0)>(a, z); break;
+        }
+        return;
+    }
+    switch (j) {
+        case 0: reg_shear<0>(a, G); break;
+        case 1: reg_shear<1>(a, G); break;
+        case 2: reg_shear<2>(a, G); break;
+        case 3: reg_shear<(kRegLog2 > 3 ? 3 : 0)>(a, G); break;
+        default: reg_shear<(kRegLog2 > 4 ? 4 : 0)>(a, G); break;
+    }
+}
+
+// A full run of kRegLog2 shears on register bits 0..kRegLog2-1 (straight line).
+__device__ __forceinline__ void reg_shear_seq_full(double2 (&a)[kRegAmps], const TileGate* G) {
+    reg_shear<0>(a, G[0]);
+    reg_shear<1>(a, G[1]);
+    reg_shear<2>(a, G[2]);
+    if (kRegLog2 > 3) reg_shear<(kRegLog2 > 3 ? 3 : 0)>(a, G[3]);
+    if (kRegLog2 > 4) reg_shear<(kRegLog2 > 4 ? 4 : 0)>(a, G[4]);
+}
+
+// Product diagonal D(i) = prod_c T_c[byte c of i] (kKindDiagN).  The k = 0
+// register amplitude's factor comes from the byte tables and multiplies all 16
+// amplitudes; then each register qubit's z multiplies the half with its bit
+// set.  (16 + 32 complex products instead of the 31 of a factor table, but
+// only a few live registers next to the 16 amplitudes.)
+__device__ __forceinline__ void reg_diag_n(double2 (&a)[kRegAmps], const double2* T, int ntab,
+                                           uint64_t il, const double2* zq, const int (&rq)[kRegLog2]) {
+    double2 f = __ldg(T + (il & 255));
+    for (int c = 1; c < ntab; ++c) f = cmul(f, __ldg(T + (c << 8) + ((il >> (8 * c)) & 255)));
+#pragma unroll
+    for (int k = 0; k < kRegAmps; ++k) a[k] = cmul(a[k], f);
+#pragma unroll
+    for (int j = 0; j < kRegLog2; ++j) {
+        const double2 z = __ldg(zq + rq[j]);
+#pragma unroll
+        for (int k = 0; k < kRegAmps; ++k)
+            if ((k >> j) & 1) a[k] = cmul(a[k], z);
+    }
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
@@ -305,7 +387,7 @@ constexpr int kDepTables = 4;  // tile index up to 32 bits (m <= 44)
 #ifndef QSB_PASS_SMEM
 #define QSB_PASS_PARAM 1
 #endif
-template <bool PHASE, bool GENERIC, bool TABLES>
+template <bool PHASE, bool GENERIC, bool TABLES, bool FACT>
 __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
 #ifdef QSB_PASS_PARAM
     k_tile(double2* __restrict__ psi, const __grid_constant__ TilePass pass_param,
@@ -527,6 +609,23 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                         for (int k = 0; k < kRegAmps; ++k) a[k] = cmul(a[k], __ldg(lut + cuts[k]));
                         continue;
                     }
+                    if (FACT && G.kind >= kKindShear) {
+                        if (G.kind == kKindDiagN) {
+                            const double2* T = reinterpret_cast<const double2*>(mats + G.offset);
+                            int rq[kRegLog2];
+#pragma unroll
+                            for (int j = 0; j < kRegLog2; ++j) rq[j] = P.tile_bits[__ffs(R.dk[1 << j]) - 1];
+                            reg_diag_n(a, T, G.cval,
+                                       base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask),
+                                       T + (G.cval << 8), rq);
+                        } else if (G.seq == kRegLog2) {
+                            reg_shear_seq_full(a, &G);
+                            g += kRegLog2 - 1;
+                        } else {
+                            reg_fact_generic(a, G);
+                        }
+                        continue;
+                    }
                     if (G.seq == kRegLog2) {
                         reg_seq_full<TABLES>(a, &G, tm_cur + 4 * g);
                         g += kRegLog2 - 1;
@@ -625,6 +724,525 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
     if (kPingPong && group == 0) named_sync(3, kCtaThreads);  // consume group 1's last hand-over
 }
 
+// ---- lean fused pass for factored programs -------------------------------------
+// A pass whose gates are only shears (QS_FUSE_FACTORED) and the product
+// diagonals at its ends: each register round is a run of n <= kRegLog2 shears
+// on register bits 0..n-1 in order, so the round's parameters are read with
+// compile-time offsets and no per-gate dispatch is left in the loop (k_tile's
+// generic gate loop costs more integer work and registers than the 2 FP64
+// instructions per amplitude a shear needs).
+struct FactRound {
+    double t[kRegLog2];      // 0 for register bits without a shear (exact identity)
+    double2 pre[kRegLog2];   // (1, 0) without a pre-diagonal
+    int32_t rq[kRegLog2];    // qubit held by register bit j (product diagonals)
+    int32_t n, pre_mask, pad0, pad1;
+};
+struct alignas(16) FactPass {
+    int32_t m, num_rounds, low_run, direct_store;
+    int32_t tile_bits[kTileLog2];
+    int32_t ntab, has_din, has_dout, pad;
+    uint64_t tiles_per_state, num_tiles;
+    uint64_t din_off, dout_off;  // DiagN tables in mats (doubles)
+    Round rounds[kMaxRounds];
+    FactRound fr[kMaxRounds];
+};
+
+template <int J, bool PRE>
+__device__ __forceinline__ void fact_shear(double2 (&a)[kRegAmps], const FactRound& F) {
+    const double t = F.t[J];
+    if (PRE) {
+        const double2 z = F.pre[J];
+#pragma unroll
+        for (int k = 0; k < kRegAmps; ++k)
+            if ((k >> J) & 1) a[k] = cmul(a[k], z);
+    }
+#pragma unroll
+    for (int k = 0; k < kRegAmps; ++k) {
+        if ((k >> J) & 1) continue;
+        const double2 x = a[k], y = a[k | (1 << J)];
+        a[k] = make_double2(__fma_rn(-t, y.x, x.x), __fma_rn(-t, y.y, x.y));
+        a[k | (1 << J)] = make_double2(__fma_rn(t, x.x, y.x), __fma_rn(t, x.y, y.y));
+    }
+}
+
+// One register round of a lean pass, straight-line for its flags: product
+// diagonal before (DIN) / after (DOUT) the shears, pre-diagonals (PRE), and the
+// store of the 16 amplitudes to HBM (GSTORE) or back to the shared tile.  Every
+// round applies kRegLog2 shears (t = 0 is an exact identity), so no amplitude
+// register is live across a data-dependent branch (each join would cost 64
+// register moves).
+template <bool DIN, bool PRE, bool DOUT, bool GSTORE>
+__device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass& P,
+                                          const FactRound& F, const double* __restrict__ mats,
+                                          uint64_t il, double2* tile, int sb,
+                                          const int (&skb)[kRegLog2], double2* gb,
+                                          const uint64_t (&okb)[kRegLog2]) {
+    if (DIN) {
+        const double2* T = reinterpret_cast<const double2*>(mats + P.din_off);
+        reg_diag_n(a, T, P.ntab, il, T + (P.ntab << 8), F.rq);
+    }
+    fact_shear<0, PRE>(a, F);
+    fact_shear<1, PRE>(a, F);
+    fact_shear<2, PRE>(a, F);
+    if (kRegLog2 > 3) fact_shear<(kRegLog2 > 3 ? 3 : 0), PRE>(a, F);
+    if (kRegLog2 > 4) fact_shear<(kRegLog2 > 4 ? 4 : 0), PRE>(a, F);
+    if (DOUT) {
+        const double2* T = reinterpret_cast<const double2*>(mats + P.dout_off);
+        reg_diag_n(a, T, P.ntab, il, T + (P.ntab << 8), F.rq);
+    }
+    if (GSTORE) {
+#pragma unroll
+        for (int k = 0; k < kRegAmps; ++k) {
+            uint64_t o = 0;
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j)
+                if ((k >> j) & 1) o += okb[j];
+            gb[o] = a[k];
+        }
+    } else {
+        int sbs = sb;
+        asm volatile("" : "+r"(sbs));
+#pragma unroll
+        for (int k = 0; k < kRegAmps; ++k) {
+            int v = 0;
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j)
+                if ((k >> j) & 1) v ^= skb[j];
+            tile[sbs ^ v] = a[k];
+        }
+    }
+}
+
+#define QSB_FACT_DISPATCH(sel, ...)                                   \
+    switch (sel) {                                                    \
+        case 0: fact_body<0, 0, 0, 0>(__VA_ARGS__); break;            \
+        case 1: fact_body<1, 0, 0, 0>(__VA_ARGS__); break;            \
+        case 2: fact_body<0, 1, 0, 0>(__VA_ARGS__); break;            \
+        case 3: fact_body<1, 1, 0, 0>(__VA_ARGS__); break;            \
+        case 4: fact_body<0, 0, 1, 0>(__VA_ARGS__); break;            \
+        case 5: fact_body<1, 0, 1, 0>(__VA_ARGS__); break;            \
+        case 6: fact_body<0, 1, 1, 0>(__VA_ARGS__); break;            \
+        case 7: fact_body<1, 1, 1, 0>(__VA_ARGS__); break;            \
+        case 8: fact_body<0, 0, 0, 1>(__VA_ARGS__); break;            \
+        case 9: fact_body<1, 0, 0, 1>(__VA_ARGS__); break;            \
+        case 10: fact_body<0, 1, 0, 1>(__VA_ARGS__); break;           \
+        case 11: fact_body<1, 1, 0, 1>(__VA_ARGS__); break;           \
+        case 12: fact_body<0, 0, 1, 1>(__VA_ARGS__); break;           \
+        case 13: fact_body<1, 0, 1, 1>(__VA_ARGS__); break;           \
+        case 14: fact_body<0, 1, 1, 1>(__VA_ARGS__); break;           \
+        default: fact_body<1, 1, 1, 1>(__VA_ARGS__); break;           \
+    }
+
+__global__ void __launch_bounds__(kTileThreads, QSB_TILE_MINB)
+    k_fact(double2* __restrict__ psi, const __grid_constant__ FactPass P,
+           const double* __restrict__ mats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* tile = reinterpret_cast<double2*>(smem_raw);
+    uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double2) * kTileAmps);
+    uint64_t* dep = rowoff + (kTileAmps >> kLowBits);
+    uint32_t* rlo = reinterpret_cast<uint32_t*>(dep + 256 * kDepTables);
+    uint32_t* rhi = rlo + kMaxRounds * (1 << kLaneLoBits);
+    const int tid = threadIdx.x;
+    for (int i = tid; i < P.num_rounds * (1 << kLaneLoBits); i += kTileThreads) {
+        const Round& R = P.rounds[i >> kLaneLoBits];
+        const int v = i & ((1 << kLaneLoBits) - 1);
+        rlo[i] = uint32_t(R.dlo[v]) | (uint32_t(R.slo[v]) << 16);
+    }
+    for (int i = tid; i < P.num_rounds * (1 << kLaneHiBits); i += kTileThreads) {
+        const Round& R = P.rounds[i >> kLaneHiBits];
+        const int v = i & ((1 << kLaneHiBits) - 1);
+        rhi[i] = uint32_t(R.dhi[v]) | (uint32_t(R.shi[v]) << 16);
+    }
+    const int low_run = P.low_run;
+    const int nrows = kTileAmps >> low_run;
+    const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
+    for (int r = tid; r < nrows; r += kTileThreads) {
+        uint64_t off = 0;
+        for (int k = 0; k < kTileLog2 - low_run; ++k)
+            if ((r >> k) & 1) off |= uint64_t(1) << P.tile_bits[low_run + k];
+        rowoff[r] = off;
+    }
+    for (int i = tid; i < kDepTables * 256; i += kTileThreads) {
+        // tile index bit b lands on the b-th non-tile qubit (ascending)
+        const int c = i >> 8, v = i & 255;
+        uint64_t out = 0;
+        for (int b = 0; b < 8; ++b) {
+            if (!((v >> b) & 1)) continue;
+            int want = 8 * c + b, cnt = 0;
+            for (int q = 0, k = 0; q < P.m; ++q) {
+                if (k < kTileLog2 && P.tile_bits[k] == q) {
+                    ++k;
+                    continue;
+                }
+                if (cnt++ == want) {
+                    out |= uint64_t(1) << q;
+                    break;
+                }
+            }
+        }
+        dep[i] = out;
+    }
+    __syncthreads();
+
+    const int m = P.m;
+    const int tps_log2 = m - kTileLog2;
+    const uint64_t stride_tiles = gridDim.x;
+    auto tile_base = [&](uint64_t t) {
+        const uint64_t x = t & (P.tiles_per_state - 1);
+        uint64_t out = 0;
+#pragma unroll
+        for (int c = 0; c < kDepTables; ++c) out |= dep[(c << 8) | ((x >> (8 * c)) & 255)];
+        return out;
+    };
+    auto goff = [&](int e) { return rowoff[e >> low_run] + (uint64_t(e) & lowmask); };
+    const uint64_t goff_tid = goff(tid);
+    const int swz_tid = swz(tid);
+    auto prefetch = [&](uint64_t t) {
+        if (t < P.num_tiles) {
+            const double2* g = psi + (((t >> tps_log2) << m) | tile_base(t)) + goff_tid;
+#pragma unroll
+            for (int i = 0; i < kLoadsPerThread; ++i)
+                cp_async16(tile + (swz_tid ^ swz(i * kTileThreads)), g + goff(i * kTileThreads));
+        }
+        cp_async_commit();
+    };
+    const bool direct = P.direct_store != 0;
+    prefetch(blockIdx.x);
+
+    for (uint64_t tile_id = blockIdx.x; tile_id < P.num_tiles; tile_id += stride_tiles) {
+        const uint64_t base_local = tile_base(tile_id);
+        double2* gbase = psi + (((tile_id >> tps_log2) << m) | base_local);
+        cp_async_wait_all();
+        named_sync(1, kTileThreads);
+        for (int r = 0; r < P.num_rounds; ++r) {
+            const Round& R = P.rounds[r];
+            const bool last = r == P.num_rounds - 1;
+            const uint32_t lo = rlo[(r << kLaneLoBits) | (tid & ((1 << kLaneLoBits) - 1))];
+            const uint32_t hi = rhi[(r << kLaneHiBits) | (tid >> kLaneLoBits)];
+            const int eb = int((lo | hi) & 0xffff);
+            const int sb = int((lo ^ hi) >> 16);
+            int skb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) skb[j] = R.sk[1 << j];
+            auto sk_of = [&](int k) {
+                int v = 0;
+#pragma unroll
+                for (int j = 0; j < kRegLog2; ++j)
+                    if ((k >> j) & 1) v ^= skb[j];
+                return v;
+            };
+            double2 a[kRegAmps];
+#pragma unroll
+            for (int k = 0; k < kRegAmps; ++k) a[k] = tile[sb ^ sk_of(k)];
+            if (last && direct) {
+                named_sync(1, kTileThreads);
+                prefetch(tile_id + stride_tiles);
+            }
+            const FactRound& F = P.fr[r];
+            const bool gstore = last && direct;
+            const int sel = int(r == 0 && P.has_din) | (F.pre_mask ? 2 : 0) |
+                            int(last && P.has_dout) << 2 | int(gstore) << 3;
+            const uint64_t il = base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask);
+            uint64_t okb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) okb[j] = gstore ? goff(R.dk[1 << j]) : 0;
+            double2* gb = gbase + (gstore ? goff(eb) : 0);
+            QSB_FACT_DISPATCH(sel, a, P, F, mats, il, tile, sb, skb, gb, okb)
+            if (gstore) break;
+            named_sync(1, kTileThreads);
+        }
+        if (!direct) {
+            double2* gb = gbase + goff_tid;
+#pragma unroll
+            for (int i = 0; i < kLoadsPerThread; ++i)
+                gb[goff(i * kTileThreads)] = tile[swz_tid ^ swz(i * kTileThreads)];
+            named_sync(1, kTileThreads);
+            prefetch(tile_id + stride_tiles);
+        }
+    }
+}
+
+// ---- the same pass with a 3-buffer ring ---------------------------------------
+// One CTA per SM, two groups of 256 threads, three 64 KiB tile buffers.  Tile
+// sequence i of the CTA lives in buffer i % 3 and is processed by group i % 2;
+// when a group has read tile i's buffer into registers (its last round) it
+// refills that buffer with tile i + 3 -- which the OTHER group will process --
+// so a load has about one tile-processing time of lead instead of the last
+// round's.  cp.async completion is signalled on a per-buffer mbarrier
+// (cp.async.mbarrier.arrive.noinc, 256 arrivals per fill), so the consuming
+// group waits on the barrier's phase, not on its own cp.async groups.
+constexpr int kRingBufs = 3;
+constexpr int kRingGroups = 2;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kRingGroups * kTileThreads, 1)
+    k_fact_ring(double2* __restrict__ psi, const __grid_constant__ FactPass P,
+                const double* __restrict__ mats) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2* tiles = reinterpret_cast<double2*>(smem_raw);
+    uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double2) * kTileAmps * kRingBufs);
+    uint64_t* dep = rowoff + (kTileAmps >> kLowBits);
+    uint32_t* rlo = reinterpret_cast<uint32_t*>(dep + 256 * kDepTables);
+    uint32_t* rhi = rlo + kMaxRounds * (1 << kLaneLoBits);
+    uint64_t* full = reinterpret_cast<uint64_t*>(rhi + kMaxRounds * (1 << kLaneHiBits));
+    constexpr int kThreads = kRingGroups * kTileThreads;
+    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneLoBits); i += kThreads) {
+        const Round& R = P.rounds[i >> kLaneLoBits];
+        const int v = i & ((1 << kLaneLoBits) - 1);
+        rlo[i] = uint32_t(R.dlo[v]) | (uint32_t(R.slo[v]) << 16);
+    }
+    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneHiBits); i += kThreads) {
+        const Round& R = P.rounds[i >> kLaneHiBits];
+        const int v = i & ((1 << kLaneHiBits) - 1);
+        rhi[i] = uint32_t(R.dhi[v]) | (uint32_t(R.shi[v]) << 16);
+    }
+    const int low_run = P.low_run;
+    const int nrows = kTileAmps >> low_run;
+    const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
+    for (int r = threadIdx.x; r < nrows; r += kThreads) {
+        uint64_t off = 0;
+        for (int k = 0; k < kTileLog2 - low_run; ++k)
+            if ((r >> k) & 1) off |= uint64_t(1) << P.tile_bits[low_run + k];
+        rowoff[r] = off;
+    }
+    for (int i = threadIdx.x; i < kDepTables * 256; i += kThreads) {
+        const int c = i >> 8, v = i & 255;
+        uint64_t out = 0;
+        for (int b = 0; b < 8; ++b) {
+            if (!((v >> b) & 1)) continue;
+            int want = 8 * c + b, cnt = 0;
+            for (int q = 0, k = 0; q < P.m; ++q) {
+                if (k < kTileLog2 && P.tile_bits[k] == q) {
+                    ++k;
+                    continue;
+                }
+                if (cnt++ == want) {
+                    out |= uint64_t(1) << q;
+                    break;
+                }
+            }
+        }
+        dep[i] = out;
+    }
+    if (threadIdx.x < kRingBufs) mbar_init(full + threadIdx.x, kTileThreads);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    __syncthreads();
+
+    const int group = threadIdx.x / kTileThreads;
+    const int tid = threadIdx.x % kTileThreads;
+    const int gbar = 1 + group;
+    const int m = P.m;
+    const int tps_log2 = m - kTileLog2;
+    const uint64_t grid = gridDim.x;
+    auto tile_of = [&](uint64_t i) { return uint64_t(blockIdx.x) + i * grid; };
+    auto tile_base = [&](uint64_t t) {
+        const uint64_t x = t & (P.tiles_per_state - 1);
+        uint64_t out = 0;
+#pragma unroll
+        for (int c = 0; c < kDepTables; ++c) out |= dep[(c << 8) | ((x >> (8 * c)) & 255)];
+        return out;
+    };
+    auto goff = [&](int e) { return rowoff[e >> low_run] + (uint64_t(e) & lowmask); };
+    const uint64_t goff_tid = goff(tid);
+    const int swz_tid = swz(tid);
+    // the issuing group's 256 threads each arrive once on the buffer's barrier
+    auto fill = [&](uint64_t i) {
+        const uint64_t t = tile_of(i);
+        if (t >= P.num_tiles) return;
+        double2* buf = tiles + int(i % kRingBufs) * kTileAmps;
+        const double2* g = psi + (((t >> tps_log2) << m) | tile_base(t)) + goff_tid;
+#pragma unroll
+        for (int k = 0; k < kLoadsPerThread; ++k)
+            cp_async16(buf + (swz_tid ^ swz(k * kTileThreads)), g + goff(k * kTileThreads));
+        cp_async_arrive_noinc(full + int(i % kRingBufs));
+    };
+    if (group == 0) {
+        fill(0);
+        fill(2);
+    } else {
+        fill(1);
+    }
+    const bool direct = P.direct_store != 0;
+
+    for (uint64_t i = group; tile_of(i) < P.num_tiles; i += kRingGroups) {
+        const uint64_t tile_id = tile_of(i);
+        const uint64_t base_local = tile_base(tile_id);
+        double2* gbase = psi + (((tile_id >> tps_log2) << m) | base_local);
+        double2* tile = tiles + int(i % kRingBufs) * kTileAmps;
+        mbar_wait(full + int(i % kRingBufs), unsigned((i / kRingBufs) & 1));
+        for (int r = 0; r < P.num_rounds; ++r) {
+            const Round& R = P.rounds[r];
+            const bool last = r == P.num_rounds - 1;
+            const uint32_t lo = rlo[(r << kLaneLoBits) | (tid & ((1 << kLaneLoBits) - 1))];
+            const uint32_t hi = rhi[(r << kLaneHiBits) | (tid >> kLaneLoBits)];
+            const int eb = int((lo | hi) & 0xffff);
+            const int sb = int((lo ^ hi) >> 16);
+            int skb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) skb[j] = R.sk[1 << j];
+            auto sk_of = [&](int k) {
+                int v = 0;
+#pragma unroll
+                for (int j = 0; j < kRegLog2; ++j)
+                    if ((k >> j) & 1) v ^= skb[j];
+                return v;
+            };
+            double2 a[kRegAmps];
+#pragma unroll
+            for (int k = 0; k < kRegAmps; ++k) a[k] = tile[sb ^ sk_of(k)];
+            if (last && direct) {
+                named_sync(gbar, kTileThreads);
+                fill(i + kRingBufs);
+            }
+            const FactRound& F = P.fr[r];
+            const bool gstore = last && direct;
+            const int sel = int(r == 0 && P.has_din) | (F.pre_mask ? 2 : 0) |
+                            int(last && P.has_dout) << 2 | int(gstore) << 3;
+            const uint64_t il = base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask);
+            uint64_t okb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) okb[j] = gstore ? goff(R.dk[1 << j]) : 0;
+            double2* gb = gbase + (gstore ? goff(eb) : 0);
+            QSB_FACT_DISPATCH(sel, a, P, F, mats, il, tile, sb, skb, gb, okb)
+            if (gstore) break;
+            named_sync(gbar, kTileThreads);
+        }
+        if (!direct) {
+            double2* gb = gbase + goff_tid;
+#pragma unroll
+            for (int k = 0; k < kLoadsPerThread; ++k)
+                gb[goff(k * kTileThreads)] = tile[swz_tid ^ swz(k * kTileThreads)];
+            named_sync(gbar, kTileThreads);
+            fill(i + kRingBufs);
+        }
+    }
+}
+
+size_t fact_ring_smem_bytes() {
+    return sizeof(double2) * kTileAmps * kRingBufs + sizeof(uint64_t) * (kTileAmps >> kLowBits) +
+           sizeof(uint64_t) * 256 * kDepTables +
+           sizeof(uint32_t) * kMaxRounds * ((1 << kLaneLoBits) + (1 << kLaneHiBits)) +
+           sizeof(uint64_t) * kRingBufs;
+}
+
+void launch_fact_ring(double2* psi, const FactPass& F, const double* mats, cudaStream_t s) {
+    constexpr int kMaxDevices = 64;
+    static std::atomic<int> configured[kMaxDevices];
+    static int sms_of[kMaxDevices];
+    const size_t smem = fact_ring_smem_bytes();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (configured[dev].load(std::memory_order_acquire) == 0) {
+        cudaFuncSetAttribute(k_fact_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        sms_of[dev] = sms;
+        configured[dev].store(1, std::memory_order_release);
+    }
+    uint64_t grid = uint64_t(sms_of[dev]);
+    if (grid > F.num_tiles) grid = F.num_tiles;
+    k_fact_ring<<<unsigned(grid), kRingGroups * kTileThreads, smem, s>>>(psi, F, mats);
+}
+
+// The lean kernel applies when every gate of the pass is a shear in in-order
+// register runs, with product diagonals only first in round 0 / last in the
+// last round.
+bool fact_pass_from(const TilePass& T, FactPass* F) {
+    memset(F, 0, sizeof(*F));
+    F->m = T.m;
+    F->num_rounds = T.num_rounds;
+    F->low_run = T.low_run;
+    F->direct_store = T.direct_store;
+    memcpy(F->tile_bits, T.tile_bits, sizeof(F->tile_bits));
+    F->tiles_per_state = T.tiles_per_state;
+    F->num_tiles = T.num_tiles;
+    memcpy(F->rounds, T.rounds, sizeof(Round) * T.num_rounds);
+    for (int r = 0; r < T.num_rounds; ++r) {
+        const Round& R = T.rounds[r];
+        FactRound& FR = F->fr[r];
+        for (int j = 0; j < kRegLog2; ++j) {
+            FR.t[j] = 0.0;
+            FR.pre[j] = make_double2(1.0, 0.0);
+            FR.rq[j] = T.tile_bits[__builtin_ctz(R.dk[1 << j])];
+        }
+        for (int g = R.first_gate; g < R.first_gate + R.num_gates; ++g) {
+            const TileGate& G = T.gates[g];
+            if (G.kind == kKindDiagN) {
+                if (r == 0 && g == 0 && !F->has_din) {
+                    F->has_din = 1;
+                    F->din_off = G.offset;
+                } else if (r == T.num_rounds - 1 && g == R.first_gate + R.num_gates - 1) {
+                    F->has_dout = 1;
+                    F->dout_off = G.offset;
+                } else {
+                    return false;
+                }
+                F->ntab = G.cval;
+                continue;
+            }
+            if (G.kind != kKindShear || G.variant != FR.n || FR.n >= kRegLog2) return false;
+            if (F->has_dout) return false;  // D_out must be the last op
+            if (G.u[0].y != 0.0) return false;  // only form A shears exist
+            FR.t[FR.n] = G.u[0].x;
+            if (G.u[1].x != 0.0) {
+                FR.pre_mask |= 1 << FR.n;
+                FR.pre[FR.n] = G.u[2];
+            }
+            FR.n++;
+        }
+    }
+    return true;
+}
+
+size_t fact_smem_bytes() {
+    return sizeof(double2) * kTileAmps + sizeof(uint64_t) * (kTileAmps >> kLowBits) +
+           sizeof(uint64_t) * 256 * kDepTables +
+           sizeof(uint32_t) * kMaxRounds * ((1 << kLaneLoBits) + (1 << kLaneHiBits));
+}
+
+void launch_fact(double2* psi, const FactPass& F, const double* mats, cudaStream_t s) {
+    constexpr int kMaxDevices = 64;
+    static std::atomic<int> configured[kMaxDevices];
+    static int sms_of[kMaxDevices], per_sm_of[kMaxDevices];
+    const size_t smem = fact_smem_bytes();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (configured[dev].load(std::memory_order_acquire) == 0) {
+        cudaFuncSetAttribute(k_fact, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int sms = 148, per_sm = 1;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fact, kTileThreads, smem);
+        sms_of[dev] = sms;
+        per_sm_of[dev] = per_sm < 1 ? 1 : per_sm;
+        configured[dev].store(1, std::memory_order_release);
+    }
+    uint64_t grid = uint64_t(sms_of[dev]) * per_sm_of[dev];
+    if (grid > F.num_tiles) grid = F.num_tiles;
+    k_fact<<<unsigned(grid), kTileThreads, smem, s>>>(psi, F, mats);
+}
+
 __global__ void k_fill(double2* __restrict__ psi, uint64_t count, double2 value) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
          i += uint64_t(gridDim.x) * blockDim.x)
@@ -719,7 +1337,7 @@ size_t tile_smem_bytes() {
            2 * sizeof(double2) * 4 * kMaxPassGates;
 }
 
-template <bool PH, bool GE, bool TB>
+template <bool PH, bool GE, bool TB, bool FA>
 void launch_tile_variant(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                          const double* mats,
                          const CutTerms& ct, uint64_t num_tiles, cudaStream_t s) {
@@ -732,10 +1350,10 @@ void launch_tile_variant(double2* psi, const TilePass& pass, const TilePass* pas
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= kMaxDevices) dev = 0;
     if (configured[dev].load(std::memory_order_acquire) == 0) {
-        cudaFuncSetAttribute(k_tile<PH, GE, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_tile<PH, GE, TB, FA>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         int sms = 148, per_sm = 1;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<PH, GE, TB>, kCtaThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tile<PH, GE, TB, FA>, kCtaThreads, smem);
         sms_of[dev] = sms;
         per_sm_of[dev] = per_sm < 1 ? 1 : per_sm;
         configured[dev].store(1, std::memory_order_release);
@@ -745,22 +1363,25 @@ void launch_tile_variant(double2* psi, const TilePass& pass, const TilePass* pas
     if (grid > need) grid = need;
 #ifdef QSB_PASS_PARAM
     (void)pass_dev;
-    k_tile<PH, GE, TB><<<unsigned(grid), kCtaThreads, smem, s>>>(psi, pass, mats, ct);
+    k_tile<PH, GE, TB, FA><<<unsigned(grid), kCtaThreads, smem, s>>>(psi, pass, mats, ct);
 #else
     (void)pass;
-    k_tile<PH, GE, TB><<<unsigned(grid), kCtaThreads, smem, s>>>(psi, pass_dev, mats, ct);
+    k_tile<PH, GE, TB, FA><<<unsigned(grid), kCtaThreads, smem, s>>>(psi, pass_dev, mats, ct);
 #endif
 }
 
-void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
+bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                       const double* mats, const CutTerms& ct, cudaStream_t s) {
-    bool phase = false, generic = false, tables = false;
+    bool phase = false, generic = false, tables = false, fact = false;
     for (int r = 0; r < pass.num_rounds; ++r) {
         const Round& R = pass.rounds[r];
         for (int g = R.first_gate; g < R.first_gate + R.num_gates; ++g) {
             const TileGate& G = pass.gates[g];
             if (G.kind == QS_KIND_CUTPHASE) {
                 phase = true;
+            } else if (G.kind >= kKindShear) {
+                fact = true;
+                if (G.seq > 0) g += G.seq - 1;
             } else {
                 // a sequence run covers G.seq gates; any of them may use a table
                 const int run = G.seq > 0 ? G.seq : 1;
@@ -771,18 +1392,35 @@ void launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_d
         }
     }
     const uint64_t nt = pass.num_tiles;
-#define QSB_TILE_CASE(PH, GE, TB) \
-    if (phase == PH && generic == GE && tables == TB) \
-        return launch_tile_variant<PH, GE, TB>(psi, pass, pass_dev, mats, ct, nt, s);
-    QSB_TILE_CASE(false, false, false)
-    QSB_TILE_CASE(false, false, true)
-    QSB_TILE_CASE(false, true, false)
-    QSB_TILE_CASE(false, true, true)
-    QSB_TILE_CASE(true, false, false)
-    QSB_TILE_CASE(true, false, true)
-    QSB_TILE_CASE(true, true, false)
-    QSB_TILE_CASE(true, true, true)
+    static const bool lean_ok = getenv("QSB_NO_LEAN") == nullptr;
+    if (fact && !phase && !generic && !tables && kGroups == 1 && lean_ok) {
+        static thread_local FactPass F;
+        static const bool ring = getenv("QSB_FACT_RING") != nullptr;  // measured slower
+        if (fact_pass_from(pass, &F)) {
+            if (ring) launch_fact_ring(psi, F, mats, s);
+            else launch_fact(psi, F, mats, s);
+            return true;
+        }
+    }
+#define QSB_TILE_CASE(PH, GE, TB, FA) \
+    if (phase == PH && generic == GE && tables == TB && fact == FA) {       \
+        launch_tile_variant<PH, GE, TB, FA>(psi, pass, pass_dev, mats, ct, nt, s); \
+        return false;                                                        \
+    }
+#define QSB_TILE_CASES(FA)               \
+    QSB_TILE_CASE(false, false, false, FA) \
+    QSB_TILE_CASE(false, false, true, FA)  \
+    QSB_TILE_CASE(false, true, false, FA)  \
+    QSB_TILE_CASE(false, true, true, FA)   \
+    QSB_TILE_CASE(true, false, false, FA)  \
+    QSB_TILE_CASE(true, false, true, FA)   \
+    QSB_TILE_CASE(true, true, false, FA)   \
+    QSB_TILE_CASE(true, true, true, FA)
+    QSB_TILE_CASES(false)
+    QSB_TILE_CASES(true)
+#undef QSB_TILE_CASES
 #undef QSB_TILE_CASE
+    return false;
 }
 
 int prof_read(unsigned long long* out) {

@@ -1,0 +1,233 @@
+"""GPU parity of QS_FUSE_FACTORED (include/qsb200.h, csrc/factor.cu).
+
+The factored rewrite computes the same operator as the reference's gate-by-gate
+numpy update (statevector.py:144-150) with different rounding, so the bar is
+the north_star tolerance, not bit equality: max |d amplitude| <= 1e-12
+(absolute) and expectation values within 1e-10 relative.  The oracle and the
+reference's golden vectors are the checkers, as in test_gpu_parity.py.
+"""
+import numpy as np
+import pytest
+
+import paper_2001_10554_b200 as qs
+from paper_2001_10554_b200 import _native as N
+from paper_2001_10554_b200 import runtime
+from paper_2001_10554_b200.circuit import Circuit, build_qaoa_circuit, qaoa_bindings
+from paper_2001_10554_b200.graphs import make_graph
+
+from conftest import bits_equal, golden, max_dev
+
+from oracle import circuit as ocirc
+from oracle import gates as ogates
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12       # amplitudes, absolute (north_star)
+RTOL_OBS = 1e-10  # expectation values, relative (north_star)
+FACT = "factored"
+
+H = np.array([[1, 1], [1, -1]], dtype=np.complex128) / np.sqrt(2)
+X = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+
+
+def mixed_program(n, count, rng):
+    """Everything the rewrite distinguishes: Haar (both shear forms), exactly
+    anti-diagonal (X), exactly diagonal (RZ, phase), rotations, controlled
+    Haar / CNOT (mixing the target), CPhase (diagonal controlled), cut phases."""
+    edges = [(0, 3), (2, 7), (5, 11), (1, n - 1), (4, 9)]
+    out = []
+    for _ in range(count):
+        r = rng.random()
+        q = int(rng.integers(n))
+        if r < 0.45:
+            out.append({"kind": "custom", "qubits": (q,), "matrix": ogates.random_unitary_2x2(rng)})
+        elif r < 0.52:
+            out.append({"kind": "custom", "qubits": (q,), "matrix": X})
+        elif r < 0.60:
+            out.append({"kind": "custom", "qubits": (q,), "matrix": H})
+        elif r < 0.68:
+            out.append({"kind": "custom", "qubits": (q,),
+                        "matrix": ogates.rz(float(rng.uniform(0, 6.3)))})
+        elif r < 0.74:
+            out.append({"kind": "custom", "qubits": (q,),
+                        "matrix": ogates.rx(float(rng.uniform(0, 6.3)))})
+        else:
+            t = int(rng.integers(n - 1))
+            t = t if t < q else t + 1
+            rr = rng.random()
+            if rr < 0.4:
+                u = ogates.random_unitary_2x2(rng)
+            elif rr < 0.7:
+                u = X
+            else:
+                u = np.diag([1.0, np.exp(1j * rng.uniform(0, 6.3))]).astype(np.complex128)
+            if rng.random() < 0.15:
+                out.append({"kind": "diagcost", "param": float(rng.uniform(0, 6.28)),
+                            "edges": edges})
+            else:
+                out.append({"kind": "cu", "qubits": (q, t), "matrix": u})
+    return out, edges
+
+
+def run_queue(n, prog, edges, psi0, fuse):
+    st = N.DeviceState(n, n)
+    st.upload(psi0)
+    graph = make_graph(n, edges)
+    q = runtime.GateQueue(st, fuse=fuse)
+    for g in prog:
+        if g["kind"] == "custom":
+            q.one_qubit(g["qubits"][0], g["matrix"])
+        elif g["kind"] == "cu":
+            q.controlled(*g["qubits"], g["matrix"])
+        else:
+            q.cut_phase(graph, g["param"])
+    passes = q.flush()
+    return st.download(), passes
+
+
+@pytest.mark.parametrize("n", [12, 14, 17])
+def test_factored_random_programs_within_tolerance(n):
+    rng = np.random.default_rng(700 + n)
+    for trial in range(3):
+        prog, edges = mixed_program(n, 90, rng)
+        psi0 = ogates.random_state(n, rng)
+        expect = ocirc.run(n, prog, psi0)
+        got, passes = run_queue(n, prog, edges, psi0, FACT)
+        assert max_dev(got, expect) <= TOL, f"n={n} trial={trial}"
+        assert passes < len(prog)
+
+
+def test_factored_layer_is_not_the_exact_path():
+    """The rewrite really runs (different rounding) and stays within 1e-12."""
+    n = 14
+    rng = np.random.default_rng(3)
+    prog = [{"kind": "custom", "qubits": (q,), "matrix": ogates.random_unitary_2x2(rng)}
+            for q in range(n)]
+    psi0 = ogates.random_state(n, rng)
+    exact, _ = run_queue(n, prog, [], psi0, True)
+    fact, _ = run_queue(n, prog, [], psi0, FACT)
+    assert bits_equal(exact, ocirc.run(n, prog, psi0))
+    assert not bits_equal(exact, fact)
+    assert max_dev(exact, fact) <= TOL
+
+
+def test_factored_only_diagonals_and_only_x():
+    n = 13
+    rng = np.random.default_rng(4)
+    psi0 = ogates.random_state(n, rng)
+    for prog in (
+        [{"kind": "custom", "qubits": (q,), "matrix": ogates.rz(0.1 + q)} for q in range(n)],
+        [{"kind": "custom", "qubits": (q % n,), "matrix": X} for q in range(2 * n + 1)],
+        [{"kind": "custom", "qubits": (5,), "matrix": H}] * 7,
+    ):
+        got, _ = run_queue(n, prog, [], psi0, FACT)
+        assert max_dev(got, ocirc.run(n, prog, psi0)) <= TOL
+
+
+def test_factored_long_program_rescales():
+    """1400 Hadamards: the shear scales multiply to 2^-700, beyond the 2^-600
+    guard, so the rewrite inserts scalar passes; the state stays normal."""
+    n = 12
+    rng = np.random.default_rng(5)
+    psi0 = ogates.random_state(n, rng)
+    prog = [{"kind": "custom", "qubits": (int(q),), "matrix": H}
+            for q in rng.integers(0, n, size=1400)]
+    got, _ = run_queue(n, prog, [], psi0, FACT)
+    assert max_dev(got, ocirc.run(n, prog, psi0)) <= TOL
+
+
+KINDS = {0: "h", 1: "rx", 2: "rz", 3: "cx"}
+
+
+def decode(arr):
+    from paper_2001_10554_b200.circuit import GateSpec
+    out = []
+    for kind, q0, q1, param in arr:
+        k = KINDS[int(kind)]
+        if k == "cx":
+            out.append(GateSpec("cx", (int(q0), int(q1))))
+        elif k == "h":
+            out.append(GateSpec("h", (int(q0),)))
+        else:
+            out.append(GateSpec(k, (int(q0),), float(param)))
+    return out
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 4])
+def test_factored_config1_n12_golden(ranks):
+    g = golden("golden_cfg1_n12.npz")
+    circ = Circuit(12, tuple(decode(g["gates"])))
+    psi = runtime.simulate_circuit(circ, num_ranks=ranks, fuse=FACT)
+    assert max_dev(psi, g["state"]) <= TOL
+
+
+def test_factored_config1_n20_golden():
+    g = golden("golden_cfg1_n20.npz")
+    circ = Circuit(20, tuple(decode(g["gates"])))
+    ctx = runtime.make_context(None, 20, fuse=FACT)
+    runtime.run_circuit(ctx, circ)
+    psi = ctx.state.download()
+    assert max_dev(psi[g["sample_idx"]], g["sample"]) <= TOL
+    probs = [runtime.measure_probability(ctx, q) for q in range(20)]
+    np.testing.assert_allclose(probs, g["probs"], rtol=RTOL_OBS, atol=0)
+
+
+def test_factored_qaoa_pool_matches_reference():
+    """Config 5 through the pool: per-state RX tables stay exact, the shared
+    Hadamard layer is factored, the cut phases commute with its diagonals."""
+    g = golden("golden_cfg5.npz")
+    graph = make_graph(20, g["edges"])
+    depth = 4
+    circ = build_qaoa_circuit(graph, depth)
+    params = g["params"]
+    S = len(params)
+    tables = {}
+    for s in range(S):
+        for name, v in qaoa_bindings(depth, params[s]).items():
+            tables.setdefault(name, np.empty(S))[s] = v
+    ctx = runtime.make_context(None, 20, num_states=S, fuse=FACT)
+    runtime.run_circuit_pool(ctx, circ, tables)
+    values = runtime.measure_maxcut(ctx, graph)
+    np.testing.assert_allclose(values, g["values"], rtol=RTOL_OBS, atol=0)
+
+
+@pytest.mark.slow
+def test_factored_n26_sweep_vs_exact_and_n28_roundtrip():
+    # n=26: the whole config-2 sweep (every qubit, 3 fused passes) against the
+    # exact fused path, full state
+    n = 26
+    rng = np.random.default_rng(9)
+    us = [ogates.random_unitary_2x2(rng) for _ in range(n)]
+    out = {}
+    for fuse in (True, FACT):
+        st = N.DeviceState(n, n)
+        N.call("qs_init_gaussian", st.handle, 11)
+        norm = st.observable(N.QS_OBS_NORM)[0]
+        N.call("qs_scale", st.handle, 1.0 / np.sqrt(norm))
+        q = runtime.GateQueue(st, fuse=fuse)
+        for _ in range(2):
+            for k in range(n):
+                q.one_qubit(k, us[k])
+        q.flush()
+        out[fuse] = st.download()
+        del st
+    assert max_dev(out[True], out[FACT]) <= TOL
+    del out
+    # n=28: forward sweep then the adjoint sweep backward returns the start
+    n = 28
+    st = N.DeviceState(n, n)
+    N.call("qs_init_gaussian", st.handle, 12)
+    norm = st.observable(N.QS_OBS_NORM)[0]
+    N.call("qs_scale", st.handle, 1.0 / np.sqrt(norm))
+    start = st.download()
+    us = [ogates.random_unitary_2x2(rng) for _ in range(n)]
+    q = runtime.GateQueue(st, fuse=FACT)
+    for k in range(n):
+        q.one_qubit(k, us[k])
+    q.flush()
+    mid = st.observable(N.QS_OBS_NORM)[0]
+    for k in reversed(range(n)):
+        q.one_qubit(k, us[k].conj().T)
+    q.flush()
+    back = st.download()
+    assert abs(mid - 1.0) < 1e-10
+    assert max_dev(back, start) <= TOL
