@@ -354,6 +354,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
             if (p < 3) low_free = false;
         P.direct_store = (low_free && P.low_run >= 3 && kLowBits >= 3) ? 1 : 0;
     }
+    int ndiag = 0;
     for (int i = 0; i < count; ++i) {
         const qs_gate& g = prog[first + i];
         TileGate& d = P.gates[i];
@@ -367,6 +368,21 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         if (g.kind == QS_KIND_CUTPHASE) continue;
         if (g.kind == kKindDiagN) {
             d.cval = g.reserved;  // byte-table count
+            // register part of the diagonal for this round: R[k] = prod_j z_{q_j}^{k_j}
+            const int slot = ndiag++;
+            if (slot >= kMaxPassDiags) return fail(QS_ERR_VALUE, "planner: too many diagonals");
+            d.pad[0] = slot;
+            const double* z = mats_host + g.offset + 512 * uint64_t(g.reserved);
+            const std::vector<int>& rp = all_pos[gate_round[i]];
+            double2* R = P.diag_r[slot];
+            R[0] = make_double2(1.0, 0.0);
+            for (int k = 1; k < (1 << kRegLog2); ++k) {
+                const int h = 31 - __builtin_clz(k);
+                const int q = P.tile_bits[rp[h]];
+                const double2 x = R[k ^ (1 << h)];
+                const double zr = z[2 * q], zi = z[2 * q + 1];
+                R[k] = make_double2(x.x * zr - x.y * zi, x.x * zi + x.y * zr);
+            }
             continue;
         }
         if (g.stride == 0) memcpy(&d.u[0], mats_host + g.offset, 8 * sizeof(double));
@@ -440,8 +456,11 @@ std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool f
             if (kind_has_target(gates[i].kind)) need |= uint64_t(1) << gates[i].target;
             uint64_t round_set = kind_has_target(gates[i].kind) ? (uint64_t(1) << gates[i].target) : 0;
             int rounds = 1;
+            int diags = gates[i].kind == kKindDiagN;
             while (j < count && j - i < kMaxPassGates) {
                 const qs_gate& g = gates[j];
+                if (g.kind == kKindDiagN && diags >= kMaxPassDiags) break;
+                diags += g.kind == kKindDiagN;
                 uint64_t nn = need, rs = round_set;
                 int nr = rounds;
                 if (kind_has_target(g.kind)) {

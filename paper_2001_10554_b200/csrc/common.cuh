@@ -82,6 +82,7 @@ constexpr int kLaneLoBits = 4;
 constexpr int kLaneHiBits = kTileLog2 - kRegLog2 - kLaneLoBits;
 constexpr int kMaxRounds = 24;
 constexpr int kMaxPassGates = 64;
+constexpr int kMaxPassDiags = 4;
 
 // swizzle of a tile element index into its shared-memory slot; linear over
 // GF(2), so swz(a ^ b) == swz(a) ^ swz(b)
@@ -125,6 +126,9 @@ struct alignas(16) TilePass {
     uint64_t nbr[64];          // cut-phase graph: neighbour mask of each vertex (qubit)
     Round rounds[kMaxRounds];
     TileGate gates[kMaxPassGates];
+    // product diagonals (kKindDiagN, slot in TileGate.pad[0]): the factor of
+    // register index k in the gate's round, prod_j z_{qubit of register j}^{k_j}
+    double2 diag_r[kMaxPassDiags][1 << kRegLog2];
 };
 
 // ---- factored programs (fuse == QS_FUSE_FACTORED, factor.cu) ---------------

@@ -310,24 +310,18 @@ __device__ __forceinline__ void reg_shear_seq_full(double2 (&a)[kRegAmps], const
     if (kRegLog2 > 4) reg_shear<(kRegLog2 > 4 ? 4 : 0)>(a, G[4]);
 }
 
-// Product diagonal D(i) = prod_c T_c[byte c of i] (kKindDiagN).  The k = 0
-// register amplitude's factor comes from the byte tables and multiplies all 16
-// amplitudes; then each register qubit's z multiplies the half with its bit
-// set.  (16 + 32 complex products instead of the 31 of a factor table, but
-// only a few live registers next to the 16 amplitudes.)
+// Product diagonal D(i) = prod_c T_c[byte c of i] (kKindDiagN).  The factor of
+// the thread's k = 0 amplitude comes from the byte tables (its register bits
+// are 0); register index k adds R[k] = prod_j z_{q_j}^{k_j}, precomputed by the
+// host for the round (the same for every thread and tile).  Two complex
+// products per amplitude.
 __device__ __forceinline__ void reg_diag_n(double2 (&a)[kRegAmps], const double2* T, int ntab,
-                                           uint64_t il, const double2* zq, const int (&rq)[kRegLog2]) {
+                                           uint64_t il, const double2* R) {
     double2 f = __ldg(T + (il & 255));
     for (int c = 1; c < ntab; ++c) f = cmul(f, __ldg(T + (c << 8) + ((il >> (8 * c)) & 255)));
+    a[0] = cmul(a[0], f);
 #pragma unroll
-    for (int k = 0; k < kRegAmps; ++k) a[k] = cmul(a[k], f);
-#pragma unroll
-    for (int j = 0; j < kRegLog2; ++j) {
-        const double2 z = __ldg(zq + rq[j]);
-#pragma unroll
-        for (int k = 0; k < kRegAmps; ++k)
-            if ((k >> j) & 1) a[k] = cmul(a[k], z);
-    }
+    for (int k = 1; k < kRegAmps; ++k) a[k] = cmul(a[k], cmul(f, R[k]));
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -612,12 +606,9 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                     if (FACT && G.kind >= kKindShear) {
                         if (G.kind == kKindDiagN) {
                             const double2* T = reinterpret_cast<const double2*>(mats + G.offset);
-                            int rq[kRegLog2];
-#pragma unroll
-                            for (int j = 0; j < kRegLog2; ++j) rq[j] = P.tile_bits[__ffs(R.dk[1 << j]) - 1];
                             reg_diag_n(a, T, G.cval,
                                        base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask),
-                                       T + (G.cval << 8), rq);
+                                       P.diag_r[G.pad[0]]);
                         } else if (G.seq == kRegLog2) {
                             reg_shear_seq_full(a, &G);
                             g += kRegLog2 - 1;
@@ -734,7 +725,6 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
 struct FactRound {
     double t[kRegLog2];      // 0 for register bits without a shear (exact identity)
     double2 pre[kRegLog2];   // (1, 0) without a pre-diagonal
-    int32_t rq[kRegLog2];    // qubit held by register bit j (product diagonals)
     int32_t n, pre_mask, pad0, pad1;
 };
 struct alignas(16) FactPass {
@@ -743,6 +733,7 @@ struct alignas(16) FactPass {
     int32_t ntab, has_din, has_dout, pad;
     uint64_t tiles_per_state, num_tiles;
     uint64_t din_off, dout_off;  // DiagN tables in mats (doubles)
+    double2 din_r[1 << kRegLog2], dout_r[1 << kRegLog2];  // register parts (TilePass::diag_r)
     Round rounds[kMaxRounds];
     FactRound fr[kMaxRounds];
 };
@@ -779,7 +770,7 @@ __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass
                                           const uint64_t (&okb)[kRegLog2]) {
     if (DIN) {
         const double2* T = reinterpret_cast<const double2*>(mats + P.din_off);
-        reg_diag_n(a, T, P.ntab, il, T + (P.ntab << 8), F.rq);
+        reg_diag_n(a, T, P.ntab, il, P.din_r);
     }
     fact_shear<0, PRE>(a, F);
     fact_shear<1, PRE>(a, F);
@@ -788,7 +779,7 @@ __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass
     if (kRegLog2 > 4) fact_shear<(kRegLog2 > 4 ? 4 : 0), PRE>(a, F);
     if (DOUT) {
         const double2* T = reinterpret_cast<const double2*>(mats + P.dout_off);
-        reg_diag_n(a, T, P.ntab, il, T + (P.ntab << 8), F.rq);
+        reg_diag_n(a, T, P.ntab, il, P.dout_r);
     }
     if (GSTORE) {
 #pragma unroll
@@ -797,7 +788,11 @@ __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass
 #pragma unroll
             for (int j = 0; j < kRegLog2; ++j)
                 if ((k >> j) & 1) o += okb[j];
+#if defined(QSB_NO_GMEM) || defined(QSB_NO_STORES)  // diagnostics: the store goes to the tile
+            tile[(uint64_t(sb) + o) & (kTileAmps - 1)] = a[k];
+#else
             gb[o] = a[k];
+#endif
         }
     } else {
         int sbs = sb;
@@ -898,7 +893,11 @@ __global__ void __launch_bounds__(kTileThreads, QSB_TILE_MINB)
     const uint64_t goff_tid = goff(tid);
     const int swz_tid = swz(tid);
     auto prefetch = [&](uint64_t t) {
+#if !defined(QSB_NO_GMEM) && !defined(QSB_NO_LOADS)
         if (t < P.num_tiles) {
+#else
+        if (false) {
+#endif
             const double2* g = psi + (((t >> tps_log2) << m) | tile_base(t)) + goff_tid;
 #pragma unroll
             for (int i = 0; i < kLoadsPerThread; ++i)
@@ -962,209 +961,6 @@ __global__ void __launch_bounds__(kTileThreads, QSB_TILE_MINB)
     }
 }
 
-// ---- the same pass with a 3-buffer ring ---------------------------------------
-// One CTA per SM, two groups of 256 threads, three 64 KiB tile buffers.  Tile
-// sequence i of the CTA lives in buffer i % 3 and is processed by group i % 2;
-// when a group has read tile i's buffer into registers (its last round) it
-// refills that buffer with tile i + 3 -- which the OTHER group will process --
-// so a load has about one tile-processing time of lead instead of the last
-// round's.  cp.async completion is signalled on a per-buffer mbarrier
-// (cp.async.mbarrier.arrive.noinc, 256 arrivals per fill), so the consuming
-// group waits on the barrier's phase, not on its own cp.async groups.
-constexpr int kRingBufs = 3;
-constexpr int kRingGroups = 2;
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(a),
-        "r"(parity)
-        : "memory");
-}
-
-__global__ void __launch_bounds__(kRingGroups * kTileThreads, 1)
-    k_fact_ring(double2* __restrict__ psi, const __grid_constant__ FactPass P,
-                const double* __restrict__ mats) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* tiles = reinterpret_cast<double2*>(smem_raw);
-    uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double2) * kTileAmps * kRingBufs);
-    uint64_t* dep = rowoff + (kTileAmps >> kLowBits);
-    uint32_t* rlo = reinterpret_cast<uint32_t*>(dep + 256 * kDepTables);
-    uint32_t* rhi = rlo + kMaxRounds * (1 << kLaneLoBits);
-    uint64_t* full = reinterpret_cast<uint64_t*>(rhi + kMaxRounds * (1 << kLaneHiBits));
-    constexpr int kThreads = kRingGroups * kTileThreads;
-    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneLoBits); i += kThreads) {
-        const Round& R = P.rounds[i >> kLaneLoBits];
-        const int v = i & ((1 << kLaneLoBits) - 1);
-        rlo[i] = uint32_t(R.dlo[v]) | (uint32_t(R.slo[v]) << 16);
-    }
-    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneHiBits); i += kThreads) {
-        const Round& R = P.rounds[i >> kLaneHiBits];
-        const int v = i & ((1 << kLaneHiBits) - 1);
-        rhi[i] = uint32_t(R.dhi[v]) | (uint32_t(R.shi[v]) << 16);
-    }
-    const int low_run = P.low_run;
-    const int nrows = kTileAmps >> low_run;
-    const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
-    for (int r = threadIdx.x; r < nrows; r += kThreads) {
-        uint64_t off = 0;
-        for (int k = 0; k < kTileLog2 - low_run; ++k)
-            if ((r >> k) & 1) off |= uint64_t(1) << P.tile_bits[low_run + k];
-        rowoff[r] = off;
-    }
-    for (int i = threadIdx.x; i < kDepTables * 256; i += kThreads) {
-        const int c = i >> 8, v = i & 255;
-        uint64_t out = 0;
-        for (int b = 0; b < 8; ++b) {
-            if (!((v >> b) & 1)) continue;
-            int want = 8 * c + b, cnt = 0;
-            for (int q = 0, k = 0; q < P.m; ++q) {
-                if (k < kTileLog2 && P.tile_bits[k] == q) {
-                    ++k;
-                    continue;
-                }
-                if (cnt++ == want) {
-                    out |= uint64_t(1) << q;
-                    break;
-                }
-            }
-        }
-        dep[i] = out;
-    }
-    if (threadIdx.x < kRingBufs) mbar_init(full + threadIdx.x, kTileThreads);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    __syncthreads();
-
-    const int group = threadIdx.x / kTileThreads;
-    const int tid = threadIdx.x % kTileThreads;
-    const int gbar = 1 + group;
-    const int m = P.m;
-    const int tps_log2 = m - kTileLog2;
-    const uint64_t grid = gridDim.x;
-    auto tile_of = [&](uint64_t i) { return uint64_t(blockIdx.x) + i * grid; };
-    auto tile_base = [&](uint64_t t) {
-        const uint64_t x = t & (P.tiles_per_state - 1);
-        uint64_t out = 0;
-#pragma unroll
-        for (int c = 0; c < kDepTables; ++c) out |= dep[(c << 8) | ((x >> (8 * c)) & 255)];
-        return out;
-    };
-    auto goff = [&](int e) { return rowoff[e >> low_run] + (uint64_t(e) & lowmask); };
-    const uint64_t goff_tid = goff(tid);
-    const int swz_tid = swz(tid);
-    // the issuing group's 256 threads each arrive once on the buffer's barrier
-    auto fill = [&](uint64_t i) {
-        const uint64_t t = tile_of(i);
-        if (t >= P.num_tiles) return;
-        double2* buf = tiles + int(i % kRingBufs) * kTileAmps;
-        const double2* g = psi + (((t >> tps_log2) << m) | tile_base(t)) + goff_tid;
-#pragma unroll
-        for (int k = 0; k < kLoadsPerThread; ++k)
-            cp_async16(buf + (swz_tid ^ swz(k * kTileThreads)), g + goff(k * kTileThreads));
-        cp_async_arrive_noinc(full + int(i % kRingBufs));
-    };
-    if (group == 0) {
-        fill(0);
-        fill(2);
-    } else {
-        fill(1);
-    }
-    const bool direct = P.direct_store != 0;
-
-    for (uint64_t i = group; tile_of(i) < P.num_tiles; i += kRingGroups) {
-        const uint64_t tile_id = tile_of(i);
-        const uint64_t base_local = tile_base(tile_id);
-        double2* gbase = psi + (((tile_id >> tps_log2) << m) | base_local);
-        double2* tile = tiles + int(i % kRingBufs) * kTileAmps;
-        mbar_wait(full + int(i % kRingBufs), unsigned((i / kRingBufs) & 1));
-        for (int r = 0; r < P.num_rounds; ++r) {
-            const Round& R = P.rounds[r];
-            const bool last = r == P.num_rounds - 1;
-            const uint32_t lo = rlo[(r << kLaneLoBits) | (tid & ((1 << kLaneLoBits) - 1))];
-            const uint32_t hi = rhi[(r << kLaneHiBits) | (tid >> kLaneLoBits)];
-            const int eb = int((lo | hi) & 0xffff);
-            const int sb = int((lo ^ hi) >> 16);
-            int skb[kRegLog2];
-#pragma unroll
-            for (int j = 0; j < kRegLog2; ++j) skb[j] = R.sk[1 << j];
-            auto sk_of = [&](int k) {
-                int v = 0;
-#pragma unroll
-                for (int j = 0; j < kRegLog2; ++j)
-                    if ((k >> j) & 1) v ^= skb[j];
-                return v;
-            };
-            double2 a[kRegAmps];
-#pragma unroll
-            for (int k = 0; k < kRegAmps; ++k) a[k] = tile[sb ^ sk_of(k)];
-            if (last && direct) {
-                named_sync(gbar, kTileThreads);
-                fill(i + kRingBufs);
-            }
-            const FactRound& F = P.fr[r];
-            const bool gstore = last && direct;
-            const int sel = int(r == 0 && P.has_din) | (F.pre_mask ? 2 : 0) |
-                            int(last && P.has_dout) << 2 | int(gstore) << 3;
-            const uint64_t il = base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask);
-            uint64_t okb[kRegLog2];
-#pragma unroll
-            for (int j = 0; j < kRegLog2; ++j) okb[j] = gstore ? goff(R.dk[1 << j]) : 0;
-            double2* gb = gbase + (gstore ? goff(eb) : 0);
-            QSB_FACT_DISPATCH(sel, a, P, F, mats, il, tile, sb, skb, gb, okb)
-            if (gstore) break;
-            named_sync(gbar, kTileThreads);
-        }
-        if (!direct) {
-            double2* gb = gbase + goff_tid;
-#pragma unroll
-            for (int k = 0; k < kLoadsPerThread; ++k)
-                gb[goff(k * kTileThreads)] = tile[swz_tid ^ swz(k * kTileThreads)];
-            named_sync(gbar, kTileThreads);
-            fill(i + kRingBufs);
-        }
-    }
-}
-
-size_t fact_ring_smem_bytes() {
-    return sizeof(double2) * kTileAmps * kRingBufs + sizeof(uint64_t) * (kTileAmps >> kLowBits) +
-           sizeof(uint64_t) * 256 * kDepTables +
-           sizeof(uint32_t) * kMaxRounds * ((1 << kLaneLoBits) + (1 << kLaneHiBits)) +
-           sizeof(uint64_t) * kRingBufs;
-}
-
-void launch_fact_ring(double2* psi, const FactPass& F, const double* mats, cudaStream_t s) {
-    constexpr int kMaxDevices = 64;
-    static std::atomic<int> configured[kMaxDevices];
-    static int sms_of[kMaxDevices];
-    const size_t smem = fact_ring_smem_bytes();
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= kMaxDevices) dev = 0;
-    if (configured[dev].load(std::memory_order_acquire) == 0) {
-        cudaFuncSetAttribute(k_fact_ring, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        sms_of[dev] = sms;
-        configured[dev].store(1, std::memory_order_release);
-    }
-    uint64_t grid = uint64_t(sms_of[dev]);
-    if (grid > F.num_tiles) grid = F.num_tiles;
-    k_fact_ring<<<unsigned(grid), kRingGroups * kTileThreads, smem, s>>>(psi, F, mats);
-}
-
 // The lean kernel applies when every gate of the pass is a shear in in-order
 // register runs, with product diagonals only first in round 0 / last in the
 // last round.
@@ -1184,7 +980,6 @@ bool fact_pass_from(const TilePass& T, FactPass* F) {
         for (int j = 0; j < kRegLog2; ++j) {
             FR.t[j] = 0.0;
             FR.pre[j] = make_double2(1.0, 0.0);
-            FR.rq[j] = T.tile_bits[__builtin_ctz(R.dk[1 << j])];
         }
         for (int g = R.first_gate; g < R.first_gate + R.num_gates; ++g) {
             const TileGate& G = T.gates[g];
@@ -1192,9 +987,11 @@ bool fact_pass_from(const TilePass& T, FactPass* F) {
                 if (r == 0 && g == 0 && !F->has_din) {
                     F->has_din = 1;
                     F->din_off = G.offset;
+                    memcpy(F->din_r, T.diag_r[G.pad[0]], sizeof(F->din_r));
                 } else if (r == T.num_rounds - 1 && g == R.first_gate + R.num_gates - 1) {
                     F->has_dout = 1;
                     F->dout_off = G.offset;
+                    memcpy(F->dout_r, T.diag_r[G.pad[0]], sizeof(F->dout_r));
                 } else {
                     return false;
                 }
@@ -1395,10 +1192,8 @@ bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_d
     static const bool lean_ok = getenv("QSB_NO_LEAN") == nullptr;
     if (fact && !phase && !generic && !tables && kGroups == 1 && lean_ok) {
         static thread_local FactPass F;
-        static const bool ring = getenv("QSB_FACT_RING") != nullptr;  // measured slower
         if (fact_pass_from(pass, &F)) {
-            if (ring) launch_fact_ring(psi, F, mats, s);
-            else launch_fact(psi, F, mats, s);
+            launch_fact(psi, F, mats, s);
             return true;
         }
     }

@@ -35,6 +35,8 @@ VARIANTS = {
     "noloads": ["-DQSB_NO_LOADS"],
     "nostores": ["-DQSB_NO_STORES"],
     "nogmem_nosmem": ["-DQSB_NO_GMEM", "-DQSB_NO_SMEM_ROUND"],
+    "r5": ["-DQSB_REG_LOG2=5"],
+    "r5nogmem": ["-DQSB_REG_LOG2=5", "-DQSB_NO_GMEM"],
 }
 
 
