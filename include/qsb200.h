@@ -154,7 +154,7 @@ int qs_last_program_passes(const qs_state* st, int32_t* passes);
  * u = k * diag(1, za) * R * diag(1, zb), R = [[c,-s],[s,c]] = scale *
  * [[1,-t],[t,1]] (scale = c, t = s/c).  out[10] = k.re k.im za.re za.im zb.re
  * zb.im 0 t scale 0.  Returns QS_ERR_VALUE when u is not unitary to 1e-12,
- * exactly diagonal or has c < 1e-3 (those stay unfactored). */
+ * exactly diagonal or has c < 1e-9 (those stay unfactored). */
 int qs_decompose_2x2(const double* u, double* out);
 
 /* ---- observables: per-state partial sums in the reference's tree order

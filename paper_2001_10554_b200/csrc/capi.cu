@@ -386,6 +386,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
             continue;
         }
         if (g.stride == 0) memcpy(&d.u[0], mats_host + g.offset, 8 * sizeof(double));
+        if (g.kind == kKindScalar) continue;
         const std::vector<int>& rp = all_pos[gate_round[i]];
         int p = pos_of(g.target), j = 0;
         for (int jj = 0; jj < kRegLog2; ++jj)
@@ -779,6 +780,10 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
         factor_program(gates, count, mats, mats_len, st->m, st->num_states, &fp);
         all.assign(mats, mats + mats_len);
         all.insert(all.end(), fp.extra.begin(), fp.extra.end());
+        uint64_t support = 0;
+        for (int e = 0; e < 2 * num_edges; ++e) support |= uint64_t(1) << edges[e];
+        static const bool reorder = getenv("QSB_NO_REORDER") == nullptr;
+        if (reorder) schedule_program(fp.gates, st->m, support, all.data(), st->num_states);
         gates = fp.gates.data();
         count = int(fp.gates.size());
         mats = all.data();

@@ -145,7 +145,10 @@ constexpr int kKindDiag1 = 17;  // params [0, 0, 0, 0, z.re, z.im, 0, 0]: amplit
                                 // `target` set *= z
 constexpr int kKindDiagN = 18;  // psi_i *= prod_c T_c[byte c of i]; `reserved` = table count;
                                 // offset -> ntab*256 complex byte tables, then 64 complex z_q
-inline bool kind_has_target(int kind) { return kind != QS_KIND_CUTPHASE && kind != kKindDiagN; }
+constexpr int kKindScalar = 19; // per-state scalar (stride 8): psi_s *= (params[0], params[1])
+inline bool kind_has_target(int kind) {
+    return kind != QS_KIND_CUTPHASE && kind != kKindDiagN && kind != kKindScalar;
+}
 
 struct FactoredProgram {
     std::vector<qs_gate> gates;
@@ -156,8 +159,12 @@ struct FactoredProgram {
 // size of the caller's table (the extra entries are appended after it).
 void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
                     int num_states, FactoredProgram* out);
+// Commutation-aware re-order of a factored program for the pass planner
+// (phase_support: the cut-phase graph's vertices).
+void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support,
+                      const double* mats, int num_states);
 // U = k diag(1,za) R diag(1,zb): out = [k, za, zb] (complex), 0, t, scale (= c).
-// Returns false when U is not unitary to 1e-12, exactly diagonal or c < 1e-3.
+// Returns false when U is not unitary to 1e-12, exactly diagonal or c < 1e-9.
 bool decompose_2x2(const double* u, double out[10]);
 
 // ---- launchers (gate_kernels.cu / reduce_kernels.cu / exchange.cu) ---------

@@ -8,7 +8,7 @@
 // amplitude for a general complex 2x2 (statevector.py:144-150).  A large t
 // costs no accuracy (fma(-t, y, x) rounds once, relative to |x - t y|, and the
 // scale c brings the result back), only growth: the amplitudes grow by at most
-// 1/c per shear until the scalar is applied, so gates with c < 1e-3 stay exact
+// 1/c per shear until the scalar is applied, so gates with c < 1e-9 stay exact
 // and a scalar pass is inserted when the pending scale passes 2^-600.  The
 // rest is bookkeeping that costs nothing per amplitude:
 //  * scalars commute with everything: k and the shear scale multiply into one
@@ -26,6 +26,7 @@
 // D_out.  Controlled gates, per-state matrix tables, non-unitary matrices and
 // cut phases stay exact.  Errors are a few ulps per gate (the tests bound them
 // by the north_star 1e-12 on amplitudes).
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -85,7 +86,7 @@ bool decompose_2x2(const double* m, double out[10]) {
         k = unit(u[2]) / za;  // u10 = k za s
         if (a00 > 0 && std::real(std::conj(k) * u[0]) < 0) za = -za, zb = -zb, k = -k;  // u00 = +k c
     }
-    if (c < 1e-3) return false;  // nearly anti-diagonal: t would exceed 1000
+    if (c < 1e-9) return false;  // nearly anti-diagonal: t would exceed 1e9
     form = 0;
     t = s / c;
     scale = c;
@@ -171,6 +172,74 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         return true;
     };
 
+    // per-state scalars (pool mode): k * scale of the per-state shears
+    std::vector<cd> Ks(num_states, cd(1.0));
+    bool per_state_k = false;
+    auto per_state_scalars = [&]() {
+        while (out->extra.size() % 2) out->extra.push_back(0.0);
+        const uint64_t off = mats_len + out->extra.size();
+        for (int s = 0; s < num_states; ++s) {
+            const double p[8] = {Ks[s].real(), Ks[s].imag(), 0, 0, 0, 0, 0, 0};
+            out->extra.insert(out->extra.end(), p, p + 8);
+            Ks[s] = 1.0;
+        }
+        qs_gate g;
+        memset(&g, 0, sizeof(g));
+        g.kind = kKindScalar;
+        g.target = -1;
+        g.control = -1;
+        g.offset = off;
+        g.stride = 8;
+        out->gates.push_back(g);
+    };
+    std::vector<double> fs;
+    auto per_state_shear = [&](const qs_gate& g) {
+        const int q = g.target;
+        fs.resize(size_t(num_states) * 10);
+        for (int st = 0; st < num_states; ++st) {
+            double* f = fs.data() + 10 * st;
+            if (!decompose_2x2(mats + g.offset + uint64_t(st) * g.stride, f)) return false;
+            // the same diagonals for every state; (za, zb) and (-za, -zb) are
+            // the same factorisation with the sign of t flipped
+            const cd za0(fs[2], fs[3]), zb0(fs[4], fs[5]), za1(f[2], f[3]), zb1(f[4], f[5]);
+            if (std::abs(za1 - za0) <= 1e-13 && std::abs(zb1 - zb0) <= 1e-13) continue;
+            if (std::abs(za1 + za0) <= 1e-13 && std::abs(zb1 + zb0) <= 1e-13) {
+                f[7] = -f[7];
+                continue;
+            }
+            return false;
+        }
+        const cd za(fs[2], fs[3]), zb(fs[4], fs[5]);
+        const cd pre = pending[q] * zb;
+        bool has_pre = false;
+        if (!mixed[q]) din[q] *= pre;
+        else has_pre = pre != 1.0;
+        while (out->extra.size() % 2) out->extra.push_back(0.0);
+        const uint64_t off = mats_len + out->extra.size();
+        double small = 1.0;
+        for (int st = 0; st < num_states; ++st) {
+            const double* f = fs.data() + 10 * st;
+            const double p[8] = {f[7], 0, has_pre ? 1.0 : 0.0, 0, pre.real(), pre.imag(), 0, 0};
+            out->extra.insert(out->extra.end(), p, p + 8);
+            Ks[st] *= cd(f[0], f[1]) * f[8];
+            small = std::min(small, std::abs(Ks[st]));
+        }
+        qs_gate s8;
+        memset(&s8, 0, sizeof(s8));
+        s8.kind = kKindShear;
+        s8.target = q;
+        s8.control = -1;
+        s8.offset = off;
+        s8.stride = 8;
+        out->gates.push_back(s8);
+        out->factored++;
+        per_state_k = true;
+        pending[q] = za;
+        mixed[q] = 1;
+        if (small < 0x1p-600) per_state_scalars();
+        return true;
+    };
+
     for (int i = 0; i < count; ++i) {
         const qs_gate& g = gates[i];
         if (g.kind == QS_KIND_CUTPHASE) {  // diagonal: commutes with every pending diagonal
@@ -188,11 +257,15 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         }
         // QS_KIND_1Q
         if (g.stride != 0) {
-            if (!diagonal_for_all_states(g)) {
+            // per-state matrices (pool mode): a per-state shear when every
+            // state's matrix factors with the same diagonals (e.g. the QAOA
+            // mixer RX(2 beta_s): za = -i, zb = i for every beta), the scales
+            // and k going to per-state scalars
+            if (!diagonal_for_all_states(g) && !per_state_shear(g)) {
                 flush(q);
                 mixed[q] = 1;
+                out->gates.push_back(g);
             }
-            out->gates.push_back(g);
             continue;
         }
         const double* u = mats + g.offset;
@@ -221,8 +294,8 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         out->factored++;
         pending[q] = za;
         mixed[q] = 1;
-        // the amplitudes grow by at most sqrt(2) per shear; a scalar pass keeps
-        // them far from overflow in very long programs
+        // the amplitudes grow by 1/c per shear; a scalar pass keeps them far
+        // from overflow in long programs
         if (std::abs(K) < 0x1p-600) {
             out->gates.push_back(diag_tables(std::vector<cd>(m, cd(1.0)), K));
             K = 1.0;
@@ -234,6 +307,109 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
     bool any_out = K != 1.0;
     for (int q = 0; q < m; ++q) any_out |= pending[q] != 1.0;
     if (any_out) out->gates.push_back(diag_tables(pending, K));
+    if (per_state_k) per_state_scalars();
+}
+
+// ---- commutation-aware order (factored programs only) -----------------------
+// Gates that commute may run in either order; in the factored mode (results to
+// the 1e-12 tolerance, not bit-identical) the program is re-ordered so that the
+// greedy pass planner packs more gates into each tile pass.  Two gates commute
+// unless one MIXES a qubit (target of a non-diagonal matrix) that the other
+// touches at all; diagonal actions (controls, diagonal matrices, cut phases,
+// product diagonals) commute with each other.  The list schedule keeps every
+// dependency and fills a pass first with ready gates that need no new tile bit,
+// then with ready gates in program order while the tile has room.  A QAOA layer
+// pair [RX(0..11), cut, RX(0..11)] then shares one pass: the config-5 pool
+// circuit needs 6 passes instead of 10.
+void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support,
+                      const double* mats, int num_states) {
+    const int n = int(gates.size());
+    if (n < 3) return;
+    const uint64_t all = m >= 64 ? ~uint64_t(0) : (uint64_t(1) << m) - 1;
+    std::vector<uint64_t> mix(n, 0), dia(n, 0);
+    auto diagonal = [&](const qs_gate& g) {
+        for (int st = 0; st < num_states; ++st) {
+            const double* u = mats + g.offset + uint64_t(st) * g.stride;
+            if (u[2] != 0 || u[3] != 0 || u[4] != 0 || u[5] != 0) return false;
+            if (g.stride == 0) break;
+        }
+        return true;
+    };
+    for (int i = 0; i < n; ++i) {
+        const qs_gate& g = gates[i];
+        const uint64_t t = g.target >= 0 ? uint64_t(1) << g.target : 0;
+        switch (g.kind) {
+            case QS_KIND_CUTPHASE: dia[i] = phase_support; break;
+            case kKindDiagN: dia[i] = all; break;
+            case kKindScalar: break;
+            case kKindDiag1: dia[i] = t; break;
+            case kKindShear: mix[i] = t; break;
+            case QS_KIND_CTRL:
+                dia[i] = uint64_t(1) << g.control;
+                (diagonal(g) ? dia[i] : mix[i]) |= t;
+                break;
+            default: (diagonal(g) ? dia[i] : mix[i]) |= t; break;
+        }
+    }
+    std::vector<std::vector<int>> succ(n);
+    std::vector<int> npred(n, 0);
+    for (int j = 0; j < n; ++j)
+        for (int i = 0; i < j; ++i)
+            if ((mix[i] & (mix[j] | dia[j])) || (dia[i] & mix[j])) {
+                succ[i].push_back(j);
+                ++npred[j];
+            }
+    std::vector<int> ready;  // kept sorted by program index
+    for (int i = 0; i < n; ++i)
+        if (npred[i] == 0) ready.push_back(i);
+    std::vector<qs_gate> out;
+    out.reserve(n);
+    const uint64_t low = m >= kTileLog2 ? kLowMask : 0;
+    while (!ready.empty()) {
+        uint64_t need = low, round_set = 0;
+        int rounds = 1, count = 0, diags = 0;
+        for (;;) {
+            int pick = -1;
+            uint64_t pick_need = 0, pick_rs = 0;
+            int pick_nr = 0;
+            for (int pass = 0; pass < 2 && pick < 0; ++pass) {
+                for (size_t k = 0; k < ready.size(); ++k) {
+                    const qs_gate& g = gates[ready[k]];
+                    uint64_t nn = need, rs = round_set;
+                    int nr = rounds;
+                    if (kind_has_target(g.kind)) {
+                        const uint64_t b = uint64_t(1) << g.target;
+                        if (pass == 0 && !(need & b)) continue;  // first: no new tile bit
+                        nn |= b;
+                        if (!(rs & b)) {
+                            if (__builtin_popcountll(rs) >= kRegLog2) {
+                                rs = 0;
+                                ++nr;
+                            }
+                            rs |= b;
+                        }
+                    }
+                    if (count > 0 && (__builtin_popcountll(nn) > kTileLog2 || nr > kMaxRounds ||
+                                      count + 1 > kMaxPassGates ||
+                                      (g.kind == kKindDiagN && diags >= kMaxPassDiags)))
+                        continue;
+                    pick = int(k);
+                    pick_need = nn, pick_rs = rs, pick_nr = nr;
+                    break;
+                }
+            }
+            if (pick < 0) break;
+            const int gi = ready[pick];
+            ready.erase(ready.begin() + pick);
+            out.push_back(gates[gi]);
+            need = pick_need, round_set = pick_rs, rounds = pick_nr;
+            ++count;
+            diags += gates[gi].kind == kKindDiagN;
+            for (int j : succ[gi])
+                if (--npred[j] == 0) ready.insert(std::lower_bound(ready.begin(), ready.end(), j), j);
+        }
+    }
+    gates.swap(out);
 }
 
 }  // namespace qsb

@@ -253,12 +253,13 @@ __device__ __forceinline__ void reg_gate_generic(double2 (&a)[kRegAmps], const d
 // ---- factored gates (QS_FUSE_FACTORED, factor.cu) ---------------------------
 // Shear on register bit J: (a, b) <- (a - t b, b + t a), 4 FMAs per pair.
 // With a pre-diagonal the b member is first multiplied by z (diag(1, z) on the
-// same qubit).
+// same qubit).  u: the gate's 4 parameter entries [t, 0], [has_pre, 0], z, -
+// (from the pass descriptor, or the state's staged table row in pool mode).
 template <int J>
-__device__ __forceinline__ void reg_shear(double2 (&a)[kRegAmps], const TileGate& G) {
-    const double t = G.u[0].x;
-    if (G.u[1].x != 0.0) {  // has_pre (params[2])
-        const double2 z = G.u[2];
+__device__ __forceinline__ void reg_shear(double2 (&a)[kRegAmps], const double2 u[4]) {
+    const double t = u[0].x;
+    if (u[1].x != 0.0) {  // has_pre
+        const double2 z = u[2];
 #pragma unroll
         for (int k = 0; k < kRegAmps; ++k)
             if ((k >> J) & 1) a[k] = cmul(a[k], z);
@@ -279,10 +280,19 @@ __device__ __forceinline__ void reg_diag1(double2 (&a)[kRegAmps], const double2 
         if ((k >> J) & 1) a[k] = cmul(a[k], z);
 }
 
-__device__ __forceinline__ void reg_fact_generic(double2 (&a)[kRegAmps], const TileGate& G) {
+template <bool TABLES>
+__device__ __forceinline__ void reg_fact_generic(double2 (&a)[kRegAmps], const TileGate& G,
+                                                 const double2* tm) {
+    double2 u[4];
+    gate_matrix<TABLES>(u, G, tm);
+    if (G.kind == kKindScalar) {
+#pragma unroll
+        for (int k = 0; k < kRegAmps; ++k) a[k] = cmul(a[k], u[0]);
+        return;
+    }
     const int j = G.variant % kRegLog2;
     if (G.kind == kKindDiag1) {
-        const double2 z = G.u[2];
+        const double2 z = u[2];
         switch (j) {
             case 0: reg_diag1<0>(a, z); break;
             case 1: reg_diag1<1>(a, z); break;
@@ -293,21 +303,33 @@ __device__ __forceinline__ void reg_fact_generic(double2 (&a)[kRegAmps], const T
         return;
     }
     switch (j) {
-        case 0: reg_shear<0>(a, G); break;
-        case 1: reg_shear<1>(a, G); break;
-        case 2: reg_shear<2>(a, G); break;
-        case 3: reg_shear<(kRegLog2 > 3 ? 3 : 0)>(a, G); break;
-        default: reg_shear<(kRegLog2 > 4 ? 4 : 0)>(a, G); break;
+        case 0: reg_shear<0>(a, u); break;
+        case 1: reg_shear<1>(a, u); break;
+        case 2: reg_shear<2>(a, u); break;
+        case 3: reg_shear<(kRegLog2 > 3 ? 3 : 0)>(a, u); break;
+        default: reg_shear<(kRegLog2 > 4 ? 4 : 0)>(a, u); break;
     }
 }
 
 // A full run of kRegLog2 shears on register bits 0..kRegLog2-1 (straight line).
-__device__ __forceinline__ void reg_shear_seq_full(double2 (&a)[kRegAmps], const TileGate* G) {
-    reg_shear<0>(a, G[0]);
-    reg_shear<1>(a, G[1]);
-    reg_shear<2>(a, G[2]);
-    if (kRegLog2 > 3) reg_shear<(kRegLog2 > 3 ? 3 : 0)>(a, G[3]);
-    if (kRegLog2 > 4) reg_shear<(kRegLog2 > 4 ? 4 : 0)>(a, G[4]);
+template <bool TABLES>
+__device__ __forceinline__ void reg_shear_seq_full(double2 (&a)[kRegAmps], const TileGate* G,
+                                                   const double2* tm) {
+    double2 u[4];
+    gate_matrix<TABLES>(u, G[0], tm);
+    reg_shear<0>(a, u);
+    gate_matrix<TABLES>(u, G[1], tm + 4);
+    reg_shear<1>(a, u);
+    gate_matrix<TABLES>(u, G[2], tm + 8);
+    reg_shear<2>(a, u);
+    if (kRegLog2 > 3) {
+        gate_matrix<TABLES>(u, G[3], tm + 12);
+        reg_shear<(kRegLog2 > 3 ? 3 : 0)>(a, u);
+    }
+    if (kRegLog2 > 4) {
+        gate_matrix<TABLES>(u, G[4], tm + 16);
+        reg_shear<(kRegLog2 > 4 ? 4 : 0)>(a, u);
+    }
 }
 
 // Product diagonal D(i) = prod_c T_c[byte c of i] (kKindDiagN).  The factor of
@@ -610,10 +632,10 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                                        base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask),
                                        P.diag_r[G.pad[0]]);
                         } else if (G.seq == kRegLog2) {
-                            reg_shear_seq_full(a, &G);
+                            reg_shear_seq_full<TABLES>(a, &G, tm_cur + 4 * g);
                             g += kRegLog2 - 1;
                         } else {
-                            reg_fact_generic(a, G);
+                            reg_fact_generic<TABLES>(a, G, tm_cur + 4 * g);
                         }
                         continue;
                     }
@@ -1178,7 +1200,9 @@ bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_d
                 phase = true;
             } else if (G.kind >= kKindShear) {
                 fact = true;
-                if (G.seq > 0) g += G.seq - 1;
+                const int run = G.seq > 0 ? G.seq : 1;
+                for (int j = 0; j < run; ++j) tables |= pass.gates[g + j].stride != 0;
+                g += run - 1;
             } else {
                 // a sequence run covers G.seq gates; any of them may use a table
                 const int run = G.seq > 0 ? G.seq : 1;

@@ -231,3 +231,45 @@ def test_factored_n26_sweep_vs_exact_and_n28_roundtrip():
     back = st.download()
     assert abs(mid - 1.0) < 1e-10
     assert max_dev(back, start) <= TOL
+
+
+def test_factored_pool_per_state_gates():
+    """Per-state matrices in pool mode: RX(theta_s) factors with the same
+    diagonals for every state (per-state shears + per-state scalars), per-state
+    Haar matrices do not (they stay exact); shared gates and cut phases mix in."""
+    from oracle import statevector as osv
+    rng = np.random.default_rng(8)
+    n, S = 13, 6
+    edges = [(0, 3), (2, 7), (5, 11), (1, 12)]
+    graph = make_graph(n, edges)
+    states = np.stack([ogates.random_state(n, rng) for _ in range(S)])
+    pool = runtime.PoolState(n, S, fuse=FACT)
+    pool.state.upload(states)
+    expected = states.copy()
+    for step in range(40):
+        q = int(rng.integers(n))
+        r = rng.random()
+        if r < 0.45:
+            us = np.stack([ogates.rx(float(x)) for x in rng.uniform(0, 2 * np.pi, S)])
+        elif r < 0.6:
+            us = np.stack([ogates.random_unitary_2x2(rng) for _ in range(S)])
+        elif r < 0.85:
+            us = np.stack([ogates.random_unitary_2x2(rng)] * S)
+        else:
+            gam = rng.uniform(0, np.pi, S)
+            pool.queue.cut_phase(graph, gam)
+            for s in range(S):
+                osv.apply_cut_phase(expected[s], edges, float(gam[s]))
+            continue
+        pool.queue.one_qubit(q, us)
+        for s in range(S):
+            osv.apply_1q(expected[s], q, us[s])
+    # nearly anti-diagonal states (t = tan(theta/2) up to ~1e8): large shears
+    for q in (0, 7, 12):
+        th = np.array([np.pi - 1e-7, 0.3, np.pi + 2e-8, 2.0, np.pi - 3e-9, 5.9])
+        us = np.stack([ogates.rx(float(x)) for x in th])
+        pool.queue.one_qubit(q, us)
+        for s in range(S):
+            osv.apply_1q(expected[s], q, us[s])
+    got = pool.amplitudes()
+    assert max_dev(got, expected) <= TOL

@@ -15,14 +15,16 @@ tables = {}
 for s in range(S):
     for k, v in qaoa_bindings(p, pos[s]).items():
         tables.setdefault(k, np.empty(S))[s] = v
-ctx = runtime.make_context(None, n, num_states=S)
+fuse = "factored" if (sys.argv[1] if len(sys.argv) > 1 else "exact") == "factored" else True
+ctx = runtime.make_context(None, n, num_states=S, fuse=fuse)
 runtime.run_circuit_pool(ctx, circ, tables)
 ctx.state.synchronize()
 ctx.state.launch_log(True)
 runtime.reset_state(ctx)
 runtime.run_circuit_pool(ctx, circ, tables)
 ms, kinds = ctx.state.read_launch_log()
-print("launches", list(zip(kinds.tolist(), np.round(ms, 3).tolist())))
+print(sys.argv[1:], "total", round(float(ms.sum()), 2), "launches",
+      list(zip(kinds.tolist(), np.round(ms, 3).tolist())))
 q = runtime.GateQueue(ctx.state)
 # plan of the same program
 gates = []
