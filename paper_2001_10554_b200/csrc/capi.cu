@@ -778,6 +778,7 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
         static thread_local FactoredProgram fp;
         static thread_local std::vector<double> all;
         factor_program(gates, count, mats, mats_len, st->m, st->num_states, &fp);
+        if (2 * fp.factored < count) goto exact;  // mostly unfactorable: the rewrite does not pay
         all.assign(mats, mats + mats_len);
         all.insert(all.end(), fp.extra.begin(), fp.extra.end());
         uint64_t support = 0;
@@ -789,6 +790,7 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
         mats = all.data();
         mats_len = all.size();
     }
+exact:
     if (int rc = grow(&st->d_mats, &st->mats_cap, mats_len ? mats_len : 1)) return rc;
     if (mats_len)
         CUDA_TRY(cudaMemcpyAsync(st->d_mats, mats, mats_len * sizeof(double),

@@ -153,7 +153,7 @@ inline bool kind_has_target(int kind) {
 struct FactoredProgram {
     std::vector<qs_gate> gates;
     std::vector<double> extra;  // parameters/tables, addressed at mats_len + local offset
-    int factored = 0;           // 1q gates turned into shears
+    int factored = 0;           // 1q gates turned into shears or absorbed as diagonals
 };
 // Rewrites gates[0..count) (validated, all local) into `out`.  mats_len is the
 // size of the caller's table (the extra entries are appended after it).

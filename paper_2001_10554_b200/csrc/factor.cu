@@ -274,6 +274,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             std::abs(std::abs(u11) - 1.0) <= 1e-12) {
             K *= u00;  // diag(u00, u11) = u00 * diag(1, u11/u00)
             pending[q] *= u11 / u00;
+            out->factored++;  // absorbed: costs nothing per amplitude
             continue;
         }
         double f[10];
@@ -372,17 +373,20 @@ void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support
             int pick = -1;
             uint64_t pick_need = 0, pick_rs = 0;
             int pick_nr = 0;
-            for (int pass = 0; pass < 2 && pick < 0; ++pass) {
+            // preference: no new register round and no new tile bit, then no
+            // new tile bit, then program order
+            for (int tier = 0; tier < 3 && pick < 0; ++tier) {
                 for (size_t k = 0; k < ready.size(); ++k) {
                     const qs_gate& g = gates[ready[k]];
                     uint64_t nn = need, rs = round_set;
                     int nr = rounds;
                     if (kind_has_target(g.kind)) {
                         const uint64_t b = uint64_t(1) << g.target;
-                        if (pass == 0 && !(need & b)) continue;  // first: no new tile bit
+                        if (tier < 2 && !(need & b)) continue;
                         nn |= b;
                         if (!(rs & b)) {
                             if (__builtin_popcountll(rs) >= kRegLog2) {
+                                if (tier == 0) continue;
                                 rs = 0;
                                 ++nr;
                             }
