@@ -229,6 +229,7 @@ bool is_diag_one(const double* e) {
 }
 
 // ---- the fusion planner ----------------------------------------------------
+thread_local uint64_t g_zero_off = 0;  // factored program being launched: a 0.0 in mats
 struct PlannedPass {
     int first, count;  // range in the program
 };
@@ -275,6 +276,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     P.tiles_per_state = uint64_t(1) << (st->m - kTileLog2);
     P.num_tiles = P.tiles_per_state * uint64_t(st->num_states);
     P.rank_offset = uint64_t(st->rank) << st->m;
+    P.zero_off = g_zero_off;
     for (int k = 0; k < ct.count; ++k)
         for (int u = 0; u < 64; ++u)
             if ((ct.mask[k] >> u) & 1) {
@@ -385,7 +387,10 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
             }
             continue;
         }
-        if (g.stride == 0) memcpy(&d.u[0], mats_host + g.offset, 8 * sizeof(double));
+        // per-state shears: the first state's row (the pre-diagonal is shared
+        // by construction; t is read per state)
+        if (g.stride == 0 || g.kind == kKindShear)
+            memcpy(&d.u[0], mats_host + g.offset, 8 * sizeof(double));
         if (g.kind == kKindScalar) continue;
         const std::vector<int>& rp = all_pos[gate_round[i]];
         int p = pos_of(g.target), j = 0;
@@ -422,6 +427,19 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         } else {
             ++i;
         }
+    }
+    static const bool debug_plan = getenv("QSB_DEBUG_PLAN") != nullptr;
+    if (debug_plan) {  // one line per pass: rounds as [gate kind:target ...]
+        fprintf(stderr, "pass tile=");
+        for (int b = 0; b < kTileLog2; ++b) fprintf(stderr, "%d%s", P.tile_bits[b], b + 1 < kTileLog2 ? "," : "");
+        for (int rr = 0; rr < P.num_rounds; ++rr) {
+            fprintf(stderr, " [");
+            for (int g = P.rounds[rr].first_gate; g < P.rounds[rr].first_gate + P.rounds[rr].num_gates; ++g)
+                fprintf(stderr, "%s%d:%d", g > P.rounds[rr].first_gate ? " " : "", P.gates[g].kind,
+                        prog[first + g].target);
+            fprintf(stderr, "]");
+        }
+        fprintf(stderr, "\n");
     }
     if (!tile_pass_in_params()) {  // QSB_PASS_SMEM builds read the pass from a device copy
         if (int rc = grow(&st->d_pass, &st->pass_cap, 1)) return rc;
@@ -777,7 +795,7 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
         // tables follow the caller's table in one upload
         static thread_local FactoredProgram fp;
         static thread_local std::vector<double> all;
-        factor_program(gates, count, mats, mats_len, st->m, st->num_states, &fp);
+        factor_program(gates, count, mats, mats_len, st->m, st->num_states, num_edges, &fp);
         if (2 * fp.factored < count) goto exact;  // mostly unfactorable: the rewrite does not pay
         all.assign(mats, mats + mats_len);
         all.insert(all.end(), fp.extra.begin(), fp.extra.end());
@@ -785,6 +803,7 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
         for (int e = 0; e < 2 * num_edges; ++e) support |= uint64_t(1) << edges[e];
         static const bool reorder = getenv("QSB_NO_REORDER") == nullptr;
         if (reorder) schedule_program(fp.gates, st->m, support, all.data(), st->num_states);
+        g_zero_off = fp.zero_off;
         gates = fp.gates.data();
         count = int(fp.gates.size());
         mats = all.data();

@@ -123,6 +123,7 @@ struct alignas(16) TilePass {
     uint64_t tiles_per_state;  // 2^(m - kTileLog2)
     uint64_t num_tiles;        // num_states * tiles_per_state
     uint64_t rank_offset;      // rank_index << m (global index of local offset 0)
+    uint64_t zero_off;         // factored programs: a 0.0 in mats (lean-pass t padding)
     uint64_t nbr[64];          // cut-phase graph: neighbour mask of each vertex (qubit)
     Round rounds[kMaxRounds];
     TileGate gates[kMaxPassGates];
@@ -154,11 +155,12 @@ struct FactoredProgram {
     std::vector<qs_gate> gates;
     std::vector<double> extra;  // parameters/tables, addressed at mats_len + local offset
     int factored = 0;           // 1q gates turned into shears or absorbed as diagonals
+    uint64_t zero_off = 0;      // a 0.0 in the extra entries (mats_len + local offset)
 };
 // Rewrites gates[0..count) (validated, all local) into `out`.  mats_len is the
 // size of the caller's table (the extra entries are appended after it).
 void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
-                    int num_states, FactoredProgram* out);
+                    int num_states, int num_edges, FactoredProgram* out);
 // Commutation-aware re-order of a factored program for the pass planner
 // (phase_support: the cut-phase graph's vertices).
 void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support,

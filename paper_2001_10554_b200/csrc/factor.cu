@@ -100,7 +100,7 @@ bool decompose_2x2(const double* m, double out[10]) {
 }
 
 void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
-                    int num_states, FactoredProgram* out) {
+                    int num_states, int num_edges, FactoredProgram* out) {
     out->gates.clear();
     out->extra.clear();
     out->factored = 0;
@@ -199,6 +199,11 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         for (int st = 0; st < num_states; ++st) {
             double* f = fs.data() + 10 * st;
             if (!decompose_2x2(mats + g.offset + uint64_t(st) * g.stride, f)) return false;
+            if (st == 0 && (f[3] < 0 || (f[3] == 0 && f[2] < 0))) {
+                // canonical sign (Im za >= 0): consecutive gates of one family
+                // (RX layers) then meet with za * zb = 1 and need no pre-diagonal
+                f[2] = -f[2], f[3] = -f[3], f[4] = -f[4], f[5] = -f[5], f[7] = -f[7];
+            }
             // the same diagonals for every state; (za, zb) and (-za, -zb) are
             // the same factorisation with the sign of t flipped
             const cd za0(fs[2], fs[3]), zb0(fs[4], fs[5]), za1(f[2], f[3]), zb1(f[4], f[5]);
@@ -308,7 +313,35 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
     bool any_out = K != 1.0;
     for (int q = 0; q < m; ++q) any_out |= pending[q] != 1.0;
     if (any_out) out->gates.push_back(diag_tables(pending, K));
-    if (per_state_k) per_state_scalars();
+    out->zero_off = mats_len + out->extra.size();
+    out->extra.push_back(0.0);
+    out->extra.push_back(0.0);
+    if (per_state_k) {
+        // the per-state scalars ride on a cut phase when the program has one
+        // (each state's LUT row times its scalar: no extra pass op)
+        int cut = -1;
+        for (int i = int(out->gates.size()) - 1; i >= 0 && cut < 0; --i)
+            if (out->gates[i].kind == QS_KIND_CUTPHASE) cut = i;
+        if (cut < 0) {
+            per_state_scalars();
+        } else {
+            qs_gate& g = out->gates[cut];
+            const uint64_t len = 2 * uint64_t(num_edges + 1);
+            const double* src = g.offset >= mats_len ? out->extra.data() + (g.offset - mats_len)
+                                                     : mats + g.offset;
+            std::vector<double> rows(len * num_states);
+            for (int st = 0; st < num_states; ++st)
+                for (uint64_t e = 0; e < len; e += 2) {
+                    const double* x = src + uint64_t(st) * g.stride + e;
+                    const cd v = cd(x[0], x[1]) * Ks[st];
+                    rows[st * len + e] = v.real(), rows[st * len + e + 1] = v.imag();
+                }
+            while (out->extra.size() % 2) out->extra.push_back(0.0);
+            g.offset = mats_len + out->extra.size();
+            g.stride = len;
+            out->extra.insert(out->extra.end(), rows.begin(), rows.end());
+        }
+    }
 }
 
 // ---- commutation-aware order (factored programs only) -----------------------

@@ -738,33 +738,41 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
 }
 
 // ---- lean fused pass for factored programs -------------------------------------
-// A pass whose gates are only shears (QS_FUSE_FACTORED) and the product
-// diagonals at its ends: each register round is a run of n <= kRegLog2 shears
-// on register bits 0..n-1 in order, so the round's parameters are read with
-// compile-time offsets and no per-gate dispatch is left in the loop (k_tile's
-// generic gate loop costs more integer work and registers than the 2 FP64
-// instructions per amplitude a shear needs).
+// A pass whose rounds are runs of shears (QS_FUSE_FACTORED) on register bits
+// 0..n-1 in order -- optionally two such runs around one cut phase -- with the
+// product diagonals at its ends.  The round's parameters are read at
+// compile-time offsets and each round is one straight-line template instance,
+// so no per-gate dispatch is left in the loop (k_tile's generic gate loop costs
+// more integer work and registers than the 2 FP64 instructions per amplitude a
+// shear needs).  TABLES: per-state t (pool mode: the QAOA mixer RX(2 beta_s));
+// PHASE: rounds may hold a cut phase (per-state LUT rows, the per-state shear
+// scalars folded in by factor.cu).
 struct FactRound {
-    double t[kRegLog2];      // 0 for register bits without a shear (exact identity)
-    double2 pre[kRegLog2];   // (1, 0) without a pre-diagonal
-    int32_t n, pre_mask, pad0, pad1;
+    double t[2][kRegLog2];        // run A / run B; 0 pads bits without a shear (exact identity)
+    double2 pre[2][kRegLog2];     // (1, 0) without a pre-diagonal
+    uint64_t toff[2][kRegLog2];   // TABLES: t = mats[toff + state * tstride]
+    uint32_t tstride[2][kRegLog2];
+    int32_t n[2], pre_any, mid;   // mid: a cut phase between run A and run B
+    uint64_t lut_off, lut_stride;
 };
 struct alignas(16) FactPass {
     int32_t m, num_rounds, low_run, direct_store;
     int32_t tile_bits[kTileLog2];
     int32_t ntab, has_din, has_dout, pad;
-    uint64_t tiles_per_state, num_tiles;
+    uint64_t tiles_per_state, num_tiles, rank_offset;
     uint64_t din_off, dout_off;  // DiagN tables in mats (doubles)
     double2 din_r[1 << kRegLog2], dout_r[1 << kRegLog2];  // register parts (TilePass::diag_r)
+    uint64_t nbr[64];            // cut-phase graph (TilePass::nbr)
     Round rounds[kMaxRounds];
     FactRound fr[kMaxRounds];
 };
 
-template <int J, bool PRE>
-__device__ __forceinline__ void fact_shear(double2 (&a)[kRegAmps], const FactRound& F) {
-    const double t = F.t[J];
+template <int J, bool PRE, bool TABLES>
+__device__ __forceinline__ void fact_shear(double2 (&a)[kRegAmps], const FactRound& F, int grp,
+                                           const double* __restrict__ mats, uint64_t st) {
+    const double t = TABLES ? __ldg(mats + F.toff[grp][J] + st * F.tstride[grp][J]) : F.t[grp][J];
     if (PRE) {
-        const double2 z = F.pre[J];
+        const double2 z = F.pre[grp][J];
 #pragma unroll
         for (int k = 0; k < kRegAmps; ++k)
             if ((k >> J) & 1) a[k] = cmul(a[k], z);
@@ -778,15 +786,59 @@ __device__ __forceinline__ void fact_shear(double2 (&a)[kRegAmps], const FactRou
     }
 }
 
+template <bool PRE, bool TABLES>
+__device__ __forceinline__ void fact_run(double2 (&a)[kRegAmps], const FactRound& F, int grp,
+                                         const double* __restrict__ mats, uint64_t st) {
+    fact_shear<0, PRE, TABLES>(a, F, grp, mats, st);
+    fact_shear<1, PRE, TABLES>(a, F, grp, mats, st);
+    fact_shear<2, PRE, TABLES>(a, F, grp, mats, st);
+    if (kRegLog2 > 3) fact_shear<(kRegLog2 > 3 ? 3 : 0), PRE, TABLES>(a, F, grp, mats, st);
+    if (kRegLog2 > 4) fact_shear<(kRegLog2 > 4 ? 4 : 0), PRE, TABLES>(a, F, grp, mats, st);
+}
+
+// psi_i *= lut[cut(i)] on the 16 register amplitudes: the cut of the k = 0
+// amplitude in full, then a Gray walk over the register qubits (flipping
+// qubit r changes the cut by deg(r) - 2 * (edges of r currently cut), and an
+// edge inside the flipped set keeps its status) -- the same walk as k_tile's.
+__device__ __forceinline__ void fact_cut_phase(double2 (&a)[kRegAmps], const FactPass& P,
+                                               const Round& R, const CutTerms& ct,
+                                               const double2* lut, uint64_t il) {
+    const uint64_t i = P.rank_offset | il;
+    const int cut0 = cut_of(i, ct);
+    int rq[kRegLog2], d[kRegLog2], bq[kRegLog2];
+    uint64_t nbq[kRegLog2];
+#pragma unroll
+    for (int j = 0; j < kRegLog2; ++j) {
+        rq[j] = P.tile_bits[__ffs(R.dk[1 << j]) - 1];
+        nbq[j] = P.nbr[rq[j]];
+        bq[j] = int((i >> rq[j]) & 1);
+        d[j] = __popcll(nbq[j]) - 2 * __popcll((i ^ (uint64_t(0) - uint64_t(bq[j]))) & nbq[j]);
+    }
+    int cuts[kRegAmps];
+    cuts[0] = cut0;
+#pragma unroll
+    for (int k = 1; k < kRegAmps; ++k) {
+        const int h = 31 - __clz(k);
+        int c = cuts[k ^ (1 << h)] + d[h];
+#pragma unroll
+        for (int j = 0; j < h; ++j)
+            if ((k >> j) & 1) c += ((nbq[h] >> rq[j]) & 1) ? 4 * (bq[h] ^ bq[j]) - 2 : 0;
+        cuts[k] = c;
+    }
+#pragma unroll
+    for (int k = 0; k < kRegAmps; ++k) a[k] = cmul(a[k], __ldg(lut + cuts[k]));
+}
+
 // One register round of a lean pass, straight-line for its flags: product
-// diagonal before (DIN) / after (DOUT) the shears, pre-diagonals (PRE), and the
-// store of the 16 amplitudes to HBM (GSTORE) or back to the shared tile.  Every
-// round applies kRegLog2 shears (t = 0 is an exact identity), so no amplitude
-// register is live across a data-dependent branch (each join would cost 64
-// register moves).
-template <bool DIN, bool PRE, bool DOUT, bool GSTORE>
+// diagonal before (DIN) / after (DOUT), pre-diagonals (PRE), a cut phase and a
+// second shear run (MID), and the store of the 16 amplitudes to HBM (GSTORE)
+// or back to the shared tile.  Every run applies kRegLog2 shears (t = 0 is an
+// exact identity), so no amplitude register is live across a data-dependent
+// branch (each join would cost 64 register moves).
+template <bool TABLES, bool DIN, bool PRE, bool DOUT, bool GSTORE, bool MID>
 __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass& P,
-                                          const FactRound& F, const double* __restrict__ mats,
+                                          const Round& R, const FactRound& F, const CutTerms& ct,
+                                          const double* __restrict__ mats, uint64_t st,
                                           uint64_t il, double2* tile, int sb,
                                           const int (&skb)[kRegLog2], double2* gb,
                                           const uint64_t (&okb)[kRegLog2]) {
@@ -794,11 +846,12 @@ __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass
         const double2* T = reinterpret_cast<const double2*>(mats + P.din_off);
         reg_diag_n(a, T, P.ntab, il, P.din_r);
     }
-    fact_shear<0, PRE>(a, F);
-    fact_shear<1, PRE>(a, F);
-    fact_shear<2, PRE>(a, F);
-    if (kRegLog2 > 3) fact_shear<(kRegLog2 > 3 ? 3 : 0), PRE>(a, F);
-    if (kRegLog2 > 4) fact_shear<(kRegLog2 > 4 ? 4 : 0), PRE>(a, F);
+    fact_run<PRE, TABLES>(a, F, 0, mats, st);
+    if (MID) {
+        fact_cut_phase(a, P, R, ct,
+                       reinterpret_cast<const double2*>(mats + F.lut_off + st * F.lut_stride), il);
+        fact_run<PRE, TABLES>(a, F, 1, mats, st);
+    }
     if (DOUT) {
         const double2* T = reinterpret_cast<const double2*>(mats + P.dout_off);
         reg_diag_n(a, T, P.ntab, il, P.dout_r);
@@ -830,29 +883,30 @@ __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass
     }
 }
 
-#define QSB_FACT_DISPATCH(sel, ...)                                   \
-    switch (sel) {                                                    \
-        case 0: fact_body<0, 0, 0, 0>(__VA_ARGS__); break;            \
-        case 1: fact_body<1, 0, 0, 0>(__VA_ARGS__); break;            \
-        case 2: fact_body<0, 1, 0, 0>(__VA_ARGS__); break;            \
-        case 3: fact_body<1, 1, 0, 0>(__VA_ARGS__); break;            \
-        case 4: fact_body<0, 0, 1, 0>(__VA_ARGS__); break;            \
-        case 5: fact_body<1, 0, 1, 0>(__VA_ARGS__); break;            \
-        case 6: fact_body<0, 1, 1, 0>(__VA_ARGS__); break;            \
-        case 7: fact_body<1, 1, 1, 0>(__VA_ARGS__); break;            \
-        case 8: fact_body<0, 0, 0, 1>(__VA_ARGS__); break;            \
-        case 9: fact_body<1, 0, 0, 1>(__VA_ARGS__); break;            \
-        case 10: fact_body<0, 1, 0, 1>(__VA_ARGS__); break;           \
-        case 11: fact_body<1, 1, 0, 1>(__VA_ARGS__); break;           \
-        case 12: fact_body<0, 0, 1, 1>(__VA_ARGS__); break;           \
-        case 13: fact_body<1, 0, 1, 1>(__VA_ARGS__); break;           \
-        case 14: fact_body<0, 1, 1, 1>(__VA_ARGS__); break;           \
-        default: fact_body<1, 1, 1, 1>(__VA_ARGS__); break;           \
+#define QSB_FB(TB, MI, sel, ...)                                                  \
+    switch (sel) {                                                                \
+        case 0: fact_body<TB, 0, 0, 0, 0, MI>(__VA_ARGS__); break;                \
+        case 1: fact_body<TB, 1, 0, 0, 0, MI>(__VA_ARGS__); break;                \
+        case 2: fact_body<TB, 0, 1, 0, 0, MI>(__VA_ARGS__); break;                \
+        case 3: fact_body<TB, 1, 1, 0, 0, MI>(__VA_ARGS__); break;                \
+        case 4: fact_body<TB, 0, 0, 1, 0, MI>(__VA_ARGS__); break;                \
+        case 5: fact_body<TB, 1, 0, 1, 0, MI>(__VA_ARGS__); break;                \
+        case 6: fact_body<TB, 0, 1, 1, 0, MI>(__VA_ARGS__); break;                \
+        case 7: fact_body<TB, 1, 1, 1, 0, MI>(__VA_ARGS__); break;                \
+        case 8: fact_body<TB, 0, 0, 0, 1, MI>(__VA_ARGS__); break;                \
+        case 9: fact_body<TB, 1, 0, 0, 1, MI>(__VA_ARGS__); break;                \
+        case 10: fact_body<TB, 0, 1, 0, 1, MI>(__VA_ARGS__); break;               \
+        case 11: fact_body<TB, 1, 1, 0, 1, MI>(__VA_ARGS__); break;               \
+        case 12: fact_body<TB, 0, 0, 1, 1, MI>(__VA_ARGS__); break;               \
+        case 13: fact_body<TB, 1, 0, 1, 1, MI>(__VA_ARGS__); break;               \
+        case 14: fact_body<TB, 0, 1, 1, 1, MI>(__VA_ARGS__); break;               \
+        default: fact_body<TB, 1, 1, 1, 1, MI>(__VA_ARGS__); break;               \
     }
 
+template <bool TABLES, bool PHASE>
 __global__ void __launch_bounds__(kTileThreads, QSB_TILE_MINB)
     k_fact(double2* __restrict__ psi, const __grid_constant__ FactPass P,
-           const double* __restrict__ mats) {
+           const double* __restrict__ mats, const __grid_constant__ CutTerms ct) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2* tile = reinterpret_cast<double2*>(smem_raw);
     uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(double2) * kTileAmps);
@@ -931,8 +985,9 @@ __global__ void __launch_bounds__(kTileThreads, QSB_TILE_MINB)
     prefetch(blockIdx.x);
 
     for (uint64_t tile_id = blockIdx.x; tile_id < P.num_tiles; tile_id += stride_tiles) {
+        const uint64_t st = tile_id >> tps_log2;
         const uint64_t base_local = tile_base(tile_id);
-        double2* gbase = psi + (((tile_id >> tps_log2) << m) | base_local);
+        double2* gbase = psi + ((st << m) | base_local);
         cp_async_wait_all();
         named_sync(1, kTileThreads);
         for (int r = 0; r < P.num_rounds; ++r) {
@@ -961,14 +1016,18 @@ __global__ void __launch_bounds__(kTileThreads, QSB_TILE_MINB)
             }
             const FactRound& F = P.fr[r];
             const bool gstore = last && direct;
-            const int sel = int(r == 0 && P.has_din) | (F.pre_mask ? 2 : 0) |
+            const int sel = int(r == 0 && P.has_din) | (F.pre_any ? 2 : 0) |
                             int(last && P.has_dout) << 2 | int(gstore) << 3;
             const uint64_t il = base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask);
             uint64_t okb[kRegLog2];
 #pragma unroll
             for (int j = 0; j < kRegLog2; ++j) okb[j] = gstore ? goff(R.dk[1 << j]) : 0;
             double2* gb = gbase + (gstore ? goff(eb) : 0);
-            QSB_FACT_DISPATCH(sel, a, P, F, mats, il, tile, sb, skb, gb, okb)
+            if (PHASE && F.mid) {
+                QSB_FB(TABLES, (PHASE && true), sel, a, P, R, F, ct, mats, st, il, tile, sb, skb, gb, okb)
+            } else {
+                QSB_FB(TABLES, false, sel, a, P, R, F, ct, mats, st, il, tile, sb, skb, gb, okb)
+            }
             if (gstore) break;
             named_sync(1, kTileThreads);
         }
@@ -983,11 +1042,12 @@ __global__ void __launch_bounds__(kTileThreads, QSB_TILE_MINB)
     }
 }
 
-// The lean kernel applies when every gate of the pass is a shear in in-order
-// register runs, with product diagonals only first in round 0 / last in the
-// last round.
-bool fact_pass_from(const TilePass& T, FactPass* F) {
+// The lean kernel applies when every round of the pass is a run of shears on
+// register bits 0,1,.. in order, or two such runs around one cut phase, with
+// product diagonals only first in round 0 / last in the last round.
+bool fact_pass_from(const TilePass& T, FactPass* F, bool* tables, bool* phase) {
     memset(F, 0, sizeof(*F));
+    *tables = *phase = false;
     F->m = T.m;
     F->num_rounds = T.num_rounds;
     F->low_run = T.low_run;
@@ -995,14 +1055,20 @@ bool fact_pass_from(const TilePass& T, FactPass* F) {
     memcpy(F->tile_bits, T.tile_bits, sizeof(F->tile_bits));
     F->tiles_per_state = T.tiles_per_state;
     F->num_tiles = T.num_tiles;
+    F->rank_offset = T.rank_offset;
+    memcpy(F->nbr, T.nbr, sizeof(F->nbr));
     memcpy(F->rounds, T.rounds, sizeof(Round) * T.num_rounds);
     for (int r = 0; r < T.num_rounds; ++r) {
         const Round& R = T.rounds[r];
         FactRound& FR = F->fr[r];
-        for (int j = 0; j < kRegLog2; ++j) {
-            FR.t[j] = 0.0;
-            FR.pre[j] = make_double2(1.0, 0.0);
-        }
+        for (int h = 0; h < 2; ++h)
+            for (int j = 0; j < kRegLog2; ++j) {
+                FR.t[h][j] = 0.0;
+                FR.pre[h][j] = make_double2(1.0, 0.0);
+                FR.toff[h][j] = 0;
+                FR.tstride[h][j] = 0;
+            }
+        int grp = 0;
         for (int g = R.first_gate; g < R.first_gate + R.num_gates; ++g) {
             const TileGate& G = T.gates[g];
             if (G.kind == kKindDiagN) {
@@ -1020,15 +1086,37 @@ bool fact_pass_from(const TilePass& T, FactPass* F) {
                 F->ntab = G.cval;
                 continue;
             }
-            if (G.kind != kKindShear || G.variant != FR.n || FR.n >= kRegLog2) return false;
             if (F->has_dout) return false;  // D_out must be the last op
-            if (G.u[0].y != 0.0) return false;  // only form A shears exist
-            FR.t[FR.n] = G.u[0].x;
-            if (G.u[1].x != 0.0) {
-                FR.pre_mask |= 1 << FR.n;
-                FR.pre[FR.n] = G.u[2];
+            if (G.kind == QS_KIND_CUTPHASE) {
+                if (grp != 0) return false;
+                grp = 1;
+                FR.mid = 1;
+                FR.lut_off = G.offset;
+                FR.lut_stride = G.stride;
+                *phase = true;
+                continue;
             }
-            FR.n++;
+            const int n = FR.n[grp];
+            if (G.kind != kKindShear || G.variant != n || n >= kRegLog2) return false;
+            if (G.u[0].y != 0.0) return false;  // only form A shears exist
+            FR.t[grp][n] = G.u[0].x;
+            if (G.u[1].x != 0.0) {  // pre-diagonal (shared by construction for per-state t)
+                FR.pre_any = 1;
+                FR.pre[grp][n] = G.u[2];
+            }
+            if (G.stride != 0) *tables = true;
+            FR.toff[grp][n] = G.offset;
+            FR.tstride[grp][n] = uint32_t(G.stride);
+            FR.n[grp]++;
+        }
+    }
+    if (*tables) {
+        // per-state runs read every t from mats: shared ones with stride 0, the
+        // padding from the zero factor.cu appends to every factored program
+        for (int r = 0; r < T.num_rounds; ++r) {
+            FactRound& FR = F->fr[r];
+            for (int h = 0; h < 2; ++h)
+                for (int j = FR.n[h]; j < kRegLog2; ++j) FR.toff[h][j] = T.zero_off;
         }
     }
     return true;
@@ -1040,7 +1128,9 @@ size_t fact_smem_bytes() {
            sizeof(uint32_t) * kMaxRounds * ((1 << kLaneLoBits) + (1 << kLaneHiBits));
 }
 
-void launch_fact(double2* psi, const FactPass& F, const double* mats, cudaStream_t s) {
+template <bool TB, bool PH>
+void launch_fact_variant(double2* psi, const FactPass& F, const double* mats, const CutTerms& ct,
+                         cudaStream_t s) {
     constexpr int kMaxDevices = 64;
     static std::atomic<int> configured[kMaxDevices];
     static int sms_of[kMaxDevices], per_sm_of[kMaxDevices];
@@ -1049,17 +1139,28 @@ void launch_fact(double2* psi, const FactPass& F, const double* mats, cudaStream
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= kMaxDevices) dev = 0;
     if (configured[dev].load(std::memory_order_acquire) == 0) {
-        cudaFuncSetAttribute(k_fact, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaFuncSetAttribute(k_fact<TB, PH>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         int sms = 148, per_sm = 1;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fact, kTileThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fact<TB, PH>, kTileThreads, smem);
         sms_of[dev] = sms;
         per_sm_of[dev] = per_sm < 1 ? 1 : per_sm;
         configured[dev].store(1, std::memory_order_release);
     }
     uint64_t grid = uint64_t(sms_of[dev]) * per_sm_of[dev];
     if (grid > F.num_tiles) grid = F.num_tiles;
-    k_fact<<<unsigned(grid), kTileThreads, smem, s>>>(psi, F, mats);
+    k_fact<TB, PH><<<unsigned(grid), kTileThreads, smem, s>>>(psi, F, mats, ct);
+}
+
+void launch_fact(double2* psi, const FactPass& F, const double* mats, const CutTerms& ct,
+                 bool tables, bool phase, cudaStream_t s) {
+    if (tables) {
+        if (phase) launch_fact_variant<true, true>(psi, F, mats, ct, s);
+        else launch_fact_variant<true, false>(psi, F, mats, ct, s);
+    } else {
+        if (phase) launch_fact_variant<false, true>(psi, F, mats, ct, s);
+        else launch_fact_variant<false, false>(psi, F, mats, ct, s);
+    }
 }
 
 __global__ void k_fill(double2* __restrict__ psi, uint64_t count, double2 value) {
@@ -1214,10 +1315,11 @@ bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_d
     }
     const uint64_t nt = pass.num_tiles;
     static const bool lean_ok = getenv("QSB_NO_LEAN") == nullptr;
-    if (fact && !phase && !generic && !tables && kGroups == 1 && lean_ok) {
+    if (fact && !generic && kGroups == 1 && lean_ok) {
         static thread_local FactPass F;
-        if (fact_pass_from(pass, &F)) {
-            launch_fact(psi, F, mats, s);
+        bool tb = false, ph = false;
+        if (fact_pass_from(pass, &F, &tb, &ph)) {
+            launch_fact(psi, F, mats, ct, tb, ph, s);
             return true;
         }
     }
