@@ -198,7 +198,17 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         fs.resize(size_t(num_states) * 10);
         for (int st = 0; st < num_states; ++st) {
             double* f = fs.data() + 10 * st;
-            if (!decompose_2x2(mats + g.offset + uint64_t(st) * g.stride, f)) return false;
+            const double* u = mats + g.offset + uint64_t(st) * g.stride;
+            // RX(theta) = [[c, -is], [-is, c]] = c * diag(1, i) [[1,-t],[t,1]] diag(1, -i)
+            // with t = -s/c: closed form (the QAOA mixer, 80 x 512 matrices a step)
+            if (u[0] == u[6] && u[1] == 0 && u[7] == 0 && u[2] == 0 && u[4] == 0 && u[3] == u[5] &&
+                std::abs(u[0] * u[0] + u[3] * u[3] - 1.0) <= 1e-12 && std::abs(u[0]) >= 1e-9) {
+                f[0] = u[0] < 0 ? -1.0 : 1.0, f[1] = 0.0;
+                f[2] = 0.0, f[3] = 1.0, f[4] = 0.0, f[5] = -1.0;
+                f[6] = 0.0, f[7] = u[3] / u[0], f[8] = std::abs(u[0]), f[9] = 0.0;
+            } else if (!decompose_2x2(u, f)) {
+                return false;
+            }
             if (st == 0 && (f[3] < 0 || (f[3] == 0 && f[2] < 0))) {
                 // canonical sign (Im za >= 0): consecutive gates of one family
                 // (RX layers) then meet with za * zb = 1 and need no pre-diagonal
