@@ -434,9 +434,11 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         for (int b = 0; b < kTileLog2; ++b) fprintf(stderr, "%d%s", P.tile_bits[b], b + 1 < kTileLog2 ? "," : "");
         for (int rr = 0; rr < P.num_rounds; ++rr) {
             fprintf(stderr, " [");
-            for (int g = P.rounds[rr].first_gate; g < P.rounds[rr].first_gate + P.rounds[rr].num_gates; ++g)
+            for (int g = P.rounds[rr].first_gate; g < P.rounds[rr].first_gate + P.rounds[rr].num_gates; ++g) {
                 fprintf(stderr, "%s%d:%d", g > P.rounds[rr].first_gate ? " " : "", P.gates[g].kind,
                         prog[first + g].target);
+                if (P.gates[g].kind == QS_KIND_CTRL) fprintf(stderr, "/c%d", P.gates[g].ctype);
+            }
             fprintf(stderr, "]");
         }
         fprintf(stderr, "\n");
