@@ -792,26 +792,28 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
     }
     for (int i = 0; i < count; ++i)
         if (int rc = validate_gate(st, gates[i], mats_len, num_edges)) return rc;
+    static thread_local FactoredProgram fp;
+    static thread_local std::vector<double> all;
     if (fuse == QS_FUSE_FACTORED && st->m >= kTileLog2) {
         // rewrite, then plan the rewritten program; its parameters and diagonal
-        // tables follow the caller's table in one upload
-        static thread_local FactoredProgram fp;
-        static thread_local std::vector<double> all;
+        // tables follow the caller's table in one upload.  Programs where fewer
+        // than half of the gates factor (noise trajectories) run exact: the
+        // rewrite does not pay there.
         factor_program(gates, count, mats, mats_len, st->m, st->num_states, num_edges, &fp);
-        if (2 * fp.factored < count) goto exact;  // mostly unfactorable: the rewrite does not pay
-        all.assign(mats, mats + mats_len);
-        all.insert(all.end(), fp.extra.begin(), fp.extra.end());
-        uint64_t support = 0;
-        for (int e = 0; e < 2 * num_edges; ++e) support |= uint64_t(1) << edges[e];
-        static const bool reorder = getenv("QSB_NO_REORDER") == nullptr;
-        if (reorder) schedule_program(fp.gates, st->m, support, all.data(), st->num_states);
-        g_zero_off = fp.zero_off;
-        gates = fp.gates.data();
-        count = int(fp.gates.size());
-        mats = all.data();
-        mats_len = all.size();
+        if (2 * fp.factored >= count) {
+            all.assign(mats, mats + mats_len);
+            all.insert(all.end(), fp.extra.begin(), fp.extra.end());
+            uint64_t support = 0;
+            for (int e = 0; e < 2 * num_edges; ++e) support |= uint64_t(1) << edges[e];
+            static const bool reorder = getenv("QSB_NO_REORDER") == nullptr;
+            if (reorder) schedule_program(fp.gates, st->m, support, all.data(), st->num_states);
+            g_zero_off = fp.zero_off;
+            gates = fp.gates.data();
+            count = int(fp.gates.size());
+            mats = all.data();
+            mats_len = all.size();
+        }
     }
-exact:
     if (int rc = grow(&st->d_mats, &st->mats_cap, mats_len ? mats_len : 1)) return rc;
     if (mats_len)
         CUDA_TRY(cudaMemcpyAsync(st->d_mats, mats, mats_len * sizeof(double),

@@ -273,3 +273,37 @@ def test_factored_pool_per_state_gates():
             osv.apply_1q(expected[s], q, us[s])
     got = pool.amplitudes()
     assert max_dev(got, expected) <= TOL
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("remap", [False, True])
+def test_factored_config4_distributed(P, remap):
+    """Config 4 recipe at n=14 over 2/4 emulated ranks (m = 13/12, so the local
+    programs are factored): local shears, global-qubit exchanges (or qubit
+    remapping) and case-(c) CNOTs, against the oracle's full state."""
+    from paper_2001_10554_b200.circuit import GateSpec
+    n = 14
+    rng = np.random.default_rng(40 + P)
+    psi0 = ogates.random_state(n, rng)
+    seq, prog = [], []
+    for layer in range(3):
+        for q in range(n):
+            u = ogates.random_unitary_2x2(rng)
+            seq.append(GateSpec("custom", (q,), matrix=u))
+            prog.append({"kind": "custom", "qubits": (q,), "matrix": u})
+        for q in range(n // 2):
+            seq.append(GateSpec("cx", (q, n - 1 - q)))
+            prog.append({"kind": "cx", "qubits": (q, n - 1 - q)})
+    circ = Circuit(n, tuple(seq))
+    expect = ocirc.run(n, prog, psi0)
+
+    def rank_fn(comm):
+        ctx = runtime.make_context(comm, n, 1, 0, fuse=FACT, remap=remap)
+        m = ctx.topology.num_local_qubits
+        ctx.partition.amplitudes = psi0[comm.rank << m:(comm.rank + 1) << m]
+        ctx.norm_check_interval = 0
+        runtime.run_circuit(ctx, circ)
+        return runtime.gather_group_state(ctx)
+
+    out = runtime.run_spmd(P, rank_fn, timeout=120.0)[0]
+    assert max_dev(out, expect) <= TOL
