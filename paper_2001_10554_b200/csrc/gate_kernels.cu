@@ -346,6 +346,29 @@ __device__ __forceinline__ void reg_diag_n(double2 (&a)[kRegAmps], const double2
     for (int k = 1; k < kRegAmps; ++k) a[k] = cmul(a[k], cmul(f, R[k]));
 }
 
+// variant j (uncontrolled, target register bit j) or kRegLog2 + kRegLog2*c + j
+// (controlled by register bit c), kRegLog2 == 4
+__device__ __forceinline__ void reg_gate_switch(double2 (&a)[kRegAmps], const double2 u[4],
+                                                int variant) {
+#if QSB_REG_LOG2 == 4
+#define QSB_CG(c, j) case 4 + 4 * (c) + (j): reg_gate<j, c>(a, u); break;
+    switch (variant) {
+        case 0: reg_gate<0, -1>(a, u); break;
+        case 1: reg_gate<1, -1>(a, u); break;
+        case 2: reg_gate<2, -1>(a, u); break;
+        case 3: reg_gate<3, -1>(a, u); break;
+        QSB_CG(0, 1) QSB_CG(0, 2) QSB_CG(0, 3)
+        QSB_CG(1, 0) QSB_CG(1, 2) QSB_CG(1, 3)
+        QSB_CG(2, 0) QSB_CG(2, 1) QSB_CG(2, 3)
+        QSB_CG(3, 0) QSB_CG(3, 1) QSB_CG(3, 2)
+        default: break;
+    }
+#undef QSB_CG
+#else
+    (void)a, (void)u, (void)variant;  // other builds use reg_gate_generic
+#endif
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
@@ -654,15 +677,21 @@ __global__ void __launch_bounds__(kCtaThreads, QSB_TILE_MINB)
                         if (G.ctype == 3 && !((base_local >> G.cval) & 1)) continue;
                         double2 u[4];
                         gate_matrix<TABLES>(u, G, tm_cur + 4 * g);
-                        // register control c: only pairs whose register index has bit c set
-                        unsigned mask = (kRegAmps >= 32) ? 0xffffffffu : ((1u << kRegAmps) - 1);
-                        if (G.ctype == 1) {
-                            mask = 0;
+                        if (kRegLog2 == 4) {
+                            // (control, target) register bits as compile-time cases:
+                            // a register-controlled gate runs exactly its 4 pairs
+                            reg_gate_switch(a, u, G.variant);
+                        } else {
+                            // register control c: only pairs whose register index has bit c set
+                            unsigned mask = (kRegAmps >= 32) ? 0xffffffffu : ((1u << kRegAmps) - 1);
+                            if (G.ctype == 1) {
+                                mask = 0;
 #pragma unroll
-                            for (int k = 0; k < kRegAmps; ++k)
-                                if ((k >> G.cval) & 1) mask |= 1u << k;
+                                for (int k = 0; k < kRegAmps; ++k)
+                                    if ((k >> G.cval) & 1) mask |= 1u << k;
+                            }
+                            reg_gate_generic(a, u, G.variant % kRegLog2, mask);
                         }
-                        reg_gate_generic(a, u, G.variant % kRegLog2, mask);
                     }
                 }
             }
