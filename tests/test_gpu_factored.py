@@ -307,3 +307,26 @@ def test_factored_config4_distributed(P, remap):
 
     out = runtime.run_spmd(P, rank_fn, timeout=120.0)[0]
     assert max_dev(out, expect) <= TOL
+
+
+def test_factored_pool_per_state_rescaling():
+    """25 per-state shears with c ~ 2e-9 (t ~ 5e8): the per-state scales pass
+    2^-600, so the rewrite inserts per-state scalar ops mid-program (and the
+    amplitudes, grown by up to 5e8 per shear, stay finite)."""
+    from oracle import statevector as osv
+    rng = np.random.default_rng(21)
+    n, S = 12, 3
+    states = np.stack([ogates.random_state(n, rng) for _ in range(S)])
+    pool = runtime.PoolState(n, S, fuse=FACT)
+    pool.state.upload(states)
+    expected = states.copy()
+    for k in range(25):
+        q = k % n
+        th = np.array([np.pi - 4e-9, np.pi + 4e-9, 1.0 + k])
+        us = np.stack([ogates.rx(float(x)) for x in th])
+        pool.queue.one_qubit(q, us)
+        for s in range(S):
+            osv.apply_1q(expected[s], q, us[s])
+    got = pool.amplitudes()
+    assert np.all(np.isfinite(got))
+    assert max_dev(got, expected) <= TOL
