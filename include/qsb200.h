@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define QSB200_ABI_VERSION 1
+#define QSB200_ABI_VERSION 2  /* 2: QS_FUSE_FACTORED, qs_decompose_2x2 */
 
 /* status codes -- the Python shim maps them to the reference exceptions */
 #define QS_OK            0

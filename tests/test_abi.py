@@ -20,7 +20,7 @@ def header_functions():
 
 def test_library_loads_and_version():
     lib = N.load()
-    assert lib.qs_abi_version() == 1
+    assert lib.qs_abi_version() == 2
 
 
 def test_exports_match_header():
