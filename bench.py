@@ -716,7 +716,8 @@ def run_qaoa(args, dist, comm, world, rank, local):
             "config": {"workload": f"config 5: QAOA MaxCut pool, {S} circuits per swarm step "
                                    f"(n={n}, p={depth}, random 3-regular graph), <C> per "
                                    "circuit, host PSO move", "pool": S, "per_gpu": count,
-                       "gates_per_circuit": gates_per_circuit, "fused": not args.no_fuse},
+                       "gates_per_circuit": gates_per_circuit, "fused": not args.no_fuse,
+                       "numerics": args.numerics},
             "circuits_per_s": circuits / wall,
             "best_ratio": float(np.max(best_val)),
             "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
@@ -890,7 +891,8 @@ def run_noise(args, dist, comm, world, rank, local):
                                    f"config-5 QAOA circuit (n={n}, p={QAOA_P}, schedule_noise, "
                                    f"T1={NOISE_T1}, T2={NOISE_T2}), <C> per trajectory",
                        "pool": S, "per_gpu": count, "gates_per_circuit": gates_per_circuit,
-                       "noise_gates": noise_gates, "fused": not args.no_fuse},
+                       "noise_gates": noise_gates, "fused": not args.no_fuse,
+                       "numerics": args.numerics},
             "trajectories_per_s": trajectories / wall,
             "mean_cut": float(np.mean(values)),
             "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",

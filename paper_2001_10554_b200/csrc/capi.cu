@@ -392,6 +392,7 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         if (g.stride == 0 || g.kind == kKindShear)
             memcpy(&d.u[0], mats_host + g.offset, 8 * sizeof(double));
         if (g.kind == kKindScalar) continue;
+        if (g.kind == kKindShear) d.pad[1] = g.reserved;  // 1: per-state pre-diagonals
         const std::vector<int>& rp = all_pos[gate_round[i]];
         int p = pos_of(g.target), j = 0;
         for (int jj = 0; jj < kRegLog2; ++jj)

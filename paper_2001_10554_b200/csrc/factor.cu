@@ -156,7 +156,33 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         const double p[8] = {0, 0, 0, 0, z.real(), z.imag(), 0, 0};
         emit(kKindDiag1, q, params(p));
     };
+    // per-state pending diagonals (pool gates whose diagonals differ between
+    // states, e.g. noise trajectories): psp[q][s] replaces pending[q] (then 1)
+    std::vector<std::vector<cd>> psp(m);
+    auto per_state_rows = [&](int kind, int q, const std::vector<double>& t, const std::vector<cd>& z,
+                              bool has_z) {
+        while (out->extra.size() % 2) out->extra.push_back(0.0);
+        const uint64_t off = mats_len + out->extra.size();
+        for (int st = 0; st < num_states; ++st) {
+            const double p[8] = {t.empty() ? 0.0 : t[st], 0, has_z ? 1.0 : 0.0, 0,
+                                 z[st].real(), z[st].imag(), 0, 0};
+            out->extra.insert(out->extra.end(), p, p + 8);
+        }
+        qs_gate g;
+        memset(&g, 0, sizeof(g));
+        g.kind = kind;
+        g.target = q;
+        g.control = -1;
+        g.offset = off;
+        g.stride = 8;
+        g.reserved = 1;  // per-state pre-diagonals: not for the lean kernel's shared pre
+        out->gates.push_back(g);
+    };
     auto flush = [&](int q) {  // make the pending diagonal on q explicit before a mixing gate
+        if (!psp[q].empty()) {
+            per_state_rows(kKindDiag1, q, {}, psp[q], true);
+            psp[q].clear();
+        }
         if (pending[q] != 1.0) {
             if (!mixed[q]) din[q] *= pending[q];
             else diag1(q, pending[q]);
@@ -196,6 +222,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
     auto per_state_shear = [&](const qs_gate& g) {
         const int q = g.target;
         fs.resize(size_t(num_states) * 10);
+        bool same = true;
         for (int st = 0; st < num_states; ++st) {
             double* f = fs.data() + 10 * st;
             const double* u = mats + g.offset + uint64_t(st) * g.stride;
@@ -219,10 +246,37 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             const cd za0(fs[2], fs[3]), zb0(fs[4], fs[5]), za1(f[2], f[3]), zb1(f[4], f[5]);
             if (std::abs(za1 - za0) <= 1e-13 && std::abs(zb1 - zb0) <= 1e-13) continue;
             if (std::abs(za1 + za0) <= 1e-13 && std::abs(zb1 + zb0) <= 1e-13) {
-                f[7] = -f[7];
+                // keep the state's triple consistent (the per-state path uses it)
+                f[2] = -f[2], f[3] = -f[3], f[4] = -f[4], f[5] = -f[5], f[7] = -f[7];
                 continue;
             }
-            return false;
+            same = false;
+        }
+        if (!same || !psp[q].empty()) {
+            // per-state diagonals: every state's pre-diagonal and pending za
+            // are its own (no product diagonal at the program ends)
+            std::vector<double> t(num_states);
+            std::vector<cd> pre(num_states), za_s(num_states);
+            bool any_pre = false;
+            double small = 1.0;
+            for (int st = 0; st < num_states; ++st) {
+                const double* f = fs.data() + 10 * st;
+                const cd zb(f[4], f[5]);
+                pre[st] = (psp[q].empty() ? pending[q] : psp[q][st]) * zb;
+                any_pre |= pre[st] != 1.0;
+                za_s[st] = cd(f[2], f[3]);
+                t[st] = f[7];
+                Ks[st] *= cd(f[0], f[1]) * f[8];
+                small = std::min(small, std::abs(Ks[st]));
+            }
+            per_state_rows(kKindShear, q, t, pre, any_pre);
+            out->factored++;
+            per_state_k = true;
+            pending[q] = 1.0;
+            psp[q] = za_s;
+            mixed[q] = 1;
+            if (small < 0x1p-600) per_state_scalars();
+            return true;
         }
         const cd za(fs[2], fs[3]), zb(fs[4], fs[5]);
         const cd pre = pending[q] * zb;
@@ -288,7 +342,8 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         if (entry(u, 1) == 0.0 && entry(u, 2) == 0.0 && std::abs(std::abs(u00) - 1.0) <= 1e-12 &&
             std::abs(std::abs(u11) - 1.0) <= 1e-12) {
             K *= u00;  // diag(u00, u11) = u00 * diag(1, u11/u00)
-            pending[q] *= u11 / u00;
+            if (psp[q].empty()) pending[q] *= u11 / u00;
+            else for (cd& z : psp[q]) z *= u11 / u00;
             out->factored++;  // absorbed: costs nothing per amplitude
             continue;
         }
@@ -300,6 +355,18 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             continue;
         }
         const cd k(f[0], f[1]), za(f[2], f[3]), zb(f[4], f[5]);
+        if (!psp[q].empty()) {
+            // shared gate after per-state diagonals on q: per-state pre-diagonals
+            std::vector<cd> pre(num_states);
+            for (int st = 0; st < num_states; ++st) pre[st] = psp[q][st] * zb;
+            per_state_rows(kKindShear, q, std::vector<double>(num_states, f[7]), pre, true);
+            K *= k * f[8];
+            out->factored++;
+            psp[q].clear();
+            pending[q] = za;
+            mixed[q] = 1;
+            continue;
+        }
         const cd pre = pending[q] * zb;
         K *= k * f[8];
         bool has_pre = false;
@@ -323,6 +390,8 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
     bool any_out = K != 1.0;
     for (int q = 0; q < m; ++q) any_out |= pending[q] != 1.0;
     if (any_out) out->gates.push_back(diag_tables(pending, K));
+    for (int q = 0; q < m; ++q)  // per-state pending diagonals close the program
+        if (!psp[q].empty()) per_state_rows(kKindDiag1, q, {}, psp[q], true);
     out->zero_off = mats_len + out->extra.size();
     out->extra.push_back(0.0);
     out->extra.push_back(0.0);

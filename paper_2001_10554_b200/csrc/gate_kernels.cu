@@ -1128,6 +1128,7 @@ bool fact_pass_from(const TilePass& T, FactPass* F, bool* tables, bool* phase) {
             const int n = FR.n[grp];
             if (G.kind != kKindShear || G.variant != n || n >= kRegLog2) return false;
             if (G.u[0].y != 0.0) return false;  // only form A shears exist
+            if (G.pad[1] != 0) return false;     // per-state pre-diagonals: k_tile
             FR.t[grp][n] = G.u[0].x;
             if (G.u[1].x != 0.0) {  // pre-diagonal (shared by construction for per-state t)
                 FR.pre_any = 1;

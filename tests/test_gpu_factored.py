@@ -330,3 +330,42 @@ def test_factored_pool_per_state_rescaling():
     got = pool.amplitudes()
     assert np.all(np.isfinite(got))
     assert max_dev(got, expected) <= TOL
+
+
+def test_factored_pool_per_state_diagonals_noise_like():
+    """Per-state gates whose diagonals differ between states (noise-trajectory
+    rotations rz.ry.rx with random angles) interleaved with shared and per-state
+    RX gates and cut phases: per-state pre-diagonals and pending diagonals."""
+    from oracle import statevector as osv
+    rng = np.random.default_rng(31)
+    n, S = 13, 5
+    edges = [(0, 4), (3, 9), (6, 12), (2, 11)]
+    graph = make_graph(n, edges)
+    states = np.stack([ogates.random_state(n, rng) for _ in range(S)])
+    pool = runtime.PoolState(n, S, fuse=FACT)
+    pool.state.upload(states)
+    expected = states.copy()
+    for step in range(60):
+        q = int(rng.integers(n))
+        r = rng.random()
+        if r < 0.4:
+            us = np.stack([ogates.rz(a) @ ogates.ry(b) @ ogates.rx(c)
+                           for a, b, c in rng.uniform(0, 0.3, size=(S, 3))])
+        elif r < 0.6:
+            us = np.stack([ogates.rx(float(x)) for x in rng.uniform(0, 2 * np.pi, S)])
+        elif r < 0.8:
+            us = np.stack([ogates.random_unitary_2x2(rng)] * S)
+        elif r < 0.9:
+            us = np.stack([ogates.rz(float(rng.uniform(0, 6)))] * S)
+        else:
+            gam = rng.uniform(0, np.pi, S)
+            pool.queue.cut_phase(graph, gam)
+            for s in range(S):
+                osv.apply_cut_phase(expected[s], edges, float(gam[s]))
+            continue
+        shared = all(np.array_equal(us[0], u) for u in us)
+        pool.queue.one_qubit(q, us[0] if shared else us)
+        for s in range(S):
+            osv.apply_1q(expected[s], q, us[s])
+    got = pool.amplitudes()
+    assert max_dev(got, expected) <= TOL
