@@ -304,6 +304,26 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         int nonround[kTileLog2 - kRegLog2], c = 0;
         for (int p = 0; p < kTileLog2; ++p)
             if (!(used & (1u << p))) nonround[c++] = p;
+        // lanes 0..2 (a quarter warp) should differ in the swizzle's bank bit
+        // (position p moves bank bit p mod 3): pull forward the first positions
+        // of distinct classes, keeping ascending order otherwise (when 0,1,2 are
+        // all lanes nothing moves, so direct stores stay 128-byte rows)
+        {
+            int picked[3], np = 0;
+            unsigned cls = 0;
+            for (int i = 0; i < c && np < 3; ++i)
+                if (!(cls & (1u << (nonround[i] % 3)))) {
+                    cls |= 1u << (nonround[i] % 3);
+                    picked[np++] = i;
+                }
+            if (np == 3) {
+                int reordered[kTileLog2 - kRegLog2], n2 = 0;
+                for (int j = 0; j < 3; ++j) reordered[n2++] = nonround[picked[j]];
+                for (int i = 0; i < c; ++i)
+                    if (i != picked[0] && i != picked[1] && i != picked[2]) reordered[n2++] = nonround[i];
+                for (int i = 0; i < c; ++i) nonround[i] = reordered[i];
+            }
+        }
         auto deposit = [](int v, const int* pos, int nbits) {
             int out = 0;
             for (int b = 0; b < nbits; ++b)
