@@ -145,7 +145,8 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count,
                      const double* mats, uint64_t mats_len,
                      const int32_t* edges, int32_t num_edges, int32_t fuse);
 /* Planner only, no device needed: first gate index of every pass the fused
- * program would launch (starts[0..min(cap, *npasses))). */
+ * program would launch (starts[0..min(cap, *npasses))).  QS_FUSE_FACTORED is
+ * planned as QS_FUSE_EXACT here (its rewrite needs the matrices). */
 int qs_plan_program(int32_t num_local_qubits, const qs_gate* gates, int32_t count, int32_t fuse,
                     int32_t* starts, int32_t cap, int32_t* npasses);
 /* Number of HBM passes the last qs_apply_program launched (planner output). */
