@@ -820,12 +820,12 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
         // tables follow the caller's table in one upload.  Programs where fewer
         // than half of the gates factor (noise trajectories) run exact: the
         // rewrite does not pay there.
-        factor_program(gates, count, mats, mats_len, st->m, st->num_states, num_edges, &fp);
+        uint64_t support = 0;
+        for (int e = 0; e < 2 * num_edges; ++e) support |= uint64_t(1) << edges[e];
+        factor_program(gates, count, mats, mats_len, st->m, st->num_states, num_edges, support, &fp);
         if (2 * fp.factored >= count) {
             all.assign(mats, mats + mats_len);
             all.insert(all.end(), fp.extra.begin(), fp.extra.end());
-            uint64_t support = 0;
-            for (int e = 0; e < 2 * num_edges; ++e) support |= uint64_t(1) << edges[e];
             static const bool reorder = getenv("QSB_NO_REORDER") == nullptr;
             if (reorder) schedule_program(fp.gates, st->m, support, all.data(), st->num_states);
             g_zero_off = fp.zero_off;

@@ -160,7 +160,7 @@ struct FactoredProgram {
 // Rewrites gates[0..count) (validated, all local) into `out`.  mats_len is the
 // size of the caller's table (the extra entries are appended after it).
 void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
-                    int num_states, int num_edges, FactoredProgram* out);
+                    int num_states, int num_edges, uint64_t phase_support, FactoredProgram* out);
 // Commutation-aware re-order of a factored program for the pass planner
 // (phase_support: the cut-phase graph's vertices).
 void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support,

@@ -100,7 +100,7 @@ bool decompose_2x2(const double* m, double out[10]) {
 }
 
 void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
-                    int num_states, int num_edges, FactoredProgram* out) {
+                    int num_states, int num_edges, uint64_t phase_support, FactoredProgram* out) {
     out->gates.clear();
     out->extra.clear();
     out->factored = 0;
@@ -189,9 +189,14 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             pending[q] = 1.0;
         }
     };
+    // a gate's matrix entries: the caller's table, or the extra entries (merged gates)
+    auto mat = [&](const qs_gate& g, int st) -> const double* {
+        const uint64_t off = g.offset + uint64_t(st) * g.stride;
+        return off >= mats_len ? out->extra.data() + (off - mats_len) : mats + off;
+    };
     auto diagonal_for_all_states = [&](const qs_gate& g) {
         for (int s = 0; s < num_states; ++s) {
-            const double* u = mats + g.offset + uint64_t(s) * g.stride;
+            const double* u = mat(g, s);
             if (u[2] != 0 || u[3] != 0 || u[4] != 0 || u[5] != 0) return false;
             if (g.stride == 0) break;
         }
@@ -225,7 +230,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         bool same = true;
         for (int st = 0; st < num_states; ++st) {
             double* f = fs.data() + 10 * st;
-            const double* u = mats + g.offset + uint64_t(st) * g.stride;
+            const double* u = mat(g, st);
             // RX(theta) = [[c, -is], [-is, c]] = c * diag(1, i) [[1,-t],[t,1]] diag(1, -i)
             // with t = -s/c: closed form (the QAOA mixer, 80 x 512 matrices a step)
             if (u[0] == u[6] && u[1] == 0 && u[7] == 0 && u[2] == 0 && u[4] == 0 && u[3] == u[5] &&
@@ -309,8 +314,83 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         return true;
     };
 
-    for (int i = 0; i < count; ++i) {
-        const qs_gate& g = gates[i];
+    // Gate fusion first: consecutive 1q gates on one qubit (nothing else on that
+    // qubit in between) become one matrix -- U2*U1, per state when either is --
+    // emitted where the qubit is next touched (or at the end).  A noise
+    // trajectory's rotation after each mixer RX then costs one shear, not two.
+    std::vector<qs_gate> prog;
+    {
+        struct Acc {
+            qs_gate g;
+            int n = 0;                    // original gates merged
+            std::vector<cd> m;            // 4 entries per state (1 state when shared)
+        };
+        std::vector<Acc> acc(m);
+        auto load = [&](const qs_gate& g, std::vector<cd>& dst) {
+            const int ns = g.stride ? num_states : 1;
+            dst.resize(4 * size_t(ns));
+            for (int st = 0; st < ns; ++st) {
+                const double* u = mats + g.offset + uint64_t(st) * g.stride;
+                for (int e = 0; e < 4; ++e) dst[4 * st + e] = cd(u[2 * e], u[2 * e + 1]);
+            }
+        };
+        auto emit_acc = [&](int q) {
+            Acc& a = acc[q];
+            if (a.n == 0) return;
+            if (a.n == 1) {
+                prog.push_back(a.g);
+            } else {
+                const int ns = int(a.m.size() / 4);
+                while (out->extra.size() % 2) out->extra.push_back(0.0);
+                qs_gate g = a.g;
+                g.offset = mats_len + out->extra.size();
+                g.stride = ns > 1 ? 8 : 0;
+                for (const cd& x : a.m) out->extra.push_back(x.real()), out->extra.push_back(x.imag());
+                prog.push_back(g);
+                out->factored += a.n - 1;  // the merged-away gates cost nothing
+            }
+            a.n = 0;
+            a.m.clear();
+        };
+        std::vector<cd> u2;
+        for (int i = 0; i < count; ++i) {
+            const qs_gate& g = gates[i];
+            if (g.kind == QS_KIND_1Q) {
+                Acc& a = acc[g.target];
+                if (a.n == 0) {
+                    a.g = g;
+                    load(g, a.m);
+                } else {
+                    load(g, u2);
+                    const int n1 = int(a.m.size() / 4), n2 = int(u2.size() / 4);
+                    const int ns = std::max(n1, n2);
+                    std::vector<cd> r(4 * size_t(ns));
+                    for (int st = 0; st < ns; ++st) {
+                        const cd* x = u2.data() + 4 * (n2 > 1 ? st : 0);    // later gate
+                        const cd* y = a.m.data() + 4 * (n1 > 1 ? st : 0);   // earlier gate
+                        r[4 * st + 0] = x[0] * y[0] + x[1] * y[2];
+                        r[4 * st + 1] = x[0] * y[1] + x[1] * y[3];
+                        r[4 * st + 2] = x[2] * y[0] + x[3] * y[2];
+                        r[4 * st + 3] = x[2] * y[1] + x[3] * y[3];
+                    }
+                    a.m.swap(r);
+                }
+                a.n++;
+                continue;
+            }
+            if (g.kind == QS_KIND_CTRL) {
+                emit_acc(g.target);
+                emit_acc(g.control);
+            } else {  // cut phase: every vertex of the graph
+                for (int q = 0; q < m; ++q)
+                    if ((phase_support >> q) & 1) emit_acc(q);
+            }
+            prog.push_back(g);
+        }
+        for (int q = 0; q < m; ++q) emit_acc(q);
+    }
+    for (size_t i = 0; i < prog.size(); ++i) {
+        const qs_gate g = prog[i];
         if (g.kind == QS_KIND_CUTPHASE) {  // diagonal: commutes with every pending diagonal
             out->gates.push_back(g);
             continue;
@@ -337,7 +417,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             }
             continue;
         }
-        const double* u = mats + g.offset;
+        const double* u = mat(g, 0);
         const cd u00 = entry(u, 0), u11 = entry(u, 3);
         if (entry(u, 1) == 0.0 && entry(u, 2) == 0.0 && std::abs(std::abs(u00) - 1.0) <= 1e-12 &&
             std::abs(std::abs(u11) - 1.0) <= 1e-12) {
