@@ -293,7 +293,9 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         double small = 1.0;
         for (int st = 0; st < num_states; ++st) {
             const double* f = fs.data() + 10 * st;
-            const double p[8] = {f[7], 0, has_pre ? 1.0 : 0.0, 0, pre.real(), pre.imag(), 0, 0};
+            // z is (1, 0) without a pre-diagonal: lean pool passes read it per state
+            const double p[8] = {f[7], 0, has_pre ? 1.0 : 0.0, 0, has_pre ? pre.real() : 1.0,
+                                 has_pre ? pre.imag() : 0.0, 0, 0};
             out->extra.insert(out->extra.end(), p, p + 8);
             Ks[st] *= cd(f[0], f[1]) * f[8];
             small = std::min(small, std::abs(Ks[st]));
@@ -452,7 +454,8 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         bool has_pre = false;
         if (!mixed[q]) din[q] *= pre;
         else has_pre = pre != 1.0;
-        const double p[8] = {f[7], f[6], has_pre ? 1.0 : 0.0, 0, pre.real(), pre.imag(), 0, 0};
+        const double p[8] = {f[7], f[6], has_pre ? 1.0 : 0.0, 0, has_pre ? pre.real() : 1.0,
+                             has_pre ? pre.imag() : 0.0, 0, 0};
         emit(kKindShear, q, params(p));
         out->factored++;
         pending[q] = za;
@@ -472,9 +475,13 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
     if (any_out) out->gates.push_back(diag_tables(pending, K));
     for (int q = 0; q < m; ++q)  // per-state pending diagonals close the program
         if (!psp[q].empty()) per_state_rows(kKindDiag1, q, {}, psp[q], true);
+    // padding row of the lean pool passes: t = 0, z = (1, 0)
+    while (out->extra.size() % 2) out->extra.push_back(0.0);
     out->zero_off = mats_len + out->extra.size();
-    out->extra.push_back(0.0);
-    out->extra.push_back(0.0);
+    {
+        const double pad[8] = {0, 0, 0, 0, 1, 0, 0, 0};
+        out->extra.insert(out->extra.end(), pad, pad + 8);
+    }
     if (per_state_k) {
         // the per-state scalars ride on a cut phase when the program has one
         // (each state's LUT row times its scalar: no extra pass op)

@@ -801,7 +801,12 @@ __device__ __forceinline__ void fact_shear(double2 (&a)[kRegAmps], const FactRou
                                            const double* __restrict__ mats, uint64_t st) {
     const double t = TABLES ? __ldg(mats + F.toff[grp][J] + st * F.tstride[grp][J]) : F.t[grp][J];
     if (PRE) {
-        const double2 z = F.pre[grp][J];
+        // pool passes read the state's pre-diagonal from its row (per-state
+        // diagonals of noise trajectories; (1, 0) where there is none)
+        const double2 z =
+            TABLES ? __ldg(reinterpret_cast<const double2*>(mats + F.toff[grp][J] +
+                                                            st * F.tstride[grp][J] + 4))
+                   : F.pre[grp][J];
 #pragma unroll
         for (int k = 0; k < kRegAmps; ++k)
             if ((k >> J) & 1) a[k] = cmul(a[k], z);
@@ -1128,7 +1133,6 @@ bool fact_pass_from(const TilePass& T, FactPass* F, bool* tables, bool* phase) {
             const int n = FR.n[grp];
             if (G.kind != kKindShear || G.variant != n || n >= kRegLog2) return false;
             if (G.u[0].y != 0.0) return false;  // only form A shears exist
-            if (G.pad[1] != 0) return false;     // per-state pre-diagonals: k_tile
             FR.t[grp][n] = G.u[0].x;
             if (G.u[1].x != 0.0) {  // pre-diagonal (shared by construction for per-state t)
                 FR.pre_any = 1;
@@ -1138,6 +1142,7 @@ bool fact_pass_from(const TilePass& T, FactPass* F, bool* tables, bool* phase) {
             FR.toff[grp][n] = G.offset;
             FR.tstride[grp][n] = uint32_t(G.stride);
             FR.n[grp]++;
+            if (G.pad[1] != 0) *tables = true;  // per-state pre-diagonals: read per state
         }
     }
     if (*tables) {
