@@ -110,6 +110,12 @@ int qs_init_constant(qs_state* st, double re, double im);           /* init_unif
  * index): identical for any rank split (not the numpy stream; unnormalised). */
 int qs_init_gaussian(qs_state* st, uint64_t seed);
 int qs_scale(qs_state* st, double factor);
+/* apply_diagonal_phase with an arbitrary phase function (statevector.py:
+ * 198-206): the caller evaluates exp(-1j * phases(owned_indices)) on the host
+ * (the reference's own numpy expression) and passes the complex factors of
+ * amplitudes [offset, offset + count); the device multiplies them in with
+ * numpy's complex product.  Staged through device scratch in chunks. */
+int qs_apply_diagonal(qs_state* st, const double* factors, uint64_t offset, uint64_t count);
 
 /* ---- gates ------------------------------------------------------------- */
 /* apply_local_one_qubit_gate (statevector.py:162-177), one matrix per state
@@ -209,6 +215,21 @@ int qs_exchange_gate_nccl(qs_state* st, int32_t peer_rank, int32_t is_lower,
 int qs_swap_qubits_peer(qs_state* st, void* peer_amps, int32_t local_qubit, int32_t rank_bit);
 int qs_swap_qubits_local(qs_state* st, int32_t a, int32_t c);
 /* CUDA IPC for peer mapping across processes (64-byte handles). */
+/* Cross-rank ordering of peer exchange kernels without host stream syncs
+ * (distribution._ordered_peer_op): every handle has two interprocess events
+ * (0: recorded before its exchange, 1: after).  A rank records its own, the
+ * pair meets on the host, and each stream waits on the partner's event, so the
+ * exchange queues behind the local passes and the host never blocks.
+ * qs_sync_event hands out the event itself (partner in the same process),
+ * qs_sync_event_ipc its 64-byte IPC handle, qs_sync_event_open opens a
+ * partner's handle (closed with the state).  qs_stream_busy: 1 while the
+ * handle's stream still has queued work (cudaStreamQuery). */
+int qs_sync_event(qs_state* st, int32_t which, void** ev);
+int qs_sync_event_ipc(qs_state* st, int32_t which, unsigned char* handle64);
+int qs_sync_event_open(qs_state* st, const unsigned char* handle64, void** ev);
+int qs_sync_event_record(qs_state* st, int32_t which);
+int qs_stream_wait_event(qs_state* st, void* ev);
+int qs_stream_busy(qs_state* st, int32_t* busy);
 int qs_state_ipc_handle(const qs_state* st, unsigned char* handle64);
 int qs_peer_open(qs_state* st, const unsigned char* handle64, void** peer_amps);
 int qs_peer_close(qs_state* st, void* peer_amps);

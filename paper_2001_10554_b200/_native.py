@@ -26,6 +26,7 @@ EXPORTS = (
     "qs_state_create", "qs_state_destroy", "qs_state_info", "qs_state_device_ptr",
     "qs_synchronize", "qs_state_upload", "qs_state_download", "qs_state_exchange_host",
     "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
+    "qs_apply_diagonal",
     "qs_apply_1q", "qs_apply_controlled", "qs_apply_cut_phase", "qs_apply_program",
     "qs_plan_program", "qs_last_program_passes", "qs_observable", "qs_marginals",
     "qs_exchange_gate_peer", "qs_exchange_gate_nccl", "qs_swap_qubits_peer",
@@ -33,6 +34,8 @@ EXPORTS = (
     "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
     "qs_event_record", "qs_event_elapsed_ms", "qs_launch_log", "qs_launch_log_read",
     "qs_compose_2x2", "qs_philox4x64", "qs_decompose_2x2",
+    "qs_sync_event", "qs_sync_event_ipc", "qs_sync_event_open", "qs_sync_event_record",
+    "qs_stream_wait_event", "qs_stream_busy",
 )
 
 
@@ -86,6 +89,7 @@ _SIGNATURES = {
     "qs_init_constant": ([_P, _D, _D], ctypes.c_int),
     "qs_init_gaussian": ([_P, _U], ctypes.c_int),
     "qs_scale": ([_P, _D], ctypes.c_int),
+    "qs_apply_diagonal": ([_P, _DP, _U, _U], ctypes.c_int),
     "qs_apply_1q": ([_P, _I, _DP, _U], ctypes.c_int),
     "qs_apply_controlled": ([_P, _I, _I, _DP, _U], ctypes.c_int),
     "qs_apply_cut_phase": ([_P, _IP, _I, _DP, _U], ctypes.c_int),
@@ -105,6 +109,12 @@ _SIGNATURES = {
     "qs_peer_open": ([_P, _BP, ctypes.POINTER(_P)], ctypes.c_int),
     "qs_peer_close": ([_P, _P], ctypes.c_int),
     "qs_nccl_unique_id": ([_BP], ctypes.c_int),
+    "qs_sync_event": ([_P, _I, ctypes.POINTER(_P)], ctypes.c_int),
+    "qs_sync_event_ipc": ([_P, _I, _BP], ctypes.c_int),
+    "qs_sync_event_open": ([_P, _BP, ctypes.POINTER(_P)], ctypes.c_int),
+    "qs_sync_event_record": ([_P, _I], ctypes.c_int),
+    "qs_stream_wait_event": ([_P, _P], ctypes.c_int),
+    "qs_stream_busy": ([_P, _IP], ctypes.c_int),
     "qs_comm_init": ([_P, _BP, _I, _I], ctypes.c_int),
     "qs_comm_destroy": ([_P], ctypes.c_int),
     "qs_event_record": ([_P, _I], ctypes.c_int),
@@ -254,9 +264,17 @@ class DeviceState:
             pass
 
     # ---- data movement --------------------------------------------------------
+    uploads = 0  # amplitudes uploaded through this handle (host -> device)
+
     def upload(self, amps: np.ndarray, offset: int = 0) -> None:
         a = np.ascontiguousarray(amps, dtype=np.complex128).ravel()
         call("qs_state_upload", self.handle, dptr(a), offset, a.size)
+        self.uploads += a.size
+
+    def apply_diagonal(self, factors: np.ndarray, offset: int = 0) -> None:
+        """psi[offset:offset+len] *= factors (qs_apply_diagonal)."""
+        f = np.ascontiguousarray(factors, dtype=np.complex128).ravel()
+        call("qs_apply_diagonal", self.handle, dptr(f), offset, f.size)
 
     def download(self, out: np.ndarray | None = None, offset: int = 0,
                  count: int | None = None) -> np.ndarray:
@@ -271,6 +289,7 @@ class DeviceState:
     def exchange_host(self, host_in: np.ndarray, host_out: np.ndarray, chunk: int = 1 << 24) -> None:
         """Download into host_out while uploading host_in (full duplex, chunked)."""
         call("qs_state_exchange_host", self.handle, dptr(host_in), dptr(host_out), chunk)
+        self.uploads += host_in.size
 
     def synchronize(self) -> None:
         call("qs_synchronize", self.handle)
@@ -279,6 +298,34 @@ class DeviceState:
         p = _P()
         call("qs_state_device_ptr", self.handle, ctypes.byref(p))
         return p.value
+
+    # ---- cross-rank ordering (qs_sync_event*) ------------------------------------
+    def sync_event(self, which: int) -> int:
+        p = _P()
+        call("qs_sync_event", self.handle, which, ctypes.byref(p))
+        return p.value
+
+    def sync_event_ipc(self, which: int) -> bytes:
+        buf = (ctypes.c_ubyte * 64)()
+        call("qs_sync_event_ipc", self.handle, which, buf)
+        return bytes(buf)
+
+    def open_sync_event(self, handle64: bytes) -> int:
+        buf = (ctypes.c_ubyte * 64).from_buffer_copy(handle64)
+        p = _P()
+        call("qs_sync_event_open", self.handle, buf, ctypes.byref(p))
+        return p.value
+
+    def record_sync_event(self, which: int) -> None:
+        call("qs_sync_event_record", self.handle, which)
+
+    def wait_event(self, ev: int) -> None:
+        call("qs_stream_wait_event", self.handle, ctypes.c_void_p(ev))
+
+    def busy(self) -> bool:
+        b = ctypes.c_int32(0)
+        call("qs_stream_busy", self.handle, ctypes.byref(b))
+        return bool(b.value)
 
     def counters(self) -> tuple[int, int]:
         msgs, amps = ctypes.c_uint64(0), ctypes.c_uint64(0)

@@ -95,29 +95,41 @@ class Circuit:
                 "unbound parameter slot(s): " + ", ".join("$" + s for s in self.slots))
 
 
-def build_qaoa_circuit(graph, depth: int) -> Circuit:
+def gamma_slot(k: int) -> str:
+    """Slot name of layer k's cost angle (circuit.py:240-241)."""
+    return f"gamma{k}"
+
+
+def beta_slot(k: int) -> str:
+    """Slot name of layer k's mixer angle (circuit.py:244-245)."""
+    return f"beta{k}"
+
+
+def build_qaoa_circuit(graph, depth: int, graph_path: str | None = None) -> Circuit:
     """H on every qubit, then per layer k: cut phase with slot gamma_k and RX
-    mixers with slot beta_k on every qubit (same sequence as the reference)."""
+    mixers with slot beta_k on every qubit (circuit.py:248-264, same gate
+    sequence); `graph_path` is kept on the cost gates for serialisation."""
     if depth < 1:
         raise ValueError("depth must be >= 1")
     n = graph.num_vertices
     gates = [GateSpec("h", (q,)) for q in range(n)]
     for k in range(1, depth + 1):
-        gates.append(GateSpec("diagcost", (), f"$gamma{k}", graph=graph))
-        gates.extend(GateSpec("rx", (q,), f"$beta{k}") for q in range(n))
+        gates.append(GateSpec("diagcost", (), "$" + gamma_slot(k), graph=graph,
+                              graph_path=graph_path))
+        gates.extend(GateSpec("rx", (q,), "$" + beta_slot(k)) for q in range(n))
     return Circuit(n, tuple(gates))
 
 
 def qaoa_bindings(depth: int, position) -> dict:
     """(gamma_1..gamma_p, beta_1..beta_p) -> slot values; betas doubled so the
-    RX mixer realises RX(2 beta)."""
+    RX mixer realises RX(2 beta) (circuit.py:267-279)."""
     position = np.asarray(position, dtype=np.float64)
     if position.shape != (2 * depth,):
         raise ValueError(f"expected {2 * depth} parameters, got shape {position.shape}")
     out = {}
     for k in range(1, depth + 1):
-        out[f"gamma{k}"] = float(position[k - 1])
-        out[f"beta{k}"] = 2.0 * float(position[depth + k - 1])
+        out[gamma_slot(k)] = float(position[k - 1])
+        out[beta_slot(k)] = 2.0 * float(position[depth + k - 1])
     return out
 
 

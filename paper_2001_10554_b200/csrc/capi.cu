@@ -145,6 +145,12 @@ struct qs_state {
     // accounting (TransportCounters analogue)
     uint64_t messages = 0, amplitudes = 0;
     int32_t last_passes = 0;
+    // cross-rank ordering of exchange kernels (qs_sync_event*): interprocess
+    // events recorded before / after an exchange; peer events opened here
+    cudaEvent_t sync_ev[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> opened_ev;
+    // NCCL exchange pipeline events, created once
+    cudaEvent_t nccl_ev[6] = {};
     // timing
     cudaEvent_t ev[8] = {};
     bool launch_log = false;
@@ -646,6 +652,11 @@ int qs_state_destroy(qs_state* st) {
     for (auto& r : st->recs) cudaEventDestroy(r.start), cudaEventDestroy(r.stop);
     for (auto& ev : st->ev)
         if (ev) cudaEventDestroy(ev);
+    for (auto& ev : st->sync_ev)
+        if (ev) cudaEventDestroy(ev);
+    for (auto& ev : st->nccl_ev)
+        if (ev) cudaEventDestroy(ev);
+    for (auto ev : st->opened_ev) cudaEventDestroy(ev);
     cudaFree(st->psi);
     cudaFree(st->d_mats);
     cudaFree(st->d_pass);
@@ -790,6 +801,29 @@ int qs_scale(qs_state* st, double factor) {
     if (int rc = ensure_device(st)) return rc;
     launch_scale(st->psi, st->amps_per_state * uint64_t(st->num_states), factor, st->stream);
     CHECK_LAUNCH();
+    return QS_OK;
+}
+
+int qs_apply_diagonal(qs_state* st, const double* factors, uint64_t offset, uint64_t count) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (int rc = ensure_device(st)) return rc;
+    const uint64_t total = st->amps_per_state * uint64_t(st->num_states);
+    if (offset > total || count > total - offset)
+        return fail(QS_ERR_VALUE, "diagonal range beyond the state");
+    if (count == 0) return QS_OK;
+    if (!factors) return fail(QS_ERR_VALUE, "factors is NULL");
+    const uint64_t chunk = std::min<uint64_t>(count, uint64_t(1) << 22);
+    if (int rc = grow(&st->d_scratch, &st->scratch_cap, size_t(2 * chunk))) return rc;
+    for (uint64_t done = 0; done < count; done += chunk) {
+        const uint64_t k = std::min(chunk, count - done);
+        CUDA_TRY(cudaMemcpyAsync(st->d_scratch, factors + 2 * done, k * sizeof(double2),
+                                 cudaMemcpyHostToDevice, st->stream));
+        launch_mul_factors(st->psi + offset + done, reinterpret_cast<const double2*>(st->d_scratch),
+                           k, st->stream);
+        CHECK_LAUNCH();
+    }
+    // the host buffer may be released when we return
+    CUDA_TRY(cudaStreamSynchronize(st->stream));
     return QS_OK;
 }
 
@@ -1111,7 +1145,7 @@ int qs_exchange_gate_peer(qs_state* st, void* peer_amps, int32_t is_lower, const
     uint64_t moved = st->amps_per_state >> (control_local >= 0 ? 1 : 0);
     st->messages += 2;
     st->amplitudes += moved;
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    // no host sync: the caller orders the partner's work with qs_sync_event*
     return QS_OK;
 }
 
@@ -1131,7 +1165,6 @@ int qs_swap_qubits_peer(qs_state* st, void* peer_amps, int32_t local_qubit, int3
     CHECK_LAUNCH();
     st->messages += 2;
     st->amplitudes += st->amps_per_state >> 1;
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
     return QS_OK;
 }
 
@@ -1226,12 +1259,12 @@ int qs_exchange_gate_nccl(qs_state* st, int32_t peer, int32_t is_lower, const do
     double2* outbound = is_lower ? st->psi + half : st->psi;
     const uint64_t mine_first = is_lower ? 0 : half;
     const uint64_t nchunks = (half + c - 1) / c;
-    cudaEvent_t ev_in[2], ev_done[2], ev_start;
-    for (int k = 0; k < 2; ++k) {
-        CUDA_TRY(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming));
-        CUDA_TRY(cudaEventCreateWithFlags(&ev_done[k], cudaEventDisableTiming));
-    }
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+    // the pipeline's events live with the handle (created on first use)
+    for (auto& ev : st->nccl_ev)
+        if (!ev) CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaEvent_t* ev_in = st->nccl_ev;
+    cudaEvent_t* ev_done = st->nccl_ev + 2;
+    cudaEvent_t ev_start = st->nccl_ev[4], ev_end = st->nccl_ev[5];
     CUDA_TRY(cudaEventRecord(ev_start, st->stream));
     CUDA_TRY(cudaStreamWaitEvent(st->comm_stream, ev_start, 0));
     const size_t dbl = 2;  // doubles per amplitude
@@ -1274,14 +1307,81 @@ int qs_exchange_gate_nccl(qs_state* st, int32_t peer, int32_t is_lower, const do
             CUDA_TRY(cudaEventRecord(ev_done[k & 1], st->stream));
         }
     }
-    cudaEvent_t ev_end;
-    CUDA_TRY(cudaEventCreateWithFlags(&ev_end, cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(ev_end, st->comm_stream));
     CUDA_TRY(cudaStreamWaitEvent(st->stream, ev_end, 0));
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
-    for (int k = 0; k < 2; ++k) cudaEventDestroy(ev_in[k]), cudaEventDestroy(ev_done[k]);
-    cudaEventDestroy(ev_start);
-    cudaEventDestroy(ev_end);
+    // stream-ordered: the next kernels on st->stream follow the exchange
+    return QS_OK;
+}
+
+// ---- cross-rank ordering without host syncs ---------------------------------
+namespace {
+int make_sync_events(qs_state* st) {
+    for (auto& ev : st->sync_ev)
+        if (!ev)
+            CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess));
+    return QS_OK;
+}
+}  // namespace
+
+int qs_sync_event(qs_state* st, int32_t which, void** ev) {
+    if (!st || !ev) return fail(QS_ERR_VALUE, "null argument");
+    if (which < 0 || which > 1) return fail(QS_ERR_VALUE, "sync event %d out of range", which);
+    if (int rc = ensure_device(st)) return rc;
+    if (int rc = make_sync_events(st)) return rc;
+    *ev = reinterpret_cast<void*>(st->sync_ev[which]);
+    return QS_OK;
+}
+
+int qs_sync_event_ipc(qs_state* st, int32_t which, unsigned char* handle64) {
+    if (!st || !handle64) return fail(QS_ERR_VALUE, "null argument");
+    if (which < 0 || which > 1) return fail(QS_ERR_VALUE, "sync event %d out of range", which);
+    if (int rc = ensure_device(st)) return rc;
+    if (int rc = make_sync_events(st)) return rc;
+    cudaIpcEventHandle_t h;
+    CUDA_TRY(cudaIpcGetEventHandle(&h, st->sync_ev[which]));
+    static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
+    memcpy(handle64, &h, 64);
+    return QS_OK;
+}
+
+int qs_sync_event_open(qs_state* st, const unsigned char* handle64, void** ev) {
+    if (!st || !handle64 || !ev) return fail(QS_ERR_VALUE, "null argument");
+    if (int rc = ensure_device(st)) return rc;
+    cudaIpcEventHandle_t h;
+    memcpy(&h, handle64, 64);
+    cudaEvent_t e;
+    CUDA_TRY(cudaIpcOpenEventHandle(&e, h));
+    st->opened_ev.push_back(e);
+    *ev = reinterpret_cast<void*>(e);
+    return QS_OK;
+}
+
+int qs_sync_event_record(qs_state* st, int32_t which) {
+    if (!st) return fail(QS_ERR_VALUE, "null state");
+    if (which < 0 || which > 1) return fail(QS_ERR_VALUE, "sync event %d out of range", which);
+    if (int rc = ensure_device(st)) return rc;
+    if (int rc = make_sync_events(st)) return rc;
+    CUDA_TRY(cudaEventRecord(st->sync_ev[which], st->stream));
+    return QS_OK;
+}
+
+int qs_stream_wait_event(qs_state* st, void* ev) {
+    if (!st || !ev) return fail(QS_ERR_VALUE, "null argument");
+    if (int rc = ensure_device(st)) return rc;
+    CUDA_TRY(cudaStreamWaitEvent(st->stream, reinterpret_cast<cudaEvent_t>(ev), 0));
+    return QS_OK;
+}
+
+int qs_stream_busy(qs_state* st, int32_t* busy) {
+    if (!st || !busy) return fail(QS_ERR_VALUE, "null argument");
+    if (int rc = ensure_device(st)) return rc;
+    cudaError_t e = cudaStreamQuery(st->stream);
+    if (e == cudaErrorNotReady) {
+        *busy = 1;
+        return QS_OK;
+    }
+    CUDA_TRY(e);
+    *busy = 0;
     return QS_OK;
 }
 

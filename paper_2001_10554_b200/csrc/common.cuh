@@ -185,6 +185,7 @@ void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s);
 void launch_gaussian(double2* psi, uint64_t count_per_state, int num_states, uint64_t rank_offset,
                      uint64_t seed, cudaStream_t s);
 void launch_scale(double2* psi, uint64_t count, double factor, cudaStream_t s);
+void launch_mul_factors(double2* psi, const double2* f, uint64_t count, cudaStream_t s);
 
 // Observables: per-state tree sums.  `scratch` must hold at least
 // reduce_scratch_doubles(m, num_states) doubles.

@@ -407,6 +407,35 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             continue;
         }
         // QS_KIND_1Q
+        if (g.stride != 0 && diagonal_for_all_states(g)) {
+            // per-state diagonal gate (per-state RZ(gamma_s), pure-dephasing
+            // noise, fused products that come out diagonal): u_s = u00_s *
+            // diag(1, u11_s / u00_s) -- the scalar joins the per-state scalars,
+            // the diagonal the per-state pending diagonal of q (it commutes with
+            // everything pending there).  Non-unitary diagonals run exact.
+            bool unit_all = true;
+            for (int st = 0; st < num_states && unit_all; ++st) {
+                const double* u = mat(g, st);
+                unit_all = std::abs(std::abs(entry(u, 0)) - 1.0) <= 1e-12 &&
+                           std::abs(std::abs(entry(u, 3)) - 1.0) <= 1e-12;
+            }
+            if (!unit_all) {
+                out->gates.push_back(g);  // diagonal: no flush needed
+                continue;
+            }
+            std::vector<cd> z(num_states);
+            for (int st = 0; st < num_states; ++st) {
+                const double* u = mat(g, st);
+                const cd u00 = entry(u, 0), u11 = entry(u, 3);
+                z[st] = (psp[q].empty() ? pending[q] : psp[q][st]) * (u11 / u00);
+                Ks[st] *= u00;
+            }
+            psp[q].swap(z);
+            pending[q] = 1.0;
+            per_state_k = true;
+            out->factored++;
+            continue;
+        }
         if (g.stride != 0) {
             // per-state matrices (pool mode): a per-state shear when every
             // state's matrix factors with the same diagonals (e.g. the QAOA
@@ -541,7 +570,9 @@ void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support
         switch (g.kind) {
             case QS_KIND_CUTPHASE: dia[i] = phase_support; break;
             case kKindDiagN: dia[i] = all; break;
-            case kKindScalar: break;
+            // a mid-program rescale must stay between the shears around it
+            // (pulled forward, the product of several would underflow)
+            case kKindScalar: dia[i] = all; break;
             case kKindDiag1: dia[i] = t; break;
             case kKindShear: mix[i] = t; break;
             case QS_KIND_CTRL:

@@ -1400,6 +1400,20 @@ void launch_scale(double2* psi, uint64_t count, double factor, cudaStream_t s) {
     k_scale<<<stream_grid(count), 256, 0, s>>>(psi, count, factor);
 }
 
+// psi_i *= f_i with numpy's complex product (psi the left operand), the
+// reference's `partition.amplitudes *= np.exp(-1j * angles)`
+// (statevector.py:198-206) for a host-evaluated phase function.
+__global__ void k_mul_factors(double2* __restrict__ psi, const double2* __restrict__ f,
+                              uint64_t count) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        psi[i] = cmul(psi[i], f[i]);
+}
+
+void launch_mul_factors(double2* psi, const double2* f, uint64_t count, cudaStream_t s) {
+    k_mul_factors<<<stream_grid(count), 256, 0, s>>>(psi, f, count);
+}
+
 void launch_gaussian(double2* psi, uint64_t per_state, int num_states, uint64_t rank_offset,
                      uint64_t seed, cudaStream_t s) {
     int m = 0;

@@ -13,33 +13,29 @@ chunked, double-buffered NCCL send/recv with the step-2 update pipelined
 against the transfers.
 
 Communicators (all collective calls in the same order on every rank, as the
-reference requires):
-  * ``single_rank_comm()``      one rank, no peers
-  * ``ThreadFabric(P)``          P ranks as threads of one process (the
-                                 reference's run_spmd model); partitions may
-                                 live on one device (emulated ranks) or on
-                                 several
-  * ``TorchComm(...)``           one process per GPU over torch.distributed
-                                 (control plane) + CUDA IPC peer mappings
+reference requires): ``GroupComm(transport, base_rank, size)`` is the
+reference's group-relative view of a world endpoint (transport.py):
+  * ``single_rank_comm()``           one rank, no peers
+  * ``InProcessFabric(P)`` endpoints P ranks as threads of one process (the
+                                     reference's run_spmd model); partitions
+                                     may live on one device (emulated ranks)
+                                     or on several
+  * ``TorchTransport()``             one process per GPU over
+                                     torch.distributed (control plane) + CUDA
+                                     IPC peer mappings and events
 """
 from __future__ import annotations
 
-import threading
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _native
 from . import statevector as sv
+from .transport import (InProcessFabric, TorchTransport, TransportError,  # noqa: F401
+                        TransportTimeout)
 
 DEFAULT_CHUNK_AMPLITUDES = 1 << 26
-
-
-class TransportTimeout(TimeoutError):
-    """A collective partner never showed up (reference transport.py:41-42)."""
-
-
-TransportError = _native.TransportError
 
 
 @dataclass(frozen=True)
@@ -128,208 +124,136 @@ def route_controlled(rank: int, topology: RankTopology, control: int, target: in
 
 # ---- communicators ----------------------------------------------------------------
 class GroupComm:
-    """Group-relative communicator for one distributed state."""
+    """Group-relative view of a world endpoint for one state group
+    (distribution.py:75-98): group ranks are the world ranks
+    [base_rank, base_rank + size) and every peer is addressed group-relative.
 
-    rank: int = 0
-    size: int = 1
-    exchange_mode: str = "peer"
+    Beyond the reference's send/receive it carries the device plane of the
+    exchange: pairwise handshakes that order one rank's exchange kernel after
+    its partner's earlier work through CUDA events (no host stream sync),
+    rank-ordered scalar gathers, and the partner's peer-memory pointer."""
+
+    def __init__(self, transport, base_rank: int, size: int):
+        if size > 1 and transport is None:
+            raise ValueError("multi-rank group needs a transport")
+        self.transport = transport
+        self.base_rank = base_rank
+        self.size = size
+        self.rank = 0 if transport is None else transport.rank - base_rank
+        if not (0 <= self.rank < size):
+            raise ValueError(
+                f"world rank {transport.rank} outside group [{base_rank}, {base_rank + size})")
+        self.exchange_mode = getattr(transport, "exchange_mode", "peer")
+
+    # the reference's point-to-point calls
+    def send(self, dest: int, payload, tag: int = 0) -> None:
+        self.transport.send(self.base_rank + dest, payload, tag=tag)
+
+    def receive(self, src: int):
+        return self.transport.receive(self.base_rank + src)
+
+    # device plane
+    def _need_peers(self) -> None:
+        if self.transport is None or self.size == 1:
+            raise TransportError("single-rank communicator has no peers")
 
     def pair_barrier(self, partner: int) -> None:
-        raise NotImplementedError
+        self._need_peers()
+        self.transport._dp_pair_barrier(self.base_rank + self.rank, self.base_rank + partner)
 
     def allgather(self, value: float, participants: int) -> list:
-        """Values of ranks [0, participants) in rank order (caller is one of them)."""
-        raise NotImplementedError
+        """Values of group ranks [0, participants) in rank order (the caller is one)."""
+        if self.transport is None or participants == 1:
+            return [float(value)]
+        return self.transport._dp_allgather(value, self.base_rank, participants)
 
     def attach(self, partition) -> None:
-        """Collective: make this rank's partition reachable by its peers."""
+        """Collective over the world endpoint: make this rank's partition reachable."""
+        if self.transport is not None:
+            self.transport._dp_attach(partition)
 
     def peer_pointer(self, partner: int) -> int:
-        raise NotImplementedError
+        self._need_peers()
+        return self.transport._dp_peer_pointer(self.base_rank + partner)
+
+    def peer_events(self, partner: int) -> tuple:
+        self._need_peers()
+        return self.transport._dp_peer_events(self.base_rank + partner)
 
     def nccl_peer(self, partner: int) -> int:
         return partner
 
-
-class _SingleComm(GroupComm):
-    def pair_barrier(self, partner: int) -> None:
-        raise TransportError("single-rank communicator has no peers")
-
-    def allgather(self, value: float, participants: int) -> list:
-        return [float(value)]
+    def account_exchange(self, messages: int, amplitudes: int) -> None:
+        """Count an exchange in the reference's TransportCounters terms."""
+        if self.transport is not None:
+            self.transport.counters.messages_sent += messages
+            self.transport.counters.amplitudes_sent += amplitudes
 
 
 def single_rank_comm() -> GroupComm:
-    return _SingleComm()
+    return GroupComm(None, 0, 1)
 
 
-class ThreadFabric:
-    """P ranks as threads of one process, like the reference's InProcessFabric
-    + run_spmd (transport.py:118-154, runtime.py:261-288).  Partitions may sit
-    on one GPU (emulated ranks: the exchange kernel of each rank touches a
-    disjoint pair set, so no kernel ever waits on another) or on several."""
-
-    def __init__(self, size: int, timeout: float = 30.0, exchange_mode: str = "peer"):
-        self.size = size
-        self.timeout = timeout
-        self.exchange_mode = exchange_mode
-        self._lock = threading.Lock()
-        self._pair: dict = {}
-        self._gather: dict = {}
-        self._parts: dict = {}
-
-    def endpoint(self, rank: int) -> "ThreadComm":
-        return ThreadComm(self, rank)
-
-    def _barrier(self, key, parties: int) -> threading.Barrier:
-        with self._lock:
-            b = self._pair.get(key)
-            if b is None:
-                b = self._pair[key] = threading.Barrier(parties)
-            return b
+def world_comm(transport) -> GroupComm:
+    """The whole world as one group (a transport, a GroupComm, or None)."""
+    if isinstance(transport, GroupComm):
+        return transport
+    if transport is None:
+        return single_rank_comm()
+    return GroupComm(transport, 0, transport.world_size)
 
 
-class ThreadComm(GroupComm):
-    def __init__(self, fabric: ThreadFabric, rank: int):
-        self.fabric = fabric
-        self.rank = rank
-        self.size = fabric.size
-        self.exchange_mode = fabric.exchange_mode
-
-    def _wait(self, barrier: threading.Barrier) -> None:
-        try:
-            barrier.wait(timeout=self.fabric.timeout)
-        except threading.BrokenBarrierError:
-            raise TransportTimeout(f"rank {self.rank}: partner never arrived") from None
-
-    def pair_barrier(self, partner: int) -> None:
-        key = ("pair", min(self.rank, partner), max(self.rank, partner))
-        self._wait(self.fabric._barrier(key, 2))
-
-    def allgather(self, value: float, participants: int) -> list:
-        f = self.fabric
-        b = f._barrier(("gather", participants), participants)
-        with f._lock:
-            f._gather.setdefault(participants, {})[self.rank] = float(value)
-        self._wait(b)
-        with f._lock:
-            vals = [f._gather[participants][r] for r in range(participants)]
-        self._wait(b)
-        return vals
-
-    def attach(self, partition) -> None:
-        with self.fabric._lock:
-            self.fabric._parts[self.rank] = partition
-
-    def peer_pointer(self, partner: int) -> int:
-        with self.fabric._lock:
-            part = self.fabric._parts.get(partner)
-        if part is None:
-            raise TransportError(f"rank {partner} has no attached partition")
-        return part.state.device_ptr()
-
-
-class TorchComm(GroupComm):
-    """One process per GPU.  torch.distributed carries the control plane
-    (barriers, scalar gathers, IPC handles; any backend -- gloo works on
-    CPU); the data plane is the peer kernel over CUDA IPC mappings or NCCL
-    inside libqsb200."""
-
-    def __init__(self, group=None, exchange_mode: str = "peer"):
-        import torch.distributed as dist
-
-        self.dist = dist
-        self.group = group
-        self.rank = dist.get_rank(group)
-        self.size = dist.get_world_size(group)
-        self.exchange_mode = exchange_mode
-        self._handles: list | None = None
-        self._peers: dict = {}
-        self._state = None
-
-    def _global(self, r: int) -> int:
-        return r if self.group is None else self.dist.get_global_rank(self.group, r)
-
-    def pair_barrier(self, partner: int) -> None:
-        import torch
-
-        t = torch.zeros(1)
-        g = self._global(partner)
-        if self.rank < partner:
-            self.dist.send(t, g, group=self.group)
-            self.dist.recv(t, g, group=self.group)
-        else:
-            self.dist.recv(t, g, group=self.group)
-            self.dist.send(t, g, group=self.group)
-
-    def allgather(self, value: float, participants: int) -> list:
-        import torch
-
-        # every group member joins the gather; ranks beyond `participants`
-        # contribute nothing and the caller ignores them
-        t = torch.tensor([float(value)], dtype=torch.float64)
-        out = [torch.zeros(1, dtype=torch.float64) for _ in range(self.size)]
-        self.dist.all_gather(out, t, group=self.group)
-        return [float(x.item()) for x in out[:participants]]
-
-    def attach(self, partition) -> None:
-        import ctypes
-
-        self._state = partition.state if partition is not None else None
-        mine = b""
-        if self._state is not None:
-            buf = (ctypes.c_ubyte * 64)()
-            _native.call("qs_state_ipc_handle", self._state.handle, buf)
-            mine = bytes(buf)
-        handles = [None] * self.size
-        self.dist.all_gather_object(handles, mine, group=self.group)
-        self._handles = handles
-        if self.exchange_mode == "nccl" and self._state is not None:
-            ident = [None]
-            if self.rank == 0:
-                buf = (ctypes.c_ubyte * 128)()
-                _native.call("qs_nccl_unique_id", buf)
-                ident = [bytes(buf)]
-            self.dist.broadcast_object_list(ident, src=self._global(0), group=self.group)
-            idb = (ctypes.c_ubyte * 128).from_buffer_copy(ident[0])
-            _native.call("qs_comm_init", self._state.handle, idb, self.size, self.rank)
-
-    def peer_pointer(self, partner: int) -> int:
-        import ctypes
-
-        if partner not in self._peers:
-            if not self._handles or not self._handles[partner]:
-                raise TransportError(f"rank {partner} has no attached partition")
-            buf = (ctypes.c_ubyte * 64).from_buffer_copy(self._handles[partner])
-            p = ctypes.c_void_p()
-            _native.call("qs_peer_open", self._state.handle, buf, ctypes.byref(p))
-            self._peers[partner] = p.value
-        return self._peers[partner]
+# Names of round 1, kept for callers: the thread fabric is the transport's
+# InProcessFabric; TorchComm is the torch.distributed world endpoint.
+ThreadFabric = InProcessFabric
+TorchComm = TorchTransport
 
 
 # ---- gates --------------------------------------------------------------------------
+def _ordered_peer_op(partition, comm: GroupComm, partner: int, launch) -> None:
+    """Run `launch(state)` -- a kernel that reads and writes the partner's
+    slice -- ordered against the partner's work without a host stream sync:
+    each side records its `pre` event, the pair meets on the host (so both
+    records are enqueued), each stream waits on the partner's `pre`, launches,
+    records `post`, meets again, and waits on the partner's `post` before its
+    own next kernel.  The host never blocks on the GPU; the exchange queues
+    behind the local passes and the next passes queue behind it."""
+    st = partition.sync_in()
+    pre, post = comm.peer_events(partner)
+    st.record_sync_event(0)
+    comm.pair_barrier(partner)
+    st.wait_event(pre)
+    launch(st)
+    st.record_sync_event(1)
+    comm.pair_barrier(partner)
+    st.wait_event(post)
+
+
 def _exchange_pairs(partition: sv.StatePartition, comm: GroupComm, q: int, u,
                     topology: RankTopology, control_local: int | None = None,
                     chunk: int = DEFAULT_CHUNK_AMPLITUDES) -> None:
     """Gate on global qubit q with the partner at rank distance 2^(q-m)
-    (distribution.py:121-178).  The barriers order the partner's previous
-    kernels before ours and ours before its next ones."""
+    (distribution.py:121-178).  Accounted like the reference's Fig. 3 scheme:
+    the half out and the updated half back, in chunks of `chunk` amplitudes."""
     m = topology.num_local_qubits
     d = 1 << (q - m)
     partner = comm.rank ^ d
     is_lower = (comm.rank & d) == 0
     mat = np.ascontiguousarray(np.asarray(u, dtype=np.complex128))
-    st = partition.sync_in()
     ctrl = -1 if control_local is None else int(control_local)
-    st.synchronize()
-    comm.pair_barrier(partner)
+    half = 1 << (m - 1)
+    if chunk < 1:
+        raise ValueError("chunk must be positive")
+    comm.account_exchange(2 * (-(-half // chunk)), 2 * half)
     if comm.exchange_mode == "nccl":
+        # NCCL orders the pair's grouped send/recv on the streams itself
+        st = partition.sync_in()
         _native.call("qs_exchange_gate_nccl", st.handle, comm.nccl_peer(partner),
                      1 if is_lower else 0, _native.dptr(mat), ctrl, int(chunk))
-    else:
-        _native.call("qs_exchange_gate_peer", st.handle, comm.peer_pointer(partner),
-                     1 if is_lower else 0, _native.dptr(mat), ctrl)
-    comm.pair_barrier(partner)
+        return
+    peer = comm.peer_pointer(partner)
+    _ordered_peer_op(partition, comm, partner, lambda st: _native.call(
+        "qs_exchange_gate_peer", st.handle, peer, 1 if is_lower else 0, _native.dptr(mat), ctrl))
 
 
 # ---- qubit remapping (SURVEY 8f row 1) -------------------------------------------
@@ -383,11 +307,10 @@ def swap_global_local(partition, comm: GroupComm, topology: RankTopology, layout
     d = 1 << (p - m)
     partner = comm.rank ^ d
     bit = 1 if comm.rank & d else 0
-    st = partition.sync_in()
-    st.synchronize()
-    comm.pair_barrier(partner)
-    _native.call("qs_swap_qubits_peer", st.handle, comm.peer_pointer(partner), l, bit)
-    comm.pair_barrier(partner)
+    peer = comm.peer_pointer(partner)
+    _ordered_peer_op(partition, comm, partner, lambda st: _native.call(
+        "qs_swap_qubits_peer", st.handle, peer, l, bit))
+    comm.account_exchange(2, 1 << (m - 1))
     layout.swap(p, l)
 
 
@@ -427,6 +350,7 @@ def restore_layout(partition, comm: GroupComm, topology: RankTopology,
 def apply_one_qubit_gate(partition, topology: RankTopology, comm: GroupComm, q: int, u,
                          chunk: int = DEFAULT_CHUNK_AMPLITUDES):
     """Collective one-qubit gate (distribution.py:181-192)."""
+    comm = world_comm(comm)
     route = route_one_qubit(comm.rank, topology, q)
     if route[0] == "idle":
         return partition
@@ -439,6 +363,7 @@ def apply_one_qubit_gate(partition, topology: RankTopology, comm: GroupComm, q: 
 def apply_controlled_gate(partition, topology: RankTopology, comm: GroupComm, control: int,
                           target: int, u, chunk: int = DEFAULT_CHUNK_AMPLITUDES):
     """Controlled gate with the reference's four locality cases (distribution.py:195-230)."""
+    comm = world_comm(comm)
     route = route_controlled(comm.rank, topology, control, target)
     kind = route[0]
     if kind in ("idle", "skip"):
@@ -454,6 +379,7 @@ def apply_controlled_gate(partition, topology: RankTopology, comm: GroupComm, co
 def group_reduce_sum(partial: float, topology: RankTopology, comm: GroupComm) -> float:
     """Sum one scalar per rank with the association of sv.tree_sum over rank
     partials (the reference's recursive doubling, distribution.py:233-252)."""
+    comm = world_comm(comm)
     if comm.rank >= topology.effective_ranks:
         return partial
     if topology.effective_ranks == 1:

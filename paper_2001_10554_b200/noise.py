@@ -290,6 +290,15 @@ def noise_gate_matrix(duration: float, model: NoiseModel, stream: RandomStream) 
     return _matrices_from_draws(stream.normal(3)[None, :], duration, model)[0]
 
 
+def apply_noise_gate(partition, q: int, duration: float, model: NoiseModel,
+                     stream: RandomStream):
+    """One stochastic noise gate on a single-rank partition (noise.py:84-90):
+    the matrix is drawn on the host from `stream`, the update is the local
+    1q kernel on the device."""
+    from . import statevector as sv
+    return sv.apply_local_one_qubit_gate(partition, q, noise_gate_matrix(duration, model, stream))
+
+
 def noise_gate_matrices(duration: float, model: NoiseModel, batch: StreamBatch) -> np.ndarray:
     """[S,2,2]: noise_gate_matrix for every stream of the batch, in one pass."""
     model.variances(duration)

@@ -28,6 +28,7 @@ from . import gates as gates_mod
 from . import statevector as sv
 from .graphs import edge_array, phase_lut, phase_lut_batch
 from . import noise as noise_mod
+from .pool import PoolLayout, build_pool, gather_state_values, incoherent_sum_over_pool
 
 NORM_CHECK_INTERVAL = 100
 NORM_TOL = 1e-10
@@ -145,62 +146,121 @@ def _angle(gate) -> float:
 # ---- contexts ------------------------------------------------------------------------
 @dataclass
 class RankContext:
-    """What one rank (one GPU or one emulated rank) needs to run circuits."""
+    """What one rank needs to run circuits (runtime.py:44-87).
 
-    comm: dist.GroupComm
+    The reference's fields come first and mean what they mean there:
+    `transport` is the world endpoint (None for one rank), `layout` the pool
+    layout of rank groups (pool.build_pool), `group`/`state_rank` this rank's
+    place in it, `comm` the group communicator, `partition` the device-resident
+    slice, and the three keyed random streams.  Shim-only fields follow, all
+    defaulted: `device`, `fuse` (numerics mode), `remap` (qubit remapping),
+    `state_offset` and `batch`.
+
+    Two pool shapes:
+      * num_states <= world (the reference's): contiguous power-of-two rank
+        groups, one state per group, each state sharded over its group;
+      * num_states > world (shim extension -- the reference raises): every rank
+        holds a contiguous block of whole states (`batch` = count, first state
+        `state_offset`) in ONE device allocation, so a pool step is one fused
+        launch per pass for all of them (runtime.PoolState)."""
+
+    transport: object
+    layout: PoolLayout
     num_qubits: int
-    num_states: int = 1
-    device: int = 0
+    seed: int
+    noise_model: "noise_mod.NoiseModel | None" = None
+    norm_check_interval: int = NORM_CHECK_INTERVAL
+    device: int | None = None
     fuse: bool = True
     remap: bool = False
-    norm_check_interval: int = NORM_CHECK_INTERVAL
-    seed: int = 0
-    noise_model: "noise_mod.NoiseModel | None" = None
-    state_offset: int = 0  # global index of this context's first pool state
+    state_offset: int | None = None
+    batch: int = 0  # > 0: batched pool extension, states held by this rank
+    pool_states: int = 0  # batched pool: states in the whole pool (tables cover them all)
+    pool_first: int = 0   # batched pool: state index of entry 0 of a whole-pool table
+    world_rank: int = field(init=False)
+    group: int | None = field(init=False)
+    state_rank: int | None = field(init=False)
     topology: dist.RankTopology = field(init=False)
-    layout: "dist.QubitLayout | None" = field(init=False, default=None)
+    comm: dist.GroupComm | None = field(init=False)
     partition: sv.StatePartition | None = field(init=False, default=None)
+    pool_stream: noise_mod.RandomStream = field(init=False)
+    local_stream: noise_mod.RandomStream = field(init=False)
+    gates_applied: int = field(init=False, default=0)
+    qubit_layout: "dist.QubitLayout | None" = field(init=False, default=None)
     pool: "PoolState | None" = field(init=False, default=None)
     queue: GateQueue | None = field(init=False, default=None)
-    gates_applied: int = field(init=False, default=0)
     _state_stream: object = field(init=False, default=None, repr=False)
 
     def __post_init__(self) -> None:
-        size = self.comm.size if self.num_states == 1 else 1
-        self.topology = dist.RankTopology(size, self.num_qubits)
-        if self.num_states > 1 and self.comm.size > 1:
-            raise ValueError("pool contexts hold whole states; split pools with split_pool()")
-        if self.comm.rank < self.topology.effective_ranks:
-            if self.num_states == 1:
-                self.partition = sv.allocate_partition(
-                    self.num_qubits, self.topology.num_local_qubits, self.comm.rank,
-                    device=self.device)
-                sv.init_basis_state(self.partition, 0)
-                self.queue = GateQueue(self.partition.state, self.fuse)
-                if self.remap and self.topology.rank_bits > 0:
-                    self.layout = dist.QubitLayout(self.num_qubits,
-                                                   self.topology.num_local_qubits)
-            else:
-                self.pool = PoolState(self.num_qubits, self.num_states, self.device, self.fuse)
-                self.queue = self.pool.queue
+        t = self.transport
+        if isinstance(t, dist.GroupComm) and t.transport is not None:
+            t = t.transport  # round-1 callers passed a group view of the world
+        elif isinstance(t, dist.GroupComm):
+            t = None
+        self.transport = t
+        self.world_rank = 0 if t is None else t.rank
+        if self.device is None:
+            self.device = _default_device(self.world_rank)
+        self.pool_stream = noise_mod.RandomStream(self.seed, noise_mod.SCOPE_POOL, 0)
+        self.local_stream = noise_mod.RandomStream(self.seed, noise_mod.SCOPE_LOCAL,
+                                                   self.world_rank)
+        if self.batch > 0:
+            # batched pool: whole states, no sharding, no peers
+            self.group = self.state_offset
+            self.state_rank = 0
+            self.topology = dist.RankTopology(1, self.num_qubits)
+            self.comm = dist.single_rank_comm()
+            self.pool = PoolState(self.num_qubits, self.batch, self.device, self.fuse)
+            self.queue = self.pool.queue
+            if t is not None:
+                dist.GroupComm(t, self.world_rank, 1).attach(None)
+            return
+        lay = self.layout
+        self.group = lay.group_of_rank(self.world_rank)
+        self.state_rank = lay.state_rank_of_rank(self.world_rank)
+        self.topology = dist.RankTopology(lay.ranks_per_state, self.num_qubits)
+        if self.group is None:
+            self.comm = None
+            if t is not None:  # the partition handles are a world collective
+                dist.GroupComm(t, self.world_rank, 1).attach(None)
+            return
+        if self.state_offset is None:
+            self.state_offset = self.group
+        self.comm = dist.GroupComm(t, lay.group_base(self.group), lay.ranks_per_state)
+        if self.state_rank < self.topology.effective_ranks:
+            self.partition = sv.allocate_partition(
+                self.num_qubits, self.topology.num_local_qubits, self.state_rank,
+                device=self.device)
+            sv.init_basis_state(self.partition, 0)
+            self.queue = GateQueue(self.partition.state, self.fuse)
+            if self.remap and self.topology.rank_bits > 0:
+                self.qubit_layout = dist.QubitLayout(self.num_qubits,
+                                                     self.topology.num_local_qubits)
         self.comm.attach(self.partition)
+        if self.comm.exchange_mode == "nccl" and hasattr(t, "nccl_init"):
+            t.nccl_init(self.comm.base_rank, self.comm.size)
 
     @property
     def is_idle(self) -> bool:
         return self.queue is None
 
     @property
+    def num_states(self) -> int:
+        """States held by this context (1, or the batch of a batched pool)."""
+        return self.batch if self.batch > 0 else 1
+
+    @property
     def state_stream(self):
         """The state-scope stream of this context's state (runtime.py:79);
-        pools get a StreamBatch with one stream per state."""
-        if self._state_stream is None:
+        a batched pool gets a StreamBatch with one stream per state."""
+        if self._state_stream is None and not (self.group is None and self.batch == 0):
             if self.pool is None:
                 self._state_stream = noise_mod.RandomStream(self.seed, noise_mod.SCOPE_STATE,
                                                             self.state_offset)
             else:
                 self._state_stream = noise_mod.StreamBatch(
                     noise_mod.RandomStream(self.seed, noise_mod.SCOPE_STATE, self.state_offset + s)
-                    for s in range(self.num_states))
+                    for s in range(self.batch))
         return self._state_stream
 
     @property
@@ -214,24 +274,63 @@ class RankContext:
             self.queue.flush()
 
 
-def make_context(comm: dist.GroupComm | None, num_qubits: int, num_states: int = 1,
-                 device: int = 0, fuse: bool = True, remap: bool = False, *, seed: int = 0,
-                 noise_model=None, state_offset: int = 0) -> RankContext:
-    """remap=True: gates on global qubits first swap the qubit into a local
-    position (half the traffic of the reference's exchange, and the gate then
-    fuses with its neighbours); reads restore the canonical layout.
-    seed/noise_model as the reference's make_context (runtime.py:90-99);
-    state_offset: global index of the first pool state (split_pool)."""
-    return RankContext(comm or dist.single_rank_comm(), num_qubits, num_states, device, fuse,
-                       remap, seed=seed, noise_model=noise_model, state_offset=state_offset)
+def _default_device(world_rank: int) -> int:
+    """One process per GPU (torchrun): LOCAL_RANK; otherwise device 0 (thread
+    ranks share the calling process's GPU unless told otherwise)."""
+    import os
+
+    if os.environ.get("QSB_ALL_RANKS_ON_DEVICE0") == "1":
+        return 0
+    lr = os.environ.get("LOCAL_RANK")
+    return int(lr) if lr is not None else 0
+
+
+def make_context(transport, num_qubits: int, num_states: int = 1, seed: int = 0,
+                 noise_model=None, *, device: int | None = None, fuse: bool = True,
+                 remap: bool = False, state_offset: int | None = None,
+                 batch: bool | None = None) -> RankContext:
+    """The reference's make_context (runtime.py:90-99): `transport` is this
+    rank's world endpoint (or None), the pool layout is build_pool(world,
+    num_states).  Shim keywords: `device` (default LOCAL_RANK or 0), `fuse`
+    (True: bit-identical fused passes; "factored": the factored numerics;
+    False: one kernel per gate), `remap` (global qubits are swapped into local
+    positions instead of exchanged), `state_offset` (global index of this
+    context's first state; keyed noise streams), `batch` (force/forbid the
+    batched pool extension; default: batched when num_states > world)."""
+    if isinstance(transport, dist.GroupComm):
+        world = transport.size if transport.transport is not None else 1
+    else:
+        world = 1 if transport is None else transport.world_size
+    if num_states < 1:
+        raise ValueError("need at least one state")
+    use_batch = num_states > world if batch is None else bool(batch)
+    if use_batch:
+        rank = 0 if transport is None else transport.rank
+        first, count = split_pool(num_states, rank, world)
+        base = 0
+        if state_offset is not None:  # a block of a larger pool split by the caller
+            base = state_offset
+            first += state_offset
+        if count < 1:
+            raise ValueError(f"{num_states} states leave rank {rank} of {world} without a state")
+        layout = PoolLayout(world, min(num_states, world), 1)
+        return RankContext(transport, layout, num_qubits, seed, noise_model, device=device,
+                           fuse=fuse, remap=remap, state_offset=first, batch=count,
+                           pool_states=num_states, pool_first=base)
+    layout = build_pool(world, num_states)
+    if layout.ranks_per_state >= (1 << num_qubits):
+        raise ValueError(f"{layout.ranks_per_state} ranks per state leave no local qubit "
+                         f"for n={num_qubits}")
+    return RankContext(transport, layout, num_qubits, seed, noise_model, device=device,
+                       fuse=fuse, remap=remap, state_offset=state_offset)
 
 
 def reset_state(ctx: RankContext, index: int = 0) -> None:
     if ctx.is_idle:
         return
     ctx.queue.discard()
-    if ctx.layout is not None:  # a fresh basis state: back to the canonical layout
-        ctx.layout = dist.QubitLayout(ctx.num_qubits, ctx.topology.num_local_qubits)
+    if ctx.qubit_layout is not None:  # a fresh basis state: back to the canonical layout
+        ctx.qubit_layout = dist.QubitLayout(ctx.num_qubits, ctx.topology.num_local_qubits)
     if ctx.partition is not None:
         sv.init_basis_state(ctx.partition, index)
     else:
@@ -240,15 +339,15 @@ def reset_state(ctx: RankContext, index: int = 0) -> None:
 
 
 def _restore(ctx: RankContext) -> None:
-    if ctx.layout is not None and not ctx.layout.is_identity():
+    if ctx.qubit_layout is not None and not ctx.qubit_layout.is_identity():
         ctx.flush()
-        dist.restore_layout(ctx.partition, ctx.comm, ctx.topology, ctx.layout)
+        dist.restore_layout(ctx.partition, ctx.comm, ctx.topology, ctx.qubit_layout)
 
 
 def _apply_gate_remapped(ctx: RankContext, gate) -> None:
     """apply_gate under a qubit layout: logical qubits are mapped to physical
     positions; a gate on a global position swaps it in first."""
-    L, topo, q = ctx.layout, ctx.topology, ctx.queue
+    L, topo, q = ctx.qubit_layout, ctx.topology, ctx.queue
     m = topo.num_local_qubits
     kind = gate.kind
     if kind == "diagcost":
@@ -292,7 +391,7 @@ def _swap_in(ctx: RankContext, qubit: int, protected=()) -> None:
     slice of a pair exchange, and the gate itself then runs locally and fuses
     with the gates that follow.  (Swapping into an untouched slot without a
     flush was measured to double the swaps in sweeps, tools/exp/remap_policy.py.)"""
-    L, m = ctx.layout, ctx.topology.num_local_qubits
+    L, m = ctx.qubit_layout, ctx.topology.num_local_qubits
     ctx.flush()
     p = L.phys[qubit]
     slot = next((l for l in reversed(L.recent) if l < m and l not in protected), None)
@@ -352,7 +451,7 @@ def apply_gate(ctx: RankContext, gate, noise_stream=None, *, noise_matrix=None) 
             return
         from .circuit import GateSpec
         gate = GateSpec("custom", gate.qubits, matrix=u)
-    if ctx.layout is not None:
+    if ctx.qubit_layout is not None:
         _apply_gate_remapped(ctx, gate)
         # the drift check needs no canonical layout (any association is fine)
         _count_and_check(ctx, restore=False)
@@ -473,36 +572,45 @@ def measure_maxcut(ctx: RankContext, graph):
     return _group_reduce(ctx, sv.maxcut_expectation(ctx.partition, graph))
 
 
-def gather_group_state(ctx: RankContext) -> np.ndarray | None:
-    """Full amplitude vector of the (single) state on rank 0 (runtime.py:239-258).
-    Threaded communicators gather through the fabric; TorchComm through
-    torch.distributed.gather_object."""
-    if ctx.is_idle and not isinstance(ctx.comm, dist.TorchComm):
+def gather_group_state(ctx: RankContext, group: int = 0) -> np.ndarray | None:
+    """Assemble group `group`'s full amplitude vector on world rank 0
+    (runtime.py:239-258): its ranks send their slices (in the canonical qubit
+    layout) through the transport, rank 0 concatenates them in rank order.
+    A batched pool's `group` is a state index; its owner sends it."""
+    t = ctx.transport
+    if ctx.batch > 0:
+        first = ctx.state_offset
+        mine = None
+        if first <= group < first + ctx.batch:
+            mine = ctx.pool.amplitudes()[group - first].copy()
+        if t is None or t.world_size == 1:
+            return mine
+        owner = None if mine is None else ctx.world_rank
+        owners = dist.GroupComm(t, 0, t.world_size).allgather(
+            -1.0 if owner is None else float(owner), t.world_size)
+        src = int(max(owners))
+        if ctx.world_rank == 0:
+            return mine if src == 0 else t.receive(src)
+        if src == ctx.world_rank:
+            t.send(0, mine)
         return None
-    if not ctx.is_idle:
+    members = ctx.group == group and not ctx.is_idle
+    if members:
         _restore(ctx)
         ctx.flush()
-    mine = ctx.state.download() if not ctx.is_idle else None
-    comm = ctx.comm
-    if comm.size == 1:
-        return mine
-    if isinstance(comm, dist.ThreadComm):
-        fab = comm.fabric
-        with fab._lock:
-            fab._gather.setdefault("state", {})[comm.rank] = mine
-        comm.allgather(0.0, ctx.topology.effective_ranks)
-        if comm.rank != 0:
-            return None
-        with fab._lock:
-            parts = [fab._gather["state"][r] for r in range(ctx.topology.effective_ranks)]
-        return np.concatenate(parts)
-    import torch.distributed as tdist
-
-    out = [None] * comm.size if comm.rank == 0 else None
-    tdist.gather_object(mine, out, dst=comm._global(0), group=comm.group)
-    if comm.rank != 0:
-        return None
-    return np.concatenate([p for p in out[: ctx.topology.effective_ranks]])
+    if t is None or t.world_size == 1:
+        return ctx.state.download()
+    base = ctx.layout.group_base(group)
+    size = ctx.layout.ranks_per_state
+    if ctx.world_rank == 0:
+        pieces = [None] * size
+        for r in range(size):
+            w = base + r
+            pieces[r] = ctx.state.download() if w == 0 else t.receive(w)
+        return np.concatenate(pieces)
+    if members:
+        t.send(0, ctx.state.download())
+    return None
 
 
 # ---- pool mode -----------------------------------------------------------------------
@@ -528,19 +636,26 @@ class PoolState:
 def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
                      noise_stream=None) -> None:
     """Every pool state runs `circuit`; state s binds slot_tables[name][s]
-    (runtime.py:192-209).  Per-state matrices/LUTs go to the device as tables;
-    noise gates draw state s's matrix from stream s of `noise_stream` (a
-    StreamBatch or a list of streams; default: the states' own streams)."""
+    (runtime.py:192-209).  A rank-group state binds its group's entry; a
+    batched pool sends its block of every table to the device as per-state
+    matrices/LUTs (one fused program for all its states).  Noise gates draw
+    state s's matrix from stream s of `noise_stream` (a StreamBatch or a list
+    of streams; default: the states' own streams)."""
     if not slot_tables:
         run_circuit(ctx, circuit, noise_stream=noise_stream)
         return
+    total = _pool_total(ctx)
+    for name, vals in slot_tables.items():
+        if len(vals) != total:
+            raise ValueError(f"table for ${name} has {len(vals)} entries for {total} states")
     if ctx.is_idle:
         return
-    S = ctx.num_states
-    for name, vals in slot_tables.items():
-        if len(vals) != S:
-            raise ValueError(f"table for ${name} has {len(vals)} entries for {S} states")
     tables = {k: np.asarray(v, dtype=np.float64) for k, v in slot_tables.items()}
+    if ctx.batch == 0:
+        bindings = {name: float(vals[ctx.group]) for name, vals in tables.items()}
+        run_circuit(ctx, circuit, bindings, noise_stream=noise_stream)
+        return
+    tables = {k: _my_values(ctx, v) for k, v in tables.items()}
     q = ctx.queue
     pre = _circuit_noise(ctx, circuit.gates, noise_stream)
     rot_cache: dict = {}
@@ -550,19 +665,11 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
             if gate.kind == "noise":
                 apply_gate(ctx, gate, noise_matrix=next(pre))
                 continue
-            if ctx.pool is None:
-                apply_gate(ctx, gate, noise_stream=noise_stream)
-                continue
             _queue_fixed(q, gate)
             continue
         if slot not in tables:
             raise ValueError(f"gate {gate.kind} has unbound slot ${slot}")
         vals = tables[slot]
-        if ctx.pool is None:
-            # single state: bind value 0 (run_circuit semantics)
-            from dataclasses import replace
-            apply_gate(ctx, replace(gate, param=float(vals[0])), noise_stream=noise_stream)
-            continue
         if gate.kind == "diagcost":
             q.cut_phase(gate.graph, vals)
         elif gate.kind in gates_mod.ROTATION_GATES:
@@ -578,6 +685,17 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
         else:
             raise ValueError(f"gate kind {gate.kind} takes no parameter")
     q.flush()
+    # the norm check of runtime.py:146-152 for every state, deferred to the end
+    # of the circuit (a check mid-program would split its fused passes): the
+    # drift is caught in the same circuit, a few gates later at most
+    before = ctx.gates_applied
+    ctx.gates_applied += sum(1 for g in circuit.gates if g.kind != "noise")
+    k = ctx.norm_check_interval
+    if k and ctx.gates_applied // k > before // k:
+        norm_sq = measure_norm_squared(ctx)
+        worst = float(np.max(np.abs(np.asarray(norm_sq, dtype=np.float64) - 1.0)))
+        if worst >= NORM_TOL:
+            raise NormDriftError(f"norm^2 drifted to {norm_sq!r} after {ctx.gates_applied} gates")
 
 
 def run_noise_ensemble(ctx: RankContext, circuit, model, trajectories: int, observe,
@@ -661,22 +779,34 @@ def noise_ensemble_csv(values, reference: float) -> str:
     return "\n".join(lines) + "\n"
 
 
+def _pool_total(ctx: RankContext) -> int:
+    return ctx.pool_states if ctx.batch > 0 else ctx.layout.num_states
+
+
+def _my_values(ctx: RankContext, vals: np.ndarray) -> np.ndarray:
+    """This context's entries of a whole-pool table (batched: its block)."""
+    first = ctx.state_offset - ctx.pool_first
+    return vals[first:first + ctx.batch]
+
+
 def apply_gate_pool(ctx: RankContext, gate, param_table=None) -> None:
     """One gate on every pool state; state s binds param_table[s]
-    (runtime.py:175-189).  A pool context sends the per-state values as one
-    table; a single-state context binds its own entry (state_offset)."""
+    (runtime.py:175-189).  A batched pool queues its block of values as one
+    per-state table (one launch for all its states)."""
     if param_table is None:
         apply_gate(ctx, gate)
         return
     vals = np.asarray(param_table, dtype=np.float64)
+    total = _pool_total(ctx)
+    if vals.shape != (total,):
+        raise ValueError(f"parameter table has {vals.size} entries for {total} states")
     if ctx.is_idle:
         return
-    if ctx.pool is None:
+    if ctx.batch == 0:
         from dataclasses import replace
-        apply_gate(ctx, replace(gate, param=float(vals[ctx.state_offset])))
+        apply_gate(ctx, replace(gate, param=float(vals[ctx.group])))
         return
-    if vals.shape != (ctx.num_states,):
-        raise ValueError(f"parameter table has {vals.size} entries for {ctx.num_states} states")
+    vals = _my_values(ctx, vals)
     q = ctx.queue
     if gate.kind == "diagcost":
         q.cut_phase(gate.graph, vals)
@@ -687,19 +817,53 @@ def apply_gate_pool(ctx: RankContext, gate, param_table=None) -> None:
                      np.stack([gates_mod.cphase(float(v)) for v in vals]))
     else:
         raise ValueError(f"gate kind {gate.kind} takes no parameter")
+    _count_and_check(ctx)
+
+
+def _batched_values(ctx: RankContext, value):
+    """Every state's value of a batched pool, in state order, on world rank 0
+    (None elsewhere): each rank's block goes to rank 0 in rank order, which is
+    state order (split_pool is contiguous)."""
+    arr = np.atleast_1d(np.asarray(value, dtype=np.float64))
+    t = ctx.transport
+    if t is None or t.world_size == 1:
+        return arr
+    if ctx.world_rank == 0:
+        parts = [arr] + [t.receive(r).real for r in range(1, t.world_size)]
+        return np.concatenate(parts)
+    t.send(0, arr)
+    return None
 
 
 def pool_sum(ctx: RankContext, value) -> float:
-    """Incoherent sum over the pool's states in the reference's fixed tree
-    order (runtime.py:230-232, pool.py:131-155); `value` is the per-state
-    array a pool context's measurements return (or one state's scalar)."""
-    return sv.tree_sum_values(np.atleast_1d(np.asarray(value, dtype=np.float64)))
+    """Incoherent sum of one group-reduced scalar per state, the same on every
+    rank, in the reference's fixed tree order (runtime.py:230-232,
+    pool.py:131-155).  A batched pool passes its per-state array."""
+    if ctx is None:  # round-1 callers: a plain array of per-state values
+        return sv.tree_sum_values(np.atleast_1d(np.asarray(value, dtype=np.float64)))
+    if ctx.batch > 0:
+        vals = _batched_values(ctx, value)
+        t = ctx.transport
+        if t is None or t.world_size == 1:
+            return sv.tree_sum_values(vals)
+        from .transport import broadcast_array
+        total = sv.tree_sum_values(vals) if vals is not None else 0.0
+        return float(broadcast_array(t, [total])[0].real)
+    return incoherent_sum_over_pool(value, ctx.layout, ctx.transport)
 
 
-def pool_gather(ctx: RankContext, value, num_groups: int | None = None) -> np.ndarray:
-    """Per-state values in state order (runtime.py:235-236)."""
-    arr = np.atleast_1d(np.asarray(value, dtype=np.float64))
-    return arr if num_groups is None else arr[:num_groups]
+def pool_gather(ctx: RankContext, value, num_groups: int | None = None):
+    """One value per state in state order on world rank 0, None elsewhere
+    (runtime.py:235-236, pool.py:158-182)."""
+    if ctx is None:
+        arr = np.atleast_1d(np.asarray(value, dtype=np.float64))
+        return arr if num_groups is None else arr[:num_groups]
+    if ctx.batch > 0:
+        vals = _batched_values(ctx, value)
+        if vals is None:
+            return None
+        return vals if num_groups is None else vals[:num_groups]
+    return gather_state_values(value, ctx.layout, ctx.transport, num_groups)
 
 
 def _queue_fixed(q: GateQueue, gate) -> None:
@@ -720,11 +884,15 @@ def split_pool(num_states: int, rank: int, world: int) -> tuple[int, int]:
 
 
 # ---- SPMD driver and convenience entry -------------------------------------------------
-def run_spmd(world_size: int, fn, timeout: float = 30.0, exchange_mode: str = "peer") -> list:
-    """fn(comm) on one thread per rank (runtime.py:261-288)."""
+def run_spmd(world_size: int, fn, timeout: float = 30.0, *, exchange_mode: str = "peer") -> list:
+    """fn(transport) on one thread per rank; results by rank (runtime.py:261-288).
+    Each thread gets its rank's world endpoint (InProcessFabric); the ranks'
+    partitions share the process's device unless contexts name others."""
     import threading
 
-    fabric = dist.ThreadFabric(world_size, timeout=timeout, exchange_mode=exchange_mode)
+    from .transport import InProcessFabric
+
+    fabric = InProcessFabric(world_size, timeout=timeout, exchange_mode=exchange_mode)
     if world_size == 1:
         return [fn(fabric.endpoint(0))]
     results: list = [None] * world_size
@@ -750,14 +918,16 @@ def run_spmd(world_size: int, fn, timeout: float = 30.0, exchange_mode: str = "p
     return results
 
 
-def simulate_circuit(circuit, num_ranks: int = 1, bindings: dict | None = None,
-                     device: int = 0, fuse: bool = True, timeout: float = 30.0,
-                     exchange_mode: str = "peer", remap: bool = False) -> np.ndarray:
-    """Run a circuit over `num_ranks` emulated ranks and return the full state
-    (runtime.py:291-302).  All emulated ranks share `device`."""
+def simulate_circuit(circuit, num_ranks: int = 1, num_states: int = 1, seed: int = 0,
+                     noise_model=None, bindings: dict | None = None, timeout: float = 30.0,
+                     *, device: int = 0, fuse: bool = True, exchange_mode: str = "peer",
+                     remap: bool = False) -> np.ndarray:
+    """Run a circuit on `num_ranks` thread ranks and return group 0's full
+    state vector (runtime.py:291-302).  All thread ranks share `device`."""
 
-    def rank_fn(comm):
-        ctx = make_context(comm, circuit.num_qubits, 1, device, fuse, remap)
+    def rank_fn(transport):
+        ctx = make_context(transport, circuit.num_qubits, num_states, seed, noise_model,
+                           device=device, fuse=fuse, remap=remap)
         run_circuit(ctx, circuit, bindings)
         return gather_group_state(ctx)
 

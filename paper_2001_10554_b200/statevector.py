@@ -70,11 +70,79 @@ def pair_update(a: np.ndarray, b: np.ndarray, u: np.ndarray):
 
 
 # ---- partitions --------------------------------------------------------------------
-class StatePartition:
-    """One rank's slice of 2^m amplitudes on a CUDA device (statevector.py:74-108)."""
+class _HostMirror(np.ndarray):
+    """Host copy of a device slice that notices writes.
 
-    def __init__(self, num_qubits: int, num_local_qubits: int, rank_index: int = 0,
-                 amplitudes: np.ndarray | None = None, *, device: int = 0):
+    Item assignment, in-place operators, ufuncs with ``out=`` and the numpy
+    functions that write into an argument -- on the mirror or on any view of
+    it -- mark the owning partition dirty; only then does the next device
+    operation upload it.  Reading never causes an upload (a
+    16 GiB H2D after merely inspecting the state).  Copies are plain arrays."""
+
+    def __array_finalize__(self, obj):
+        self._owner = getattr(obj, "_owner", None)
+
+    def _touch(self):
+        owner = self._owner
+        if owner is not None:
+            owner._dirty = True
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        self._touch()
+
+    def __array_ufunc__(self, ufunc, method, *inputs, **kwargs):
+        args = [x.view(np.ndarray) if isinstance(x, _HostMirror) else x for x in inputs]
+        outs = kwargs.get("out")
+        if outs:
+            kwargs["out"] = tuple(o.view(np.ndarray) if isinstance(o, _HostMirror) else o
+                                  for o in outs)
+        res = getattr(ufunc, method)(*args, **kwargs)
+        if outs:
+            for o in outs:
+                if isinstance(o, _HostMirror):
+                    o._touch()
+            return outs[0] if len(outs) == 1 else outs
+        return res
+
+    _WRITERS = ("copyto", "place", "put", "putmask", "put_along_axis", "fill_diagonal")
+
+    def __array_function__(self, func, types, args, kwargs):
+        plain = tuple(a.view(np.ndarray) if isinstance(a, _HostMirror) else a for a in args)
+        res = func(*plain, **kwargs)
+        if func.__name__ in self._WRITERS and args and isinstance(args[0], _HostMirror):
+            args[0]._touch()
+        if isinstance(res, _HostMirror):
+            res = res.view(np.ndarray)
+        return res
+
+    def fill(self, value):
+        super().fill(value)
+        self._touch()
+
+    def put(self, *a, **k):
+        super().put(*a, **k)
+        self._touch()
+
+    def sort(self, *a, **k):
+        super().sort(*a, **k)
+        self._touch()
+
+    def copy(self, order="C"):
+        return np.array(self.view(np.ndarray), copy=True, order=order)
+
+
+class StatePartition:
+    """One rank's slice of 2^m amplitudes on a CUDA device (statevector.py:74-108).
+
+    ``amplitudes`` (the reference's field, a constructor argument there) may be
+    None here: the slice is then allocated on the device without a host copy.
+    Reading ``amplitudes`` downloads a write-tracking host mirror; writes
+    through it (``part.amplitudes[:] = x``, as the reference's tests do) are
+    uploaded before the next device operation, reads are not."""
+
+    def __init__(self, num_qubits: int, num_local_qubits: int, rank_index: int,
+                 amplitudes: np.ndarray | None, *, device: int = 0):
         n, m, r = num_qubits, num_local_qubits, rank_index
         if not (0 < m <= n):
             raise ValueError(f"need 0 < num_local_qubits <= num_qubits, got m={m}, n={n}")
@@ -92,7 +160,8 @@ class StatePartition:
         self.rank_index = r
         self.device = device
         self.state = DeviceState(n, m, r, 1, device)
-        self._mirror: np.ndarray | None = None
+        self._mirror: _HostMirror | None = None
+        self._dirty = False
         if amplitudes is not None:
             self.state.upload(amplitudes)
 
@@ -112,7 +181,9 @@ class StatePartition:
     @property
     def amplitudes(self) -> np.ndarray:
         if self._mirror is None:
-            self._mirror = self.state.download()
+            mirror = self.state.download().view(_HostMirror)
+            mirror._owner = self
+            self._mirror, self._dirty = mirror, False
         return self._mirror
 
     @amplitudes.setter
@@ -120,14 +191,22 @@ class StatePartition:
         value = np.ascontiguousarray(value, dtype=np.complex128)
         if value.shape != (1 << self.num_local_qubits,):
             raise ValueError("amplitude slice has the wrong length")
-        self._mirror = None
+        self._drop_mirror()
         self.state.upload(value)
 
-    def sync_in(self) -> DeviceState:
-        """Push a host mirror that may have been written, then drop it."""
+    def _drop_mirror(self) -> None:
         if self._mirror is not None:
-            mirror, self._mirror = self._mirror, None
-            self.state.upload(mirror)
+            self._mirror._owner = None  # later writes to it no longer reach the state
+        self._mirror, self._dirty = None, False
+
+    def sync_in(self, mutating: bool = True) -> DeviceState:
+        """Before a device operation: upload the host mirror if it was written;
+        a mutating operation then drops it (a read-only one keeps it)."""
+        if self._mirror is not None and self._dirty:
+            self.state.upload(self._mirror.view(np.ndarray))
+            self._dirty = False
+        if mutating:
+            self._drop_mirror()
         return self.state
 
     def __repr__(self) -> str:
@@ -139,7 +218,7 @@ class StatePartition:
 def read_amplitudes(partition: StatePartition, out: np.ndarray | None = None) -> np.ndarray:
     """Copy the slice into `out` (e.g. a pinned host buffer) or a new array;
     unlike ``.amplitudes`` no host mirror is kept."""
-    st = partition.sync_in()
+    st = partition.sync_in(False)
     return st.download(out)
 
 
@@ -154,8 +233,11 @@ def exchange_amplitudes(partition: StatePartition, new: np.ndarray, out: np.ndar
 
 def allocate_partition(num_qubits: int, num_local_qubits: int | None = None,
                        rank_index: int = 0, *, device: int = 0) -> StatePartition:
+    """A zeroed slice on the device (statevector.py:111-115)."""
     m = num_qubits if num_local_qubits is None else num_local_qubits
-    return StatePartition(num_qubits, m, rank_index, device=device)
+    part = StatePartition(num_qubits, m, rank_index, None, device=device)
+    _native.call("qs_init_zero", part.state.handle)
+    return part
 
 
 def full_state_bytes(num_qubits: int) -> int:
@@ -166,13 +248,13 @@ def init_basis_state(partition: StatePartition, index: int) -> StatePartition:
     if not (0 <= index < (1 << partition.num_qubits)):
         raise ValueError(
             f"basis index {index} out of range for {partition.num_qubits} qubits")
-    partition._mirror = None
+    partition._drop_mirror()
     _native.call("qs_init_basis", partition.state.handle, index)
     return partition
 
 
 def init_uniform(partition: StatePartition) -> StatePartition:
-    partition._mirror = None
+    partition._drop_mirror()
     # the value the reference assigns (statevector.py:140), evaluated on the host
     value = 2.0 ** (-partition.num_qubits / 2.0)
     _native.call("qs_init_constant", partition.state.handle, value, 0.0)
@@ -226,12 +308,8 @@ class CutPhase:
         self.gamma = float(gamma)
 
     def __call__(self, idx):
-        idx = np.asarray(idx, dtype=np.uint64)
-        cuts = np.zeros(idx.shape, dtype=np.float64)
-        one = np.uint64(1)
-        for u, v in self.graph.edges:
-            cuts += ((idx >> np.uint64(u)) ^ (idx >> np.uint64(v))) & one
-        return self.gamma * cuts
+        from .graphs import cut_counts
+        return self.gamma * cut_counts(self.graph, idx)
 
 
 def apply_cut_phase(partition: StatePartition, graph, gamma: float) -> StatePartition:
@@ -244,35 +322,41 @@ def apply_cut_phase(partition: StatePartition, graph, gamma: float) -> StatePart
 
 
 def apply_diagonal_phase(partition: StatePartition, phases) -> StatePartition:
-    """psi_i *= exp(-1j * phases(i)) (statevector.py:198-206).
+    """psi_i *= exp(-1j * phases(i)) over the owned indices (statevector.py:198-206).
 
-    The device evaluates the reference's only in-tree phase function, the QAOA
-    cut phase; pass a :class:`CutPhase`.  An arbitrary Python callable would
-    need host evaluation per amplitude, which this core does not do."""
-    if not isinstance(phases, CutPhase):
-        raise TypeError("apply_diagonal_phase on the B200 core takes a CutPhase(graph, gamma); "
-                        "arbitrary callables would need a host (CPU) evaluation path")
-    return apply_cut_phase(partition, phases.graph, phases.gamma)
+    A :class:`CutPhase` (the reference's in-tree phase function, runtime.py:
+    131-133) runs entirely on the device (edge list + LUT).  Any other
+    callable is the caller's host code: it is evaluated on the owned indices
+    as the reference does, the factors exp(-1j * angles) are formed with the
+    same numpy expression, and the device multiplies them in
+    (qs_apply_diagonal) -- bit-identical to the reference."""
+    if isinstance(phases, CutPhase):
+        return apply_cut_phase(partition, phases.graph, phases.gamma)
+    angles = np.asarray(phases(partition.owned_indices()), dtype=np.float64)
+    factors = np.exp(-1j * angles)
+    st = partition.sync_in()
+    st.apply_diagonal(np.broadcast_to(factors, (1 << partition.num_local_qubits,)))
+    return partition
 
 
 # ---- observables (partial sums in tree order) ------------------------------------
 def norm_squared(partition: StatePartition) -> float:
-    return float(partition.sync_in().observable(_native.QS_OBS_NORM)[0])
+    return float(partition.sync_in(False).observable(_native.QS_OBS_NORM)[0])
 
 
 def get_probability(partition: StatePartition, q: int) -> float:
     if not (0 <= q < partition.num_qubits):
         raise ValueError(f"qubit {q} out of range")
-    return float(partition.sync_in().observable(_native.QS_OBS_PROB, q)[0])
+    return float(partition.sync_in(False).observable(_native.QS_OBS_PROB, q)[0])
 
 
 def z_expectation(partition: StatePartition, q: int) -> float:
     if not (0 <= q < partition.num_qubits):
         raise ValueError(f"qubit {q} out of range")
-    return float(partition.sync_in().observable(_native.QS_OBS_Z, q)[0])
+    return float(partition.sync_in(False).observable(_native.QS_OBS_Z, q)[0])
 
 
 def maxcut_expectation(partition: StatePartition, graph) -> float:
     if graph.num_vertices > partition.num_qubits:
         raise ValueError("graph vertices exceed qubit count")
-    return float(partition.sync_in().observable(_native.QS_OBS_MAXCUT, 0, edge_array(graph))[0])
+    return float(partition.sync_in(False).observable(_native.QS_OBS_MAXCUT, 0, edge_array(graph))[0])

@@ -10,6 +10,10 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# the reference's own tests (tests/ref_suite/_fetched) run in a subprocess of
+# their own (tests/test_*ref_suite.py), never collected into this session
+collect_ignore = ["ref_suite"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); parity tests proper")

@@ -369,3 +369,87 @@ def test_factored_pool_per_state_diagonals_noise_like():
             osv.apply_1q(expected[s], q, us[s])
     got = pool.amplitudes()
     assert max_dev(got, expected) <= TOL
+
+
+def test_factored_pool_per_state_diagonal_gates():
+    """Per-state gates that are diagonal for every state (per-state RZ(gamma_s)
+    between CNOTs, pure dephasing, fused products that come out diagonal) fold
+    into the per-state pending diagonals and scalars; none may be dropped
+    (CNOT, per-state RZ, CNOT + 10 H lost the RZ)."""
+    from oracle import statevector as osv
+    rng = np.random.default_rng(41)
+    n, S = 12, 4
+    states = np.stack([ogates.random_state(n, rng) for _ in range(S)])
+    cx = X
+    # the advisor's harness: CNOT, per-state RZ, CNOT, then 10 Hadamards
+    pool = runtime.PoolState(n, S, fuse=FACT)
+    pool.state.upload(states)
+    expected = states.copy()
+    pool.queue.controlled(0, 1, cx)
+    rz = np.stack([ogates.rz(float(g)) for g in rng.uniform(0, 2 * np.pi, S)])
+    pool.queue.one_qubit(1, rz)
+    pool.queue.controlled(0, 1, cx)
+    for q in range(2, 12):
+        pool.queue.one_qubit(q, H)
+    for s in range(S):
+        osv.apply_controlled(expected[s], 0, 1, cx)
+        osv.apply_1q(expected[s], 1, rz[s])
+        osv.apply_controlled(expected[s], 0, 1, cx)
+        for q in range(2, 12):
+            osv.apply_1q(expected[s], q, H)
+    got = pool.amplitudes()
+    assert max_dev(got, expected) <= TOL
+    # random mix with per-state diagonals everywhere (and a per-state product
+    # noise . T . noise that comes out diagonal)
+    pool = runtime.PoolState(n, S, fuse=FACT)
+    pool.state.upload(states)
+    expected = states.copy()
+    T = np.diag([1.0, np.exp(0.25j * np.pi)]).astype(np.complex128)
+    for step in range(80):
+        q = int(rng.integers(n))
+        r = rng.random()
+        if r < 0.3:
+            us = np.stack([ogates.rz(float(a)) for a in rng.uniform(0, 2 * np.pi, S)])
+        elif r < 0.4:
+            a = rng.uniform(0, 1, S)
+            us = np.stack([ogates.rz(float(x)) @ T @ ogates.rz(float(-2 * x)) for x in a])
+        elif r < 0.6:
+            us = np.stack([ogates.rx(float(x)) for x in rng.uniform(0, 2 * np.pi, S)])
+        elif r < 0.75:
+            us = np.stack([ogates.random_unitary_2x2(rng)] * S)
+        else:
+            t = int(rng.integers(n - 1))
+            t = t if t < q else t + 1
+            pool.queue.controlled(q, t, cx)
+            for s in range(S):
+                osv.apply_controlled(expected[s], q, t, cx)
+            continue
+        pool.queue.one_qubit(q, us)
+        for s in range(S):
+            osv.apply_1q(expected[s], q, us[s])
+    got = pool.amplitudes()
+    assert max_dev(got, expected) <= TOL
+
+
+def test_factored_pool_two_rescales_keep_their_place():
+    """Two or more mid-program per-state rescales under the default re-order:
+    each must stay between the shears around it (pulled to the
+    front, their product underflowed the state to zero)."""
+    from oracle import statevector as osv
+    rng = np.random.default_rng(43)
+    n, S = 16, 2
+    states = np.stack([ogates.random_state(n, rng) for _ in range(S)])
+    pool = runtime.PoolState(n, S, fuse=FACT)
+    pool.state.upload(states)
+    expected = states.copy()
+    for layer in range(8):
+        for q in range(n):
+            th = np.array([np.pi - 3e-9, np.pi + 5e-9]) + 1e-10 * layer
+            us = np.stack([ogates.rx(float(x)) for x in th])
+            pool.queue.one_qubit(q, us)
+            for s in range(S):
+                osv.apply_1q(expected[s], q, us[s])
+    got = pool.amplitudes()
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got)) > 1e-6
+    assert max_dev(got, expected) <= TOL

@@ -1,0 +1,43 @@
+"""The reference's own hot-path test suite (pkg/tests: test_statevector,
+test_distribution, test_pool, test_runtime, test_circuit, test_gates and
+acceptance criteria 1-4), unchanged, run against the shim on the GPU through
+the `qpool` alias (tests/ref_suite).  This is the drop-in check of SURVEY.md
+section 4: every reference caller contract the tests exercise -- make_context
+/ simulate_circuit / run_spmd signatures, rank-group pools, transport
+counters, write-through `partition.amplitudes`, arbitrary phase callables --
+holds over the CUDA core."""
+import os
+import sys
+
+import pytest
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "ref_suite"))
+import runner  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(res):
+    tail = res.stdout[-6000:] + res.stderr[-3000:]
+    assert res.returncode == 0, tail
+    assert " passed" in res.stdout and " failed" not in res.stdout, tail
+
+
+def test_reference_suite_fetched():
+    assert runner.available(), ("tests/ref_suite/_fetched is missing: build() fetches it from "
+                                "/root/reference in the build container")
+
+
+@pytest.mark.timeout(1500)
+@pytest.mark.parametrize("module", runner.MODULES)
+def test_reference_module_passes_on_the_shim(module):
+    if not runner.available():
+        pytest.skip("reference suite not fetched")
+    _check(runner.run([module]))
+
+
+@pytest.mark.timeout(1500)
+def test_reference_acceptance_criteria_1_to_4():
+    if not runner.available():
+        pytest.skip("reference suite not fetched")
+    _check(runner.run([runner.ACCEPTANCE, "-k", runner.ACCEPTANCE_K]))

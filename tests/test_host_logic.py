@@ -219,7 +219,29 @@ def test_pool_helpers_follow_reference_tree_order():
     from paper_2001_10554_b200.statevector import tree_sum_values
 
     vals = np.random.default_rng(2).standard_normal(7)
-    assert pool.incoherent_sum_over_pool(vals) == tree_sum_values(vals)
+    assert pool.incoherent_sum_over_pool(0.3, pool.build_pool(1, 1), None) == 0.3
+    # world 7, 3 states of 2 ranks (rank 6 idle): every rank gets the tree sum
+    # of the group leaders' values, rank 0 the values in group order
+    import threading
+    from paper_2001_10554_b200 import transport as tp
+    fab = tp.InProcessFabric(7, timeout=5.0)
+    layout = pool.build_pool(7, 3)
+    out = [None] * 7
+
+    def run(r):
+        t = fab.endpoint(r)
+        g = layout.group_of_rank(r)
+        mine = 0.0 if g is None else float(vals[g])
+        out[r] = (pool.incoherent_sum_over_pool(mine, layout, t),
+                  pool.gather_state_values(mine, layout, t))
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(7)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert all(o[0] == tree_sum_values(vals[:3]) for o in out)
+    assert np.array_equal(out[0][1], vals[:3]) and all(o[1] is None for o in out[1:])
     assert runtime.pool_sum(None, vals) == tree_sum_values(vals)
     assert runtime.pool_sum(None, 0.25) == 0.25
     assert np.array_equal(runtime.pool_gather(None, vals, 3), vals[:3])
