@@ -42,16 +42,24 @@ LAUNCH_KINDS = {1: "k_gate1q", 2: "k_controlled", 3: "k_cut_phase", 4: "k_tile",
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 10; the QAOA swarm: 50, BASELINE config 5)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--local-qubits", type=int, default=30)
+    ap.add_argument("--local-qubits", type=int, default=None,
+                    help="amplitudes per GPU = 2^M (default: 30 for the config-2 sweep at "
+                         "N=1, 33 for the weak-scaled config-4 layer at N>1)")
     ap.add_argument("--no-fuse", action="store_true")
     ap.add_argument("--numerics", default="factored", choices=["factored", "exact"],
                     help="factored: QS_FUSE_FACTORED (Euler-factored 1q gates, within 1e-12 "
                          "of the reference); exact: QS_FUSE_EXACT (bit-identical)")
-    ap.add_argument("--workload", default="sweep",
-                    choices=["sweep", "qaoa", "cfg3", "cfg4", "noise"])
+    ap.add_argument("--workload", default=None,
+                    choices=["sweep", "qaoa", "cfg3", "cfg4", "noise"],
+                    help="default: sweep (config 2) at N=1, cfg4 (config 4, weak-scaled) at N>1")
+    ap.add_argument("--ref-local-qubits", type=int, default=23,
+                    help="reference arm at N>1: amplitudes per thread-rank (host RAM bound)")
+    ap.add_argument("--no-config4-point", action="store_true",
+                    help="N=1 sweep: skip the config-4 n=33 point of the weak-scaling curve")
     ap.add_argument("--seed", type=int, default=20260809)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -61,7 +69,14 @@ def parse():
     ap.add_argument("--remap", action="store_true",
                     help="gates on global qubits swap the qubit into a local position "
                          "(half the NVLink traffic) instead of the pair exchange")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.workload is None:
+        args.workload = "sweep" if args.gpus == 1 else "cfg4"
+    if args.steps is None:
+        args.steps = 50 if args.workload == "qaoa" else 10
+    if args.local_qubits is None:
+        args.local_qubits = 33 if (args.gpus > 1 and args.workload == "cfg4") else 30
+    return args
 
 
 def fuse_mode(args):
@@ -203,44 +218,143 @@ def haar(rng):
     return haar_2x2(rng)
 
 
+def host_gaussian_state(m: int, seed: int) -> np.ndarray:
+    """Normalised i.i.d. N(0,1) re/im state of 2^m amplitudes (the recipe of
+    tests/oracles.py:99-101), filled in parallel chunks from spawned seeds."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import cpu_baseline as cb
+
+    psi = np.empty(1 << m, dtype=np.complex128)
+    view = psi.view(np.float64)
+    chunk = 1 << 24
+    seeds = np.random.SeedSequence(seed).spawn(max(1, view.size // chunk))
+
+    def fill(k):
+        g = np.random.default_rng(seeds[k])
+        g.standard_normal(out=view[k * chunk:(k + 1) * chunk])
+
+    with ThreadPoolExecutor(cb.threads()) as ex:
+        list(ex.map(fill, range(len(seeds))))
+    norm = 0.0
+    for k in range(0, psi.size, chunk):
+        a = psi[k:k + chunk]
+        norm += float(np.vdot(a, a).real)
+    psi *= 1.0 / np.sqrt(norm)
+    return psi
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU algorithm (oracle port; the Python
-    reference cannot travel to the GPU box) on the host cores."""
+    """--impl reference: the reference's own CPU algorithm of the path (the
+    oracle's numpy restatement, all host threads; the Python reference cannot
+    travel to the GPU box) on OUR arm's workload, each step a bounded sample.
+    N=1: the config-2 sweep on a normalised Gaussian 2^m state, 3 consecutive
+    gates of the sweep per step (targets in sweep order, fresh Haar each).
+    N>1 (torchrun): rank 0 alone runs the reference's distributed path --
+    local gates plus the Fig. 3 pair exchange (oracle/distribution.py,
+    restating distribution.py:121-230) -- on N thread-ranks at a reduced
+    2^ref_local_qubits amplitudes per rank, one config-4 layer per step."""
     world, rank, local = dist_env()
     if rank != 0:
         return 0
     from oracle import cpu_baseline as cb
 
+    if world > 1:
+        return run_reference_dist(args, world)
     m = args.local_qubits
-    rng = np.random.default_rng(args.seed)
-    psi = np.full(1 << m, 2.0 ** (-m / 2.0), dtype=np.complex128)
-    for s in range(args.warmup):
-        cb.apply_1q_threaded(psi, s % m, haar(rng))
-    times = []
+    rng = np.random.default_rng(args.seed + 1)
+    psi = host_gaussian_state(m, args.seed)
+    per_step = 3
+    q = 0
+
+    def step():
+        nonlocal q
+        for _ in range(per_step):
+            cb.apply_1q_threaded(psi, q, haar(rng))
+            q = (q + 1) % m
+
+    for _ in range(args.warmup):
+        step()
     t0 = time.perf_counter()
-    for s in range(args.steps):
-        q = (s * 7) % m
-        a = time.perf_counter()
-        cb.apply_1q_threaded(psi, q, haar(rng))
-        times.append(time.perf_counter() - a)
+    for _ in range(args.steps):
+        step()
     dt = time.perf_counter() - t0
-    units = args.steps * (2.0 ** m) / 2.0 ** 30
+    units = args.steps * per_step * (2.0 ** m) / 2.0 ** 30
     value = units / dt
+    sample = (f"{per_step} consecutive gates of the config-2 sweep per step (targets in sweep "
+              f"order, fresh Haar 2x2 each) on a normalised Gaussian 2^{m} c128 state, "
+              f"oracle/cpu_baseline.py (numpy, {cb.threads()} threads)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128 (f64 pairs)", "data": "synthetic",
-        # our arm's workload; each reference step is a bounded sample of it
         "config": {"workload": f"config 2 sweep: Haar 2x2 on each of the {m} qubits in turn, "
                                f"fresh unitaries per step, normalised Gaussian state, "
                                f"2^{m} c128 amplitudes per GPU (n={m}, 0 global qubits)",
-                   "qubits": m, "local_qubits": m,
-                   "sample": f"one Haar 2x2 gate per step, targets (7*step) mod {m}, on a "
-                             f"uniform 2^{m} state (same arithmetic per gate-update)",
+                   "qubits": m, "local_qubits": m, "sample": sample, "same_workload": True,
                    "parallelism": f"{cb.threads()} host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.threads(), "kind": "port",
-                         "sample": f"{args.steps} single-gate steps at n={m}"},
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def run_reference_dist(args, world):
+    """Rank 0 of a torchrun: the reference's distributed config-4 layer on
+    `world` thread-ranks (oracle restatement), host RAM-bounded size."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import distribution as odist
+    from oracle import statevector as osv
+
+    m = args.ref_local_qubits
+    p = world.bit_length() - 1
+    n = m + p
+    psi = host_gaussian_state(n, args.seed)
+    parts = [psi[r << m:(r + 1) << m] for r in range(world)]
+    rng = np.random.default_rng(args.seed + 1)
+    pool = ThreadPoolExecutor(world)
+    cx = [(q, n - 1 - q) for q in range(n // 2)]
+    X = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+
+    def layer():
+        for q in range(n):
+            u = haar(rng)
+            if q < m:  # every rank its local pairs, concurrently
+                list(pool.map(lambda part: osv.apply_1q(part, q, u), parts))
+            else:
+                odist.apply_one_qubit_gate(parts, n, q, u)
+        for c, t in cx:
+            if c < m and t < m:
+                list(pool.map(lambda part: osv.apply_controlled(part, c, t, X), parts))
+            else:
+                odist.apply_controlled_gate(parts, n, c, t, X)
+
+    for _ in range(args.warmup):
+        layer()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        layer()
+    dt = time.perf_counter() - t0
+    gates = n + len(cx)
+    value = args.steps * gates * (2.0 ** n) / 2.0 ** 30 / dt
+    sample = (f"config-4 layers at n={n} = {m} local + {p} global qubits on {world} thread-ranks "
+              f"(2^{m} c128 per rank; the GPU arm holds 2^{args.local_qubits}), oracle "
+              "restatement of the reference's local kernels and Fig. 3 pair exchange")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128 (f64 pairs)", "data": "synthetic",
+        "config": {"workload": f"config 4 layer (weak-scaled): Haar 2x2 on all n qubits, then "
+                               f"CX(q, n-1-q) for q < n/2; {world} ranks",
+                   "qubits": n, "local_qubits": m, "sample": sample, "same_workload": False,
+                   "parallelism": f"{world} thread-ranks"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": world, "kind": "port",
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -248,32 +362,48 @@ def run_reference(args):
 
 
 # ---- our arm ----------------------------------------------------------------------------
+def physical_devices(dist, local: int) -> int:
+    """Distinct (host, device) pairs the ranks ran on (emulated ranks share one)."""
+    if dist is None:
+        return 1
+    import socket
+
+    mine = (socket.gethostname(), int(local))
+    allv = [None] * dist.get_world_size()
+    dist.all_gather_object(allv, mine)
+    return len(set(allv))
+
+
 def run_ours(args):
     world, rank, local = dist_env()
-    if os.environ.get("QSB_ALL_RANKS_ON_DEVICE0"):
+    emulated = bool(os.environ.get("QSB_ALL_RANKS_ON_DEVICE0"))
+    if emulated:
         local = 0  # functional multi-rank run on one GPU (exchange kernels never wait on each other)
     dist = init_dist(world)
     import paper_2001_10554_b200 as qs
     from paper_2001_10554_b200 import _native, runtime
     from paper_2001_10554_b200 import distribution as qdist
+    from paper_2001_10554_b200 import transport as qtp
     from paper_2001_10554_b200.workloads import device_gaussian
 
     if qs.device_count() < 1:
         raise SystemExit("bench.py: no CUDA device -- the B200 core has no CPU fallback")
     if world & (world - 1):
         raise SystemExit("bench.py: --gpus must be a power of two")
+    devices = physical_devices(dist, local)
     m = args.local_qubits
     p = world.bit_length() - 1
     n = m + p
-    comm = qdist.TorchComm(exchange_mode=args.exchange) if world > 1 else qdist.single_rank_comm()
+    transport = qtp.TorchTransport(exchange_mode=args.exchange) if world > 1 else None
     if args.workload == "qaoa":
-        return run_qaoa(args, dist, comm, world, rank, local)
+        return run_qaoa(args, dist, transport, world, rank, local)
     if args.workload == "noise":
-        return run_noise(args, dist, comm, world, rank, local)
-    ctx = runtime.make_context(comm, n, 1, device=local, fuse=fuse_mode(args),
+        return run_noise(args, dist, transport, world, rank, local)
+    ctx = runtime.make_context(transport, n, 1, device=local, fuse=fuse_mode(args),
                                remap=args.remap)
     ctx.norm_check_interval = 0
     st = ctx.state
+    comm = ctx.comm
     group_norm = (lambda x: qdist.group_reduce_sum(x, ctx.topology, comm)) if world > 1 else None
     device_gaussian(st, args.seed, group_norm)
     rng = np.random.default_rng(args.seed + 1)
@@ -296,21 +426,22 @@ def run_ours(args):
         sweeps = [[(prng.uniform(0, 2 * np.pi), haar(prng)) for _ in pairs]
                   for _ in range(total_steps)]
 
-    def step(us):
+    def step(us, c=None):
+        c = ctx if c is None else c
         if cfg3:
-            for (c, t), (phi, u) in zip(pairs, us):
-                runtime.apply_gate(ctx, GateSpec("cx", (c, t)))
-                runtime.apply_gate(ctx, GateSpec("cphase", (c, t), float(phi)))
-                runtime.apply_gate(ctx, GateSpec("cu", (c, t), matrix=u))
-            ctx.flush()
+            for (cq, tq), (phi, u) in zip(pairs, us):
+                runtime.apply_gate(c, GateSpec("cx", (cq, tq)))
+                runtime.apply_gate(c, GateSpec("cphase", (cq, tq), float(phi)))
+                runtime.apply_gate(c, GateSpec("cu", (cq, tq), matrix=u))
+            c.flush()
             return
         # config 2: Haar gate on every qubit; config 4 adds CX(q, n-1-q), q < n/2
         # (pairs cross the local/global boundary: routed like the reference)
         for k in range(n):
-            runtime.apply_gate(ctx, GateSpec("custom", (k,), matrix=us[k]))
-        for c, t in cx_pairs:
-            runtime.apply_gate(ctx, GateSpec("cx", (c, t)))
-        ctx.flush()
+            runtime.apply_gate(c, GateSpec("custom", (k,), matrix=us[k]))
+        for cq, tq in cx_pairs:
+            runtime.apply_gate(c, GateSpec("cx", (cq, tq)))
+        c.flush()
 
     for s in range(args.warmup):
         step(sweeps[s])
@@ -353,19 +484,43 @@ def run_ours(args):
     for k, v in kinds.items():
         share[LAUNCH_KINDS.get(k, str(k))] = {"launches": len(v), "ms": float(np.sum(v)),
                                              "share": float(np.sum(v) / ms_dev)}
-    # roofline on ALGORITHMIC bytes (32*2^m B per 1q gate, 16*2^m per
-    # controlled gate) x the gate-updates one launch processes; a fused pass
-    # moves each amplitude once (32*2^m B physical, ncu `traffic`), so the
-    # algorithmic rate exceeds the copy peak by the fusion depth
+    # Roofline of the dominant kernel on its own algorithmic bytes: one fused
+    # pass reads and writes each amplitude of the slice once, 32*2^m B, the
+    # least any pass can move (SURVEY 8(d)'s per-gate figure is the same 32 B
+    # per amplitude); frac = that / avg launch time / measured copy peak.
+    # fusion_gain = gate-updates one launch applies (the unfused simulator
+    # moves 32*2^m B per gate-update, so the algorithmic-per-gate rate is
+    # fusion_gain x the pass rate).
     launches_per_step = len(kinds.get(dom, [])) / max(args.steps, 1)
-    bytes_per_launch = bytes_per_step_per_gpu / max(launches_per_step, 1e-9)
     units_per_launch = gates_per_step / max(launches_per_step, 1e-9)
-    achieved = bytes_per_launch / (dom_ms / 1e3) / 1e9
-    physical = 32.0 * (2 ** m) / (dom_ms / 1e3) / 1e9
+    pass_bytes = 32.0 * (2 ** m)
+    physical = pass_bytes / (dom_ms / 1e3) / 1e9
     tr = ncu_traffic(LAUNCH_KINDS.get(dom, ""))
     traffic = None
     if tr and tr.get("bytes_per_amplitude"):
         traffic = tr["bytes_per_amplitude"] * (2 ** m)
+
+    # global-qubit gates: NVLink bytes per exchange launch (per direction per
+    # GPU: the partner's half read + our half written back by the partner =
+    # 2^m * 16 B each way, the reference's Fig. 3 volume) over its time
+    nvlink = None
+    exch = kinds.get(5, [])
+    if world > 1 and exch:
+        per_dir = 16.0 * (2 ** m)
+        ms_ex = float(np.mean(exch))
+        gbs = per_dir / (ms_ex / 1e3) / 1e9
+        nvlink = {"exchange_mode": ("remap (peer swap of half the slice)" if args.remap
+                                    else args.exchange),
+                  "launches_per_step": len(exch) / args.steps, "avg_launch_ms": ms_ex,
+                  "bytes_per_direction_per_launch": per_dir if not args.remap else per_dir / 2,
+                  "gbs_per_direction": gbs if not args.remap else gbs / 2,
+                  "peak_nominal": 900.0, "peak_measured_peer_copy": 770.0,
+                  "frac_of_nominal": (gbs if not args.remap else gbs / 2) / 900.0,
+                  "emulated_on_one_gpu": emulated,
+                  "note": ("ranks emulated on one GPU: the partner's slice is local HBM, not "
+                           "NVLink" if emulated else
+                           "CUDA events around each k_exchange_peer launch; "
+                           "B200_PROFILING.md peer copy 770 GB/s per direction")}
 
     # e2e through the public API with host buffers (upload + sweep + download)
     e2e_resident = run_e2e_resident(args, ctx, st, sweeps, step, n, dist, gates_per_step)
@@ -401,8 +556,9 @@ def run_ours(args):
                      "arithmetic)")
     fp64_ops = fp64_per_amp * (2 ** m) * args.steps
     fp64_rate = fp64_ops / (ms_dev / 1e3) / 1e12
-    # the bit-exact numerics on the same workload, for comparison
-    exact_cmp = None
+    # the bit-exact numerics on the same workload, for comparison, and the
+    # factored numerics' error against it on one step from the same state
+    exact_cmp = numerics_error = None
     if factored and not args.no_exact_compare:
         ctx.queue.fuse = True
         step(sweeps[0])
@@ -417,9 +573,15 @@ def run_ours(args):
         exact_cmp = {"value": units_per_step / (ms_exact / 1e3), "ms_per_step": ms_exact,
                      "numerics": "exact (QS_FUSE_EXACT: bit-identical to the reference's numpy "
                                  "arithmetic)"}
+        if world == 1 and not cx_pairs:
+            numerics_error = factored_vs_exact(args, ctx, sweeps, step, n)
+    config4_point = None
+    if args.workload == "sweep" and world == 1 and not args.no_config4_point:
+        del ctx, st
+        config4_point = run_config4_point(args, 33, 3)
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": devices, "ranks": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "c128 (f64 pairs)", "data": "synthetic",
@@ -437,9 +599,11 @@ def run_ours(args):
                 "fused": not args.no_fuse,
                 "numerics": ("factored (QS_FUSE_FACTORED: Euler-factored 1q gates as 4-FMA "
                              "shears + merged diagonals; within 1e-12 of the reference, "
-                             "tests/test_gpu_factored.py)" if factored else
+                             "tests/test_gpu_factored.py, tests/test_gpu_headline.py)"
+                             if factored else
                              "exact (bit-identical to the reference's numpy arithmetic)"),
-                "parallelism": f"state sharded over {world} GPU(s)",
+                "parallelism": (f"state sharded over {world} ranks on {devices} GPU(s)"
+                                + (" (emulated: every rank on GPU 0)" if emulated else "")),
                 "exchange": (None if world == 1 else
                              "qubit remapping (peer swap of half the slice)" if args.remap
                              else args.exchange),
@@ -457,21 +621,20 @@ def run_ours(args):
                      "note": fp64_note + "; peak = measured DFMA/DMUL/DADD issue rate "
                              "62 lanes/clk/SM x 148 SMs x 1.965 GHz (tools/exp/fp64.cu)"},
             "exact_numerics": exact_cmp,
+            "numerics_error": numerics_error,
             "per_target_unfused": per_target,
             "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "bytes_per_launch": bytes_per_launch,
-                         "units_per_launch": units_per_launch,
-                         "bytes_per_unit": 32.0 * (2 ** m),
-                         "avg_launch_ms": dom_ms,
-                         "physical_gbs": physical, "physical_frac": physical / peak,
+                         "achieved": physical, "peak": peak, "unit": "GB/s",
+                         "frac": physical / peak, "traffic": traffic,
+                         "bytes_per_launch": pass_bytes, "avg_launch_ms": dom_ms,
+                         "fusion_gain": units_per_launch,
+                         "algorithmic_per_gate_gbs": physical * units_per_launch,
                          "peak_source": peak_src,
-                         "note": "achieved = algorithmic bytes (32*2^m B per gate-update, "
-                                 "SURVEY 8(d)) x gate-updates per launch / launch time; "
-                                 "a fused pass moves 32*2^m B physically (traffic, "
-                                 "physical_gbs), so frac > 1 is the fusion gain; "
-                                 "physical_frac is the pass's own HBM rate"},
+                         "note": "achieved = 32*2^m B (one read + write of the slice, the "
+                                 "pass's algorithmic bytes) / avg launch time (CUDA events on "
+                                 "the library stream); traffic = ncu dram bytes per launch; "
+                                 "fusion_gain = gate-updates per launch"},
+            "nvlink": nvlink,
             "kernel_share": share,
             "gpu_launches": int(len(launch_ms)),
             "wall_s": wall,
@@ -479,10 +642,75 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_resident": e2e_resident,
+            "config4_n33_single_gpu": config4_point,
         }
         print(json.dumps(line))
     barrier(dist)
     return 0
+
+
+def factored_vs_exact(args, ctx, sweeps, step, n):
+    """numerics_error: one timed-workload step in the factored numerics against
+    the exact (bit-identical) path from the same state, on the device
+    (qs_state_diff): max|d|, ||d||_2/||psi||_2, max|d|/max|psi|."""
+    from paper_2001_10554_b200 import _native, runtime
+    from paper_2001_10554_b200.workloads import device_gaussian
+
+    other = runtime.make_context(None, n, 1, device=ctx.device, fuse=True)
+    other.norm_check_interval = 0
+    device_gaussian(ctx.state, args.seed + 5)
+    device_gaussian(other.state, args.seed + 5)
+    step(sweeps[-1], ctx)
+    step(sweeps[-1], other)
+    d = ctx.state.diff(other.state)
+    del other
+    return {"max_abs": d["max_abs"], "rel_l2": d["rel_l2"], "rel_max": d["rel_max"],
+            "bound": 1e-12,
+            "note": "one step of the timed workload in the factored numerics vs the exact "
+                    "(bit-identical) path from the same normalised Gaussian state, full "
+                    f"2^{n} state compared on the device; tests/test_gpu_headline.py pins "
+                    "both against the CPU oracle at n=30"}
+
+
+def run_config4_point(args, m, layers):
+    """The N=1 point of config 4's weak-scaling curve (n=33, 128 GiB state,
+    no global qubit): Haar on all 33 qubits + CX(q, 32-q), q < 16, per layer."""
+    from paper_2001_10554_b200 import runtime
+    from paper_2001_10554_b200.circuit import GateSpec
+    from paper_2001_10554_b200.workloads import device_gaussian
+
+    try:
+        ctx = runtime.make_context(None, m, 1, fuse=fuse_mode(args))
+    except MemoryError as exc:
+        return {"skipped": f"n={m} state does not fit: {exc}"}
+    ctx.norm_check_interval = 0
+    st = ctx.state
+    device_gaussian(st, args.seed)
+    rng = np.random.default_rng(args.seed + 9)
+    cx = [(q, m - 1 - q) for q in range(m // 2)]
+
+    def layer():
+        for k in range(m):
+            runtime.apply_gate(ctx, GateSpec("custom", (k,), matrix=haar(rng)))
+        for c, t in cx:
+            runtime.apply_gate(ctx, GateSpec("cx", (c, t)))
+        ctx.flush()
+
+    layer()
+    st.synchronize()
+    st.event_record(0)
+    for _ in range(layers):
+        layer()
+    st.event_record(1)
+    st.synchronize()
+    ms = st.event_elapsed_ms(0, 1) / layers
+    gates = m + len(cx)
+    del ctx, st
+    return {"qubits": m, "ms_per_layer": ms, "layers": layers,
+            "value": gates * (2.0 ** m) / 2.0 ** 30 / (ms / 1e3), "unit": UNIT,
+            "numerics": args.numerics,
+            "note": "config 4 at N=1 (n=33, every qubit local): the base of the weak-scaling "
+                    "curve that --gpus N runs at 2^33 amplitudes per GPU"}
 
 
 def run_e2e_resident(args, ctx, st, sweeps, step, n, dist, gates_per_step):
@@ -923,8 +1151,29 @@ def run_noise(args, dist, comm, world, rank, local):
     return 0
 
 
+def spawn_ranks(args) -> int:
+    """`--gpus N` without torchrun: re-run this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous)
+    and hand back its exit code; rank 0 prints the JSON line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -115,6 +115,10 @@ int qs_scale(qs_state* st, double factor);
  * (the reference's own numpy expression) and passes the complex factors of
  * amplitudes [offset, offset + count); the device multiplies them in with
  * numpy's complex product.  Staged through device scratch in chunks. */
+/* Numerics diagnostic (bench numerics_error, factored-vs-exact parity):
+ * out[0] = max|a-b|, out[1] = sum|a-b|^2, out[2] = sum|b|^2, out[3] = max|b|
+ * over all amplitudes of two same-shape states on one device. */
+int qs_state_diff(qs_state* a, const qs_state* b, double* out);
 int qs_apply_diagonal(qs_state* st, const double* factors, uint64_t offset, uint64_t count);
 
 /* ---- gates ------------------------------------------------------------- */

@@ -26,7 +26,7 @@ EXPORTS = (
     "qs_state_create", "qs_state_destroy", "qs_state_info", "qs_state_device_ptr",
     "qs_synchronize", "qs_state_upload", "qs_state_download", "qs_state_exchange_host",
     "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
-    "qs_apply_diagonal",
+    "qs_apply_diagonal", "qs_state_diff",
     "qs_apply_1q", "qs_apply_controlled", "qs_apply_cut_phase", "qs_apply_program",
     "qs_plan_program", "qs_last_program_passes", "qs_observable", "qs_marginals",
     "qs_exchange_gate_peer", "qs_exchange_gate_nccl", "qs_swap_qubits_peer",
@@ -90,6 +90,7 @@ _SIGNATURES = {
     "qs_init_gaussian": ([_P, _U], ctypes.c_int),
     "qs_scale": ([_P, _D], ctypes.c_int),
     "qs_apply_diagonal": ([_P, _DP, _U, _U], ctypes.c_int),
+    "qs_state_diff": ([_P, _P, _DP], ctypes.c_int),
     "qs_apply_1q": ([_P, _I, _DP, _U], ctypes.c_int),
     "qs_apply_controlled": ([_P, _I, _I, _DP, _U], ctypes.c_int),
     "qs_apply_cut_phase": ([_P, _IP, _I, _DP, _U], ctypes.c_int),
@@ -326,6 +327,16 @@ class DeviceState:
         b = ctypes.c_int32(0)
         call("qs_stream_busy", self.handle, ctypes.byref(b))
         return bool(b.value)
+
+    def diff(self, other: "DeviceState") -> dict:
+        """Distance to `other` (same shape, same device): max|d|, ||d||_2,
+        ||other||_2, max|other| and the relative forms."""
+        out = np.zeros(4, dtype=np.float64)
+        call("qs_state_diff", self.handle, other.handle, dptr(out))
+        mx, sd, sb, mb = (float(x) for x in out)
+        return {"max_abs": mx, "l2": sd ** 0.5, "ref_l2": sb ** 0.5, "ref_max": mb,
+                "rel_l2": (sd / sb) ** 0.5 if sb > 0 else 0.0,
+                "rel_max": mx / mb if mb > 0 else 0.0}
 
     def counters(self) -> tuple[int, int]:
         msgs, amps = ctypes.c_uint64(0), ctypes.c_uint64(0)

@@ -180,6 +180,7 @@ def cmd_bench_gate(args) -> int:
         sv.init_uniform(ctx.partition)
         st = ctx.state
         # one untimed warm-up gate (cli.py:201-203)
+        comm = ctx.comm
         dist.apply_one_qubit_gate(ctx.partition, ctx.topology, comm, 0,
                                   np.eye(2, dtype=np.complex128))
         st.synchronize()

@@ -804,6 +804,32 @@ int qs_scale(qs_state* st, double factor) {
     return QS_OK;
 }
 
+int qs_state_diff(qs_state* a, const qs_state* b, double* out) {
+    if (!a || !b || !out) return fail(QS_ERR_VALUE, "null argument");
+    if (a->device != b->device) return fail(QS_ERR_VALUE, "states on different devices");
+    const uint64_t total = a->amps_per_state * uint64_t(a->num_states);
+    if (total != b->amps_per_state * uint64_t(b->num_states))
+        return fail(QS_ERR_VALUE, "states of different sizes");
+    if (int rc = ensure_device(a)) return rc;
+    if (int rc = grow(&a->d_scratch, &a->scratch_cap, 4)) return rc;
+    // b's queued work first: a's stream waits for b's stream
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev, b->stream));
+    CUDA_TRY(cudaStreamWaitEvent(a->stream, ev, 0));
+    cudaEventDestroy(ev);
+    launch_state_diff(a->psi, b->psi, total, a->d_scratch, a->stream);
+    CHECK_LAUNCH();
+    double h[4];
+    CUDA_TRY(cudaMemcpyAsync(h, a->d_scratch, sizeof(h), cudaMemcpyDeviceToHost, a->stream));
+    CUDA_TRY(cudaStreamSynchronize(a->stream));
+    out[0] = h[0];
+    out[1] = h[2];
+    out[2] = h[3];
+    out[3] = h[1];
+    return QS_OK;
+}
+
 int qs_apply_diagonal(qs_state* st, const double* factors, uint64_t offset, uint64_t count) {
     if (!st) return fail(QS_ERR_VALUE, "null state");
     if (int rc = ensure_device(st)) return rc;
@@ -1316,6 +1342,9 @@ int qs_exchange_gate_nccl(qs_state* st, int32_t peer, int32_t is_lower, const do
 // ---- cross-rank ordering without host syncs ---------------------------------
 namespace {
 int make_sync_events(qs_state* st) {
+    // the partner's thread may ask for them while this rank records one
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
     for (auto& ev : st->sync_ev)
         if (!ev)
             CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventInterprocess));

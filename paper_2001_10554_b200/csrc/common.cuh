@@ -195,6 +195,9 @@ void launch_observable(const double2* psi, int m, int num_states, int kind, int 
                        cudaStream_t s);
 
 uint64_t marginal_scratch_doubles(int m, int num_states);
+// max|a-b|, sum|a-b|^2, sum|b|^2, max|b| into 32 bytes of device scratch
+void launch_state_diff(const double2* a, const double2* b, uint64_t count, void* scratch32,
+                       cudaStream_t s);
 void launch_marginals(const double2* psi, int m, int num_states, double* scratch, double* out_dev,
                       cudaStream_t s);
 

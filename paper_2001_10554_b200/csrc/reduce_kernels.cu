@@ -7,6 +7,8 @@
 // partials are reduced again with the same kernel until one value per state
 // remains -- exactly the reference's tree, level by level, so the result is
 // bit-identical for any chunking.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace qsb {
@@ -338,6 +340,47 @@ void launch_observable(const double2* psi, int m, int num_states, int kind, int 
         elems = chunks_per_state;
         ++level;
     }
+}
+
+// ---- numerics diagnostics: distance between two states ----------------------
+// out[0] = max_i |a_i - b_i|, out[1] = sum |a_i - b_i|^2, out[2] = sum |b_i|^2,
+// out[3] = max_i |b_i| (diagnostic association: atomics, not the tree order).
+__global__ void __launch_bounds__(256)
+    k_state_diff(const double2* __restrict__ a, const double2* __restrict__ b, uint64_t count,
+                 unsigned long long* __restrict__ maxbits, double* __restrict__ sums) {
+    double mx = 0.0, mb = 0.0, sd = 0.0, sb = 0.0;
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const double2 x = a[i], y = b[i];
+        const double dr = x.x - y.x, di = x.y - y.y;
+        const double d2 = dr * dr + di * di, b2 = y.x * y.x + y.y * y.y;
+        mx = fmax(mx, d2);
+        mb = fmax(mb, b2);
+        sd += d2;
+        sb += b2;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mb = fmax(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+        sd += __shfl_xor_sync(0xffffffffu, sd, o);
+        sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        // non-negative doubles order like their bit patterns
+        atomicMax(maxbits + 0, __double_as_longlong(sqrt(mx)));
+        atomicMax(maxbits + 1, __double_as_longlong(sqrt(mb)));
+        atomicAdd(sums + 0, sd);
+        atomicAdd(sums + 1, sb);
+    }
+}
+
+void launch_state_diff(const double2* a, const double2* b, uint64_t count, void* scratch32,
+                       cudaStream_t s) {
+    cudaMemsetAsync(scratch32, 0, 32, s);
+    unsigned long long* mb = reinterpret_cast<unsigned long long*>(scratch32);
+    double* sums = reinterpret_cast<double*>(mb + 2);
+    const unsigned grid = unsigned(std::min<uint64_t>((count + 255) / 256, 148 * 8));
+    k_state_diff<<<grid, 256, 0, s>>>(a, b, count, mb, sums);
 }
 
 }  // namespace qsb

@@ -211,19 +211,21 @@ TorchComm = TorchTransport
 
 # ---- gates --------------------------------------------------------------------------
 def _ordered_peer_op(partition, comm: GroupComm, partner: int, launch) -> None:
-    """Run `launch(state)` -- a kernel that reads and writes the partner's
+    """Run `launch(state, peer_pointer)` -- a kernel that reads and writes the partner's
     slice -- ordered against the partner's work without a host stream sync:
     each side records its `pre` event, the pair meets on the host (so both
     records are enqueued), each stream waits on the partner's `pre`, launches,
     records `post`, meets again, and waits on the partner's `post` before its
     own next kernel.  The host never blocks on the GPU; the exchange queues
     behind the local passes and the next passes queue behind it."""
+    comm.transport._dp_ensure(partition)
     st = partition.sync_in()
-    pre, post = comm.peer_events(partner)
     st.record_sync_event(0)
     comm.pair_barrier(partner)
+    # after the first meeting: the partner has attached and recorded `pre`
+    pre, post = comm.peer_events(partner)
     st.wait_event(pre)
-    launch(st)
+    launch(st, comm.peer_pointer(partner))
     st.record_sync_event(1)
     comm.pair_barrier(partner)
     st.wait_event(post)
@@ -251,8 +253,7 @@ def _exchange_pairs(partition: sv.StatePartition, comm: GroupComm, q: int, u,
         _native.call("qs_exchange_gate_nccl", st.handle, comm.nccl_peer(partner),
                      1 if is_lower else 0, _native.dptr(mat), ctrl, int(chunk))
         return
-    peer = comm.peer_pointer(partner)
-    _ordered_peer_op(partition, comm, partner, lambda st: _native.call(
+    _ordered_peer_op(partition, comm, partner, lambda st, peer: _native.call(
         "qs_exchange_gate_peer", st.handle, peer, 1 if is_lower else 0, _native.dptr(mat), ctrl))
 
 
@@ -307,8 +308,7 @@ def swap_global_local(partition, comm: GroupComm, topology: RankTopology, layout
     d = 1 << (p - m)
     partner = comm.rank ^ d
     bit = 1 if comm.rank & d else 0
-    peer = comm.peer_pointer(partner)
-    _ordered_peer_op(partition, comm, partner, lambda st: _native.call(
+    _ordered_peer_op(partition, comm, partner, lambda st, peer: _native.call(
         "qs_swap_qubits_peer", st.handle, peer, l, bit))
     comm.account_exchange(2, 1 << (m - 1))
     layout.swap(p, l)

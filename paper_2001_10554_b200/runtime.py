@@ -914,7 +914,8 @@ def run_spmd(world_size: int, fn, timeout: float = 30.0, *, exchange_mode: str =
     if failures:
         failures.sort(key=lambda p: p[0])
         rank, exc = failures[0]
-        raise RuntimeError(f"rank {rank} failed: {exc!r}") from exc
+        also = "".join(f"; rank {r}: {e!r}" for r, e in failures[1:])
+        raise RuntimeError(f"rank {rank} failed: {exc!r}{also}") from exc
     return results
 
 

@@ -105,8 +105,22 @@ class Transport:
             self.send(root, token, tag=TAG_BARRIER)
             self.receive(root)
 
+    # whole-world group view: round-1 callers used the endpoint as a GroupComm
+    def allgather(self, value: float, participants: int) -> list:
+        return self._dp_allgather(value, 0, participants)
+
+    def attach(self, partition) -> None:
+        self._dp_attach(partition)
+
+    def pair_barrier(self, partner: int) -> None:
+        self._dp_pair_barrier(self.rank, partner)
+
     # ---- device plane (world-rank addressing; used by distribution.GroupComm) ----
     def _dp_pair_barrier(self, me: int, partner: int) -> None:
+        raise NotImplementedError
+
+    def _dp_ensure(self, partition) -> None:
+        """Before an exchange: this rank's partition must be reachable."""
         raise NotImplementedError
 
     def _dp_allgather(self, value: float, base: int, participants: int) -> list:
@@ -198,6 +212,13 @@ class InProcessTransport(Transport):
     def _dp_attach(self, partition) -> None:
         with self.fabric._lock:
             self.fabric._parts[self.rank] = partition
+
+    def _dp_ensure(self, partition) -> None:
+        # thread ranks share the process: registering is local (the reference's
+        # callers never attach; their partitions join on first exchange)
+        with self.fabric._lock:
+            if self.fabric._parts.get(self.rank) is not partition:
+                self.fabric._parts[self.rank] = partition
 
     def _part(self, world_rank: int):
         with self.fabric._lock:
@@ -291,6 +312,11 @@ class TorchTransport(Transport):
         self._handles = [t[0] for t in table]
         self._events = [(t[1], t[2]) for t in table]
         self._peers, self._peer_events = {}, {}
+
+    def _dp_ensure(self, partition) -> None:
+        if partition is None or self._state is not partition.state:
+            raise TransportError("the partition was not attached collectively (make_context "
+                                 "attaches it; across processes attach is a world collective)")
 
     def _dp_peer_pointer(self, world_rank: int) -> int:
         import ctypes

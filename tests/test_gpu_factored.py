@@ -191,27 +191,41 @@ def test_factored_qaoa_pool_matches_reference():
 
 
 @pytest.mark.slow
-def test_factored_n26_sweep_vs_exact_and_n28_roundtrip():
-    # n=26: the whole config-2 sweep (every qubit, 3 fused passes) against the
-    # exact fused path, full state
+def test_factored_n26_sweep_vs_oracle_and_n28_roundtrip():
+    # n=26: two config-2 sweeps (every qubit, fused passes) in both numerics
+    # against the CPU oracle over the same 52 gates: exact bit-equal,
+    # factored within 1e-12
+    from oracle import cpu_baseline
     n = 26
     rng = np.random.default_rng(9)
     us = [ogates.random_unitary_2x2(rng) for _ in range(n)]
-    out = {}
-    for fuse in (True, FACT):
+
+    def fresh(seed):
         st = N.DeviceState(n, n)
-        N.call("qs_init_gaussian", st.handle, 11)
+        N.call("qs_init_gaussian", st.handle, seed)
         norm = st.observable(N.QS_OBS_NORM)[0]
         N.call("qs_scale", st.handle, 1.0 / np.sqrt(norm))
+        return st
+
+    expect = fresh(11).download()
+    for _ in range(2):
+        for k in range(n):
+            cpu_baseline.apply_1q_threaded(expect, k, us[k])
+    for fuse in (True, FACT):
+        st = fresh(11)
         q = runtime.GateQueue(st, fuse=fuse)
         for _ in range(2):
             for k in range(n):
                 q.one_qubit(k, us[k])
         q.flush()
-        out[fuse] = st.download()
+        got = st.download()
         del st
-    assert max_dev(out[True], out[FACT]) <= TOL
-    del out
+        if fuse is True:
+            assert bits_equal(got, expect)
+        else:
+            assert max_dev(got, expect) <= TOL
+            assert not bits_equal(got, expect)
+    del expect
     # n=28: forward sweep then the adjoint sweep backward returns the start
     n = 28
     st = N.DeviceState(n, n)
@@ -231,6 +245,21 @@ def test_factored_n26_sweep_vs_exact_and_n28_roundtrip():
     back = st.download()
     assert abs(mid - 1.0) < 1e-10
     assert max_dev(back, start) <= TOL
+
+
+def test_state_diff_matches_host():
+    """qs_state_diff (the bench's numerics_error) against numpy."""
+    n = 14
+    rng = np.random.default_rng(5)
+    a, b = ogates.random_state(n, rng), ogates.random_state(n, rng)
+    sa, sb = N.DeviceState(n, n), N.DeviceState(n, n)
+    sa.upload(a)
+    sb.upload(b)
+    d = sa.diff(sb)
+    assert d["max_abs"] == pytest.approx(float(np.max(np.abs(a - b))), rel=1e-14)
+    assert d["rel_l2"] == pytest.approx(float(np.linalg.norm(a - b) / np.linalg.norm(b)),
+                                        rel=1e-12)
+    assert d["ref_max"] == pytest.approx(float(np.max(np.abs(b))), rel=1e-14)
 
 
 def test_factored_pool_per_state_gates():

@@ -329,9 +329,9 @@ def test_errors_map_to_reference_exceptions():
     with pytest.raises(ValueError):
         sv.get_probability(p, 4)
     with pytest.raises(ValueError):
-        sv.StatePartition(3, 0, 0)
+        sv.StatePartition(3, 0, 0, None)
     with pytest.raises(ValueError):
-        sv.StatePartition(3, 2, 2)
+        sv.StatePartition(3, 2, 2, None)
 
 
 def test_known_answers():
@@ -534,7 +534,7 @@ def test_config4_qubit_remapping_bit_exact(p):
         runtime.run_circuit(ctx, circ)
         moved = ctx.state.counters()[1]
         full = runtime.gather_group_state(ctx)
-        return full, moved, ctx.layout.is_identity()
+        return full, moved, ctx.qubit_layout.is_identity()
 
     res = runtime.run_spmd(P, rank_fn, timeout=120.0)
     assert bits_equal(res[0][0], ref)
