@@ -108,12 +108,11 @@ class _HostMirror(np.ndarray):
     _WRITERS = ("copyto", "place", "put", "putmask", "put_along_axis", "fill_diagonal")
 
     def __array_function__(self, func, types, args, kwargs):
-        plain = tuple(a.view(np.ndarray) if isinstance(a, _HostMirror) else a for a in args)
-        res = func(*plain, **kwargs)
+        res = super().__array_function__(func, types, args, kwargs)
         if func.__name__ in self._WRITERS and args and isinstance(args[0], _HostMirror):
             args[0]._touch()
-        if isinstance(res, _HostMirror):
-            res = res.view(np.ndarray)
+        if isinstance(res, _HostMirror) and res.base is None:
+            res = res.view(np.ndarray)  # a fresh array, not a view of the slice
         return res
 
     def fill(self, value):
