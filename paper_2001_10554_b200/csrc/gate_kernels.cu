@@ -10,9 +10,13 @@
 //  k_tile        fused pass: a 2^12-amplitude tile in shared memory, gates
 //                applied in program order in register "rounds" of 4 qubits;
 //                one HBM read + write for a whole run of gates.
+#include <cuda.h>
+
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 
@@ -1198,6 +1202,494 @@ void launch_fact(double2* psi, const FactPass& F, const double* mats, const CutT
     }
 }
 
+// ---- lean factored pass with TMA tile movement ----------------------------------
+// k_fact_tma: one CTA per SM, two groups of 256 threads.  A tile is fetched by
+// ONE tensor-map TMA (cp.async.bulk.tensor, SWIZZLE_128B) into a landing buffer
+// L that is separate from the groups' reslice buffers W0/W1 (the round-1
+// k_fact landed each tile in its single working buffer, so the next tile could
+// only be requested in the last round).  Tiles alternate between the groups;
+// group g reads its tile out of L in round 0 (straight into registers) and, as
+// soon as the group has read it, one thread requests the next tile -- the other
+// group's -- into L, so a load is in flight while both groups compute.  Landing
+// is signalled on one mbarrier per group (expect_tx = 64 KiB).  The tile's
+// shared-memory layout is the TMA layout: tile position p sits at smem bit
+// pi(p) (the tensor map's dim order) and 16-byte chunks are XOR-swizzled with
+// smem bits 3..5 (SWIZZLE_128B); the host planner (tma_plan) picks the dim
+// order so that every register round's quarter-warp lanes hit 8 distinct bank
+// groups, and rewrites the rounds' swizzled deposit tables for that layout,
+// so the round bodies are k_fact's.
+struct alignas(64) TmaPass {
+    CUtensorMap map;             // 128 bytes, 64-byte aligned
+    int32_t rank;                // tensor dims (2..5)
+    int32_t ncoord;              // dims whose coordinate comes from the tile index
+    int32_t coord_dim[4];
+    int32_t coord_shift[4];
+    uint64_t coord_mask[4];      // ~0 for the top field
+    int32_t sig[kTileLog2];      // smem index of each tile-position basis vector
+};
+
+constexpr int kTmaThreads = 2 * kTileThreads;
+constexpr uint32_t kTileBytes = uint32_t(sizeof(double2)) * kTileAmps;
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    unsigned done = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
+// thread-uniform: issue the whole tile as one tensor copy, landing on `bar`
+__device__ __forceinline__ void tma_load_tile(const TmaPass& T, uint64_t tile, double2* dst,
+                                              uint64_t* bar) {
+    int c[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (i < T.ncoord) c[T.coord_dim[i]] = int((tile >> T.coord_shift[i]) & T.coord_mask[i]);
+    const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kTileBytes)
+                 : "memory");
+    const void* map = &T.map;
+    switch (T.rank) {
+        case 2:
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(d), "l"(map), "r"(c[0]), "r"(c[1]), "r"(b)
+                : "memory");
+            break;
+        case 3:
+            asm volatile(
+                "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(d), "l"(map), "r"(c[0]), "r"(c[1]),
+                "r"(c[2]), "r"(b)
+                : "memory");
+            break;
+        case 4:
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(d), "l"(map), "r"(c[0]), "r"(c[1]),
+                "r"(c[2]), "r"(c[3]), "r"(b)
+                : "memory");
+            break;
+        default:
+            asm volatile(
+                "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(d), "l"(map), "r"(c[0]),
+                "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b)
+                : "memory");
+            break;
+    }
+}
+
+template <bool TABLES, bool PHASE>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    k_fact_tma(double2* __restrict__ psi, const __grid_constant__ FactPass P,
+               const double* __restrict__ mats, const __grid_constant__ CutTerms ct,
+               const __grid_constant__ TmaPass T) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double2* Lbuf = reinterpret_cast<double2*>(smem_raw);
+    uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + 3 * kTileBytes);
+    uint64_t* dep = rowoff + (kTileAmps >> kLowBits);
+    uint32_t* rlo = reinterpret_cast<uint32_t*>(dep + 256 * kDepTables);
+    uint32_t* rhi = rlo + kMaxRounds * (1 << kLaneLoBits);
+    uint64_t* full = reinterpret_cast<uint64_t*>(rhi + kMaxRounds * (1 << kLaneHiBits));
+    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneLoBits); i += kTmaThreads) {
+        const Round& R = P.rounds[i >> kLaneLoBits];
+        const int v = i & ((1 << kLaneLoBits) - 1);
+        rlo[i] = uint32_t(R.dlo[v]) | (uint32_t(R.slo[v]) << 16);
+    }
+    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneHiBits); i += kTmaThreads) {
+        const Round& R = P.rounds[i >> kLaneHiBits];
+        const int v = i & ((1 << kLaneHiBits) - 1);
+        rhi[i] = uint32_t(R.dhi[v]) | (uint32_t(R.shi[v]) << 16);
+    }
+    const int low_run = P.low_run;
+    const int nrows = kTileAmps >> low_run;
+    const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
+    for (int r = threadIdx.x; r < nrows; r += kTmaThreads) {
+        uint64_t off = 0;
+        for (int k = 0; k < kTileLog2 - low_run; ++k)
+            if ((r >> k) & 1) off |= uint64_t(1) << P.tile_bits[low_run + k];
+        rowoff[r] = off;
+    }
+    for (int i = threadIdx.x; i < kDepTables * 256; i += kTmaThreads) {
+        const int c = i >> 8, v = i & 255;
+        uint64_t out = 0;
+        for (int b = 0; b < 8; ++b) {
+            if (!((v >> b) & 1)) continue;
+            int want = 8 * c + b, cnt = 0;
+            for (int q = 0, k = 0; q < P.m; ++q) {
+                if (k < kTileLog2 && P.tile_bits[k] == q) {
+                    ++k;
+                    continue;
+                }
+                if (cnt++ == want) {
+                    out |= uint64_t(1) << q;
+                    break;
+                }
+            }
+        }
+        dep[i] = out;
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(full + 0, 1);
+        mbar_init(full + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < P.num_tiles) tma_load_tile(T, blockIdx.x, Lbuf, full);
+
+    const int group = threadIdx.x / kTileThreads;  // warp-uniform
+    const int tid = threadIdx.x % kTileThreads;
+    const int gbar = 1 + group;
+    double2* W = Lbuf + kTileAmps * (1 + group);
+    const int m = P.m;
+    const int tps_log2 = m - kTileLog2;
+    auto tile_base = [&](uint64_t t) {
+        const uint64_t x = t & (P.tiles_per_state - 1);
+        uint64_t out = 0;
+#pragma unroll
+        for (int c = 0; c < kDepTables; ++c) out |= dep[(c << 8) | ((x >> (8 * c)) & 255)];
+        return out;
+    };
+    auto goff = [&](int e) { return rowoff[e >> low_run] + (uint64_t(e) & lowmask); };
+    auto sig_of = [&](int e) {
+        int v = 0;
+#pragma unroll
+        for (int b = 0; b < kTileLog2; ++b)
+            if ((e >> b) & 1) v ^= T.sig[b];
+        return v;
+    };
+    const bool direct = P.direct_store != 0;
+    unsigned parity = 0;
+    for (uint64_t k = group;; k += 2, parity ^= 1) {
+        const uint64_t tile_id = blockIdx.x + k * gridDim.x;
+        if (tile_id >= P.num_tiles) break;
+        const uint64_t st = tile_id >> tps_log2;
+        const uint64_t base_local = tile_base(tile_id);
+        double2* gbase = psi + ((st << m) | base_local);
+        mbar_wait(full + group, parity);
+        for (int r = 0; r < P.num_rounds; ++r) {
+            const Round& R = P.rounds[r];
+            const bool last = r == P.num_rounds - 1;
+            const uint32_t lo = rlo[(r << kLaneLoBits) | (tid & ((1 << kLaneLoBits) - 1))];
+            const uint32_t hi = rhi[(r << kLaneHiBits) | (tid >> kLaneLoBits)];
+            const int eb = int((lo | hi) & 0xffff);
+            const int sb = int((lo ^ hi) >> 16);
+            int skb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) skb[j] = R.sk[1 << j];
+            auto sk_of = [&](int kk) {
+                int v = 0;
+#pragma unroll
+                for (int j = 0; j < kRegLog2; ++j)
+                    if ((kk >> j) & 1) v ^= skb[j];
+                return v;
+            };
+            const double2* src = r == 0 ? Lbuf : W;
+            double2 a[kRegAmps];
+#pragma unroll
+            for (int kk = 0; kk < kRegAmps; ++kk) a[kk] = src[sb ^ sk_of(kk)];
+            if (r == 0) {
+                // the group has read L: request the next tile (the other group's)
+                named_sync(gbar, kTileThreads);
+                if (tid == 0) {
+                    const uint64_t next = blockIdx.x + (k + 1) * gridDim.x;
+                    if (next < P.num_tiles) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        tma_load_tile(T, next, Lbuf, full + ((k + 1) & 1));
+                    }
+                }
+            }
+            const FactRound& F = P.fr[r];
+            const bool gstore = last && direct;
+            const int sel = int(r == 0 && P.has_din) | (F.pre_any ? 2 : 0) |
+                            int(last && P.has_dout) << 2 | int(gstore) << 3;
+            const uint64_t il = base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask);
+            uint64_t okb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) okb[j] = gstore ? goff(R.dk[1 << j]) : 0;
+            double2* gb = gbase + (gstore ? goff(eb) : 0);
+            if (PHASE && F.mid) {
+                QSB_FB(TABLES, (PHASE && true), sel, a, P, R, F, ct, mats, st, il, W, sb, skb, gb, okb)
+            } else {
+                QSB_FB(TABLES, false, sel, a, P, R, F, ct, mats, st, il, W, sb, skb, gb, okb)
+            }
+            if (gstore) break;
+            named_sync(gbar, kTileThreads);
+        }
+        if (!direct) {
+            double2* gb = gbase + goff(tid);
+            const int s_tid = sig_of(tid);
+#pragma unroll
+            for (int i = 0; i < kLoadsPerThread; ++i)
+                gb[goff(i * kTileThreads)] = W[s_tid ^ sig_of(i * kTileThreads)];
+        }
+    }
+}
+
+size_t fact_tma_smem_bytes() {
+    return 3 * size_t(kTileBytes) + sizeof(uint64_t) * (kTileAmps >> kLowBits) +
+           sizeof(uint64_t) * 256 * kDepTables +
+           sizeof(uint32_t) * kMaxRounds * ((1 << kLaneLoBits) + (1 << kLaneHiBits)) +
+           2 * sizeof(uint64_t);
+}
+
+// ---- host: the TMA plan of a lean pass ------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = []() -> EncodeTiledFn {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// One dimension of the tensor map: `len` consecutive local qubits from `lo`
+// (tile: box covers them; non-tile: box 1, coordinate = tile-index field),
+// or the pool's state index on top.
+struct TmaDim {
+    int lo, len;
+    bool tile;
+    bool states;        // the top non-tile run merged with the state index
+    int field_shift;    // non-tile: first tile-index bit of this run
+};
+
+// Rewrite the rounds' lane orders and swizzled deposits for smem index
+// sigma(e) = pi(e) ^ ((pi(e) >> 3) & 7), where pi sends tile position p to
+// smem bit pos_bit[p]; lanes 0..2 (a quarter warp) take one position of each
+// bank class, preferring tile positions 0,1,2 (128-byte rows for direct stores).
+bool retarget_rounds(FactPass& F, const int pos_bit[kTileLog2], int sig[kTileLog2]) {
+    auto pi = [&](int e) {
+        int v = 0;
+        for (int p = 0; p < kTileLog2; ++p)
+            if ((e >> p) & 1) v |= 1 << pos_bit[p];
+        return v;
+    };
+    auto sigma = [&](int e) {
+        const int v = pi(e);
+        return v ^ ((v >> 3) & 7);
+    };
+    int cls[kTileLog2];
+    for (int p = 0; p < kTileLog2; ++p) {
+        const int b = pos_bit[p];
+        cls[p] = b < 3 ? b : (b < 6 ? b - 3 : -1);
+        sig[p] = sigma(1 << p);
+    }
+    for (int r = 0; r < F.num_rounds; ++r) {
+        Round& R = F.rounds[r];
+        unsigned regs = 0;
+        for (int j = 0; j < kRegLog2; ++j) regs |= R.dk[1 << j];
+        int lanes[kTileLog2 - kRegLog2], nl = 0;
+        for (int p = 0; p < kTileLog2; ++p)
+            if (!((regs >> p) & 1)) lanes[nl++] = p;
+        if (nl != kTileLog2 - kRegLog2) return false;
+        int order[kTileLog2 - kRegLog2], no = 0;
+        unsigned used = 0;
+        if (!((regs >> 0) & 1) && !((regs >> 1) & 1) && !((regs >> 2) & 1)) {
+            for (int p = 0; p < 3; ++p) order[no++] = p, used |= 1u << p;
+        } else {
+            for (int c = 0; c < 3; ++c) {
+                int pick = -1;
+                for (int i = 0; i < nl && pick < 0; ++i)
+                    if (cls[lanes[i]] == c && !((used >> lanes[i]) & 1)) pick = lanes[i];
+                if (pick < 0) return false;  // a class with no lane: conflicts
+                order[no++] = pick;
+                used |= 1u << pick;
+            }
+        }
+        for (int i = 0; i < nl; ++i)
+            if (!((used >> lanes[i]) & 1)) order[no++] = lanes[i];
+        auto deposit = [](int v, const int* pos, int nbits) {
+            int out = 0;
+            for (int b = 0; b < nbits; ++b)
+                if ((v >> b) & 1) out |= 1 << pos[b];
+            return out;
+        };
+        for (int v = 0; v < (1 << kLaneLoBits); ++v) {
+            R.dlo[v] = uint16_t(deposit(v, order, kLaneLoBits));
+            R.slo[v] = uint16_t(sigma(R.dlo[v]));
+        }
+        for (int v = 0; v < (1 << kLaneHiBits); ++v) {
+            R.dhi[v] = uint16_t(deposit(v, order + kLaneLoBits, kLaneHiBits));
+            R.shi[v] = uint16_t(sigma(R.dhi[v]));
+        }
+        for (int v = 0; v < (1 << kRegLog2); ++v) R.sk[v] = uint16_t(sigma(R.dk[v]));
+    }
+    if (F.direct_store) {
+        // the last round must still put tile positions 0,1,2 on lanes 0..2
+        const Round& R = F.rounds[F.num_rounds - 1];
+        for (int p = 0; p < 3; ++p)
+            if (R.dlo[1 << p] != (1 << p)) return false;
+    }
+    return true;
+}
+
+bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
+    static const bool off = getenv("QSB_NO_TMA") != nullptr;
+    if (off || F.low_run < 3 || !encode_fn()) return false;
+    const int m = F.m;
+    const uint64_t num_states = F.num_tiles / F.tiles_per_state;
+    uint32_t is_tile = 0;  // over local qubits
+    for (int p = 0; p < kTileLog2; ++p) is_tile |= 1u << F.tile_bits[p];
+    if (m > 62) return false;
+    // position of each qubit among the tile positions (or -1)
+    auto pos_of = [&](int q) {
+        for (int p = 0; p < kTileLog2; ++p)
+            if (F.tile_bits[p] == q) return p;
+        return -1;
+    };
+    // maximal runs above qubit 2
+    std::vector<TmaDim> tile_runs, nontile;
+    int below = 0;
+    for (int q = 3; q < m;) {
+        const bool t = q < 32 && ((is_tile >> q) & 1);
+        int e = q;
+        while (e + 1 < m && ((e + 1 < 32 && ((is_tile >> (e + 1)) & 1)) == t)) ++e;
+        TmaDim d{q, e - q + 1, t, false, 0};
+        if (t) {
+            tile_runs.push_back(d);
+        } else {
+            d.field_shift = below;
+            below += d.len;
+            nontile.push_back(d);
+        }
+        q = e + 1;
+    }
+    if (num_states > 1) {
+        if (!nontile.empty() && nontile.back().lo + nontile.back().len == m)
+            nontile.back().states = true;
+        else
+            nontile.push_back(TmaDim{m, 0, false, true, below});
+    }
+    // candidate XOR sources: 3 consecutive positions of one tile run, that
+    // piece first in dim order; the monotone order is tried first
+    struct Cand { int run, start; };
+    std::vector<Cand> cands;
+    for (int i = 0; i < (int)tile_runs.size(); ++i)
+        if (tile_runs[i].len >= 3) cands.push_back({i, tile_runs[i].lo});
+    for (int i = 0; i < (int)tile_runs.size(); ++i)
+        for (int s = tile_runs[i].lo + 1; s + 2 < tile_runs[i].lo + tile_runs[i].len; ++s)
+            cands.push_back({i, s});
+    for (const Cand& c : cands) {
+        // tile pieces: [start, start+len') first (<= 8 qubits), then the rest
+        std::vector<TmaDim> dims;
+        auto push_tile = [&](int lo, int len) {
+            while (len > 0) {
+                const int l = std::min(len, 8);
+                dims.push_back(TmaDim{lo, l, true, false, 0});
+                lo += l;
+                len -= l;
+            }
+        };
+        const TmaDim& R0 = tile_runs[c.run];
+        push_tile(c.start, R0.lo + R0.len - c.start);
+        push_tile(R0.lo, c.start - R0.lo);
+        for (int i = 0; i < (int)tile_runs.size(); ++i)
+            if (i != c.run) push_tile(tile_runs[i].lo, tile_runs[i].len);
+        for (const TmaDim& d : nontile) dims.push_back(d);
+        if (1 + dims.size() > 5) continue;
+        // smem bit of each tile position: dim0 = qubits 0..2, then dim order
+        int pos_bit[kTileLog2], bit = 3;
+        for (int p = 0; p < 3; ++p) pos_bit[p] = p;
+        for (const TmaDim& d : dims)
+            if (d.tile)
+                for (int q = d.lo; q < d.lo + d.len; ++q) pos_bit[pos_of(q)] = bit++;
+        if (bit != kTileLog2) continue;
+        FactPass G = F;
+        int sig[kTileLog2];
+        if (!retarget_rounds(G, pos_bit, sig)) continue;
+        // the tensor map
+        cuuint64_t gdim[5], gstride[4];
+        cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+        gdim[0] = 2u << 3;  // re/im doubles of qubits 0..2
+        box[0] = 16;
+        T->ncoord = 0;
+        for (size_t i = 0; i < dims.size(); ++i) {
+            const TmaDim& d = dims[i];
+            const uint64_t extent = (uint64_t(1) << d.len) * (d.states ? num_states : 1);
+            gdim[i + 1] = extent;
+            gstride[i] = uint64_t(sizeof(double2)) << d.lo;
+            box[i + 1] = d.tile ? (1u << d.len) : 1u;
+            if (!d.tile) {
+                const int k = T->ncoord++;
+                T->coord_dim[k] = int(i + 1);
+                T->coord_shift[k] = d.field_shift;
+                T->coord_mask[k] = d.states ? ~uint64_t(0) : (uint64_t(1) << d.len) - 1;
+            }
+        }
+        const int rank = int(dims.size()) + 1;
+        if (rank < 2) continue;
+        const CUresult rc = encode_fn()(&T->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank),
+                                        psi, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (rc != CUDA_SUCCESS) continue;
+        T->rank = rank;
+        for (int p = 0; p < kTileLog2; ++p) T->sig[p] = sig[p];
+        F = G;
+        return true;
+    }
+    return false;
+}
+
+template <bool TB, bool PH>
+void launch_fact_tma_variant(double2* psi, const FactPass& F, const double* mats,
+                             const CutTerms& ct, const TmaPass& T, cudaStream_t s) {
+    constexpr int kMaxDevices = 64;
+    static std::atomic<int> configured[kMaxDevices];
+    static int sms_of[kMaxDevices];
+    const size_t smem = fact_tma_smem_bytes();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (configured[dev].load(std::memory_order_acquire) == 0) {
+        cudaFuncSetAttribute(k_fact_tma<TB, PH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        sms_of[dev] = sms;
+        configured[dev].store(1, std::memory_order_release);
+    }
+    uint64_t grid = uint64_t(sms_of[dev]);
+    const uint64_t need = (F.num_tiles + 1) / 2;
+    if (grid > need) grid = need;
+    k_fact_tma<TB, PH><<<unsigned(grid), kTmaThreads, smem, s>>>(psi, F, mats, ct, T);
+}
+
+bool launch_fact_tma(double2* psi, FactPass& F, const double* mats, const CutTerms& ct,
+                     bool tables, bool phase, cudaStream_t s) {
+    static thread_local TmaPass T;
+    if (!tma_plan(F, psi, &T)) return false;
+    if (tables) {
+        if (phase) launch_fact_tma_variant<true, true>(psi, F, mats, ct, T, s);
+        else launch_fact_tma_variant<true, false>(psi, F, mats, ct, T, s);
+    } else {
+        if (phase) launch_fact_tma_variant<false, true>(psi, F, mats, ct, T, s);
+        else launch_fact_tma_variant<false, false>(psi, F, mats, ct, T, s);
+    }
+    return true;
+}
+
 __global__ void k_fill(double2* __restrict__ psi, uint64_t count, double2 value) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
          i += uint64_t(gridDim.x) * blockDim.x)
@@ -1354,7 +1846,7 @@ bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_d
         static thread_local FactPass F;
         bool tb = false, ph = false;
         if (fact_pass_from(pass, &F, &tb, &ph)) {
-            launch_fact(psi, F, mats, ct, tb, ph, s);
+            if (!launch_fact_tma(psi, F, mats, ct, tb, ph, s)) launch_fact(psi, F, mats, ct, tb, ph, s);
             return true;
         }
     }
