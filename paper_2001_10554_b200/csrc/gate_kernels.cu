@@ -1226,6 +1226,7 @@ struct alignas(64) TmaPass {
     int32_t coord_shift[4];
     uint64_t coord_mask[4];      // ~0 for the top field
     int32_t sig[kTileLog2];      // smem index of each tile-position basis vector
+    int32_t prefetch;            // L2 prefetch distance in tiles of this CTA
 };
 
 constexpr int kTmaThreads = 2 * kTileThreads;
@@ -1291,6 +1292,40 @@ __device__ __forceinline__ void tma_load_tile(const TmaPass& T, uint64_t tile, d
     }
 }
 
+// L2 prefetch of a whole tile (one instruction): the DRAM read of tile k+d
+// starts while tiles k..k+d-1 are in flight, so the load into L hits L2
+__device__ __forceinline__ void tma_prefetch_tile(const TmaPass& T, uint64_t tile) {
+    int c[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (i < T.ncoord) c[T.coord_dim[i]] = int((tile >> T.coord_shift[i]) & T.coord_mask[i]);
+    const void* map = &T.map;
+    switch (T.rank) {
+        case 2:
+            asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map),
+                         "r"(c[0]), "r"(c[1])
+                         : "memory");
+            break;
+        case 3:
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map),
+                         "r"(c[0]), "r"(c[1]), "r"(c[2])
+                         : "memory");
+            break;
+        case 4:
+            asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                             map),
+                         "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3])
+                         : "memory");
+            break;
+        default:
+            asm volatile(
+                "cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(map),
+                "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4])
+                : "memory");
+            break;
+    }
+}
+
 template <bool TABLES, bool PHASE>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     k_fact_tma(double2* __restrict__ psi, const __grid_constant__ FactPass P,
@@ -1347,7 +1382,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x < P.num_tiles) tma_load_tile(T, blockIdx.x, Lbuf, full);
+    if (threadIdx.x == 0 && blockIdx.x < P.num_tiles) {
+        tma_load_tile(T, blockIdx.x, Lbuf, full);
+        for (int d = 1; d <= T.prefetch; ++d) {
+            const uint64_t t = blockIdx.x + uint64_t(d) * gridDim.x;
+            if (t < P.num_tiles) tma_prefetch_tile(T, t);
+        }
+    }
 
     const int group = threadIdx.x / kTileThreads;  // warp-uniform
     const int tid = threadIdx.x % kTileThreads;
@@ -1409,6 +1450,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         tma_load_tile(T, next, Lbuf, full + ((k + 1) & 1));
                     }
+                    const uint64_t ahead = next + uint64_t(T.prefetch) * gridDim.x;
+                    if (T.prefetch > 0 && ahead < P.num_tiles) tma_prefetch_tile(T, ahead);
                 }
             }
             const FactRound& F = P.fr[r];
@@ -1544,6 +1587,12 @@ bool retarget_rounds(FactPass& F, const int pos_bit[kTileLog2], int sig[kTileLog
     return true;
 }
 
+CUtensorMapL2promotion l2_promotion() {
+    static const int v = getenv("QSB_TMA_PROMO") ? atoi(getenv("QSB_TMA_PROMO")) : 128;
+    return v >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                    : v >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
+
 bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
     static const bool off = getenv("QSB_NO_TMA") != nullptr;
     if (off || F.low_run < 3 || !encode_fn()) return false;
@@ -1641,11 +1690,22 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
         if (rank < 2) continue;
         const CUresult rc = encode_fn()(&T->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank),
                                         psi, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
                                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (rc != CUDA_SUCCESS) continue;
         T->rank = rank;
         for (int p = 0; p < kTileLog2; ++p) T->sig[p] = sig[p];
+        // L2 prefetch of this CTA's tile after next: measured to help tiles of
+        // 128-byte rows spread over a few 2 MiB pages (config-2 pass 2: 7.2 ->
+        // 6.6 ms) and to hurt contiguous tiles and tiles spread over hundreds of
+        // pages (pass 3: 8.1 -> 11.2 ms); QSB_TMA_PF overrides
+        static const int pf_env = getenv("QSB_TMA_PF") ? atoi(getenv("QSB_TMA_PF")) : -1;
+        int high = 0, contiguous = 1;
+        for (int p = 0; p < kTileLog2; ++p) {
+            high += F.tile_bits[p] >= 17;
+            contiguous &= F.tile_bits[p] == p;
+        }
+        T->prefetch = pf_env >= 0 ? pf_env : (!contiguous && high <= 4 ? 1 : 0);
         F = G;
         return true;
     }
