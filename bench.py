@@ -858,44 +858,60 @@ def cpu_qaoa_sample(graph, positions, depth, threads):
 
 
 def run_qaoa(args, dist, comm, world, rank, local):
-    """BASELINE config 5: a pool of 512 QAOA MaxCut circuits (n=20, p=4) per
-    swarm step, split across GPUs in contiguous blocks (no state exchange).
-    A step = reset + 104 gates on every pool state + <C> per state + the
-    host PSO move; parameter tables go host->device and <C> device->host
-    inside every step (so the step is end to end)."""
+    """BASELINE config 5 as the reference's `qpool qaoa-pso --vertices 20
+    --depth 4 --particles 512 --budget 512*K` runs it (cli.py:249-262,
+    optimize.py:172-216): the keyed 3-regular graph
+    random_3regular_graph(20, pool_stream.split(0)), the keyed swarm
+    init_swarm(512, 8, stream=pool_stream.split(1)), and per swarm step all 512
+    particles evaluated as one pool program (reset + 104 gates + <C>), the
+    values shared pool-wide, then step_swarm.  The pool is split across GPUs
+    in contiguous blocks (no state exchange).  Parameter tables go
+    host->device and <C> device->host inside every step (the step is end to
+    end)."""
+    from paper_2001_10554_b200 import optimize as qopt
     from paper_2001_10554_b200 import runtime
     from paper_2001_10554_b200.circuit import build_qaoa_circuit
-    from paper_2001_10554_b200.workloads import random_3regular_graph
+    from paper_2001_10554_b200.noise import SCOPE_POOL, RandomStream
 
     n, depth, S = QAOA_N, QAOA_P, QAOA_POOL
     first, count = runtime.split_pool(S, rank, world)
-    rng = np.random.default_rng(args.seed)
-    graph = random_3regular_graph(n, rng)
+    pool_stream = RandomStream(args.seed, SCOPE_POOL, 0)
+    graph = qopt.random_3regular_graph(n, pool_stream.split(0))
     circ = build_qaoa_circuit(graph, depth)
-    exact = exact_maxcut(graph, n)
-    pos = rng.uniform(0, np.pi, size=(S, 2 * depth))[first:first + count]
-    vel = rng.uniform(-0.5, 0.5, size=(S, 2 * depth))[first:first + count]
-    best_pos, best_val = pos.copy(), np.full(count, -np.inf)
-    gbest = pos[0].copy()
-    ctx = runtime.make_context(None, n, num_states=count, device=local, fuse=fuse_mode(args))
+    exact = qopt.exact_maxcut(graph)
+    swarm = qopt.init_swarm(S, 2 * depth, stream=pool_stream.split(1))
+    ctx = runtime.make_context(None, n, count, args.seed, device=local, fuse=fuse_mode(args))
     ctx.norm_check_interval = 0
     st = ctx.state
     edges = np.asarray(graph.edges, dtype=np.int32)
-    prng = np.random.default_rng(args.seed + rank)
+    host_ms = []
+
+    def share(mine):
+        if dist is None:
+            return mine
+        import torch
+
+        buf = torch.zeros(S, dtype=torch.float64)
+        buf[first:first + count] = torch.from_numpy(mine)
+        dist.all_reduce(buf)  # disjoint blocks: the sum is the concatenation
+        return buf.numpy()
 
     def step():
-        nonlocal pos, vel, best_pos, best_val, gbest
+        pos = np.stack([swarm.particles[k].position for k in range(first, first + count)])
         runtime.reset_state(ctx)
-        runtime.run_circuit_pool(ctx, circ, qaoa_tables(pos, depth))
-        values = ctx.pool.observable(3, 0, edges) / exact
-        pos, vel, best_pos, best_val, gbest = pso_step(pos, vel, best_pos, best_val, gbest,
-                                                       values, prng)
+        runtime.run_circuit_pool(ctx, circ, qopt.qaoa_slot_tables(pos, depth))
+        mine = ctx.pool.observable(3, 0, edges) / exact
+        values = share(np.asarray(mine, dtype=np.float64))
+        t = time.perf_counter()
+        qopt.step_swarm(swarm, values)
+        host_ms.append(1e3 * (time.perf_counter() - t))
         return values
 
     for _ in range(args.warmup):
         step()
     st.synchronize()
     barrier(dist)
+    host_ms.clear()
     clocks = ClockSampler(local)
     clocks.start()
     st.launch_log(True)
@@ -919,16 +935,21 @@ def run_qaoa(args, dist, comm, world, rank, local):
     dom = max(kinds, key=lambda k: sum(kinds[k]))
     dom_ms = float(np.mean(kinds[dom]))
     peak, peak_src = measured_peak()
-    # algorithmic bytes (32*2^n B per gate per state) x the
-    # gate-updates one k_tile launch processes on average
     gates_per_step = count * len(circ.gates)
-    launches_per_step = len(kinds[dom]) / args.steps
-    bytes_per_launch = 32.0 * (2 ** n) * gates_per_step / launches_per_step
+    pass_kinds = [k for k in kinds if LAUNCH_KINDS.get(k, "") in ("k_tile", "k_fact", "k_fact_tma")]
+    passes_per_step = sum(len(kinds[k]) for k in pass_kinds) / args.steps
+    pass_ms = sum(sum(kinds[k]) for k in pass_kinds) / args.steps
+    # one pass reads and writes this GPU's pool once (32 B per amplitude)
     physical = 32.0 * (2 ** n) * count / (dom_ms / 1e3) / 1e9
+    tr = (ncu_traffic(LAUNCH_KINDS.get(dom, "") + "@qaoa") or
+          ncu_traffic(LAUNCH_KINDS.get(dom, "")))
+    traffic = (tr["bytes_per_amplitude"] * count * (2 ** n)
+               if tr and tr.get("bytes_per_amplitude") else None)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_baseline as cb
 
+        pos = np.stack([p.position for p in swarm.particles])
         cps, dt, _ = cpu_qaoa_sample(graph, pos, depth, cb.threads())
         cpu = {"value": cps * gates_per_circuit * (2.0 ** n) / 2.0 ** 30, "unit": UNIT,
                "cores": cb.threads(), "kind": "port",
@@ -941,24 +962,29 @@ def run_qaoa(args, dist, comm, world, rank, local):
             "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "c128 (f64 pairs)", "data": "synthetic",
-            "config": {"workload": f"config 5: QAOA MaxCut pool, {S} circuits per swarm step "
-                                   f"(n={n}, p={depth}, random 3-regular graph), <C> per "
-                                   "circuit, host PSO move", "pool": S, "per_gpu": count,
+            "config": {"workload": f"config 5: qaoa-pso --vertices {n} --depth {depth} "
+                                   f"--particles {S} --seed {args.seed}: keyed random 3-regular "
+                                   "graph (pool_stream.split(0)), keyed swarm "
+                                   "(pool_stream.split(1)), one swarm step = the 512 "
+                                   "circuits as one pool program + <C> + step_swarm",
+                       "pool": S, "per_gpu": count, "swarm_steps": args.steps,
                        "gates_per_circuit": gates_per_circuit, "fused": not args.no_fuse,
-                       "numerics": args.numerics},
+                       "numerics": args.numerics,
+                       "l2": f"pool of {count} x 2^{n} c128 = {count * 16 * 2 ** n / 2 ** 30:.0f} "
+                             "GiB per GPU, larger than L2"},
             "circuits_per_s": circuits / wall,
-            "best_ratio": float(np.max(best_val)),
+            "global_best_ratio": float(swarm.global_best_value),
+            "host_pso_ms_per_step": float(np.mean(host_ms)) if host_ms else None,
+            "pass_ms_per_step": pass_ms, "passes_per_step": passes_per_step,
             "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
-                         "achieved": bytes_per_launch / (dom_ms / 1e3) / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": bytes_per_launch / (dom_ms / 1e3) / 1e9 / peak,
-                         "traffic": None, "bytes_per_launch": bytes_per_launch,
-                         "units_per_launch": gates_per_step / launches_per_step,
-                         "bytes_per_unit": 32.0 * (2 ** n), "avg_launch_ms": dom_ms,
-                         "physical_gbs": physical, "physical_frac": physical / peak,
+                         "achieved": physical, "peak": peak, "unit": "GB/s",
+                         "frac": physical / peak, "traffic": traffic,
+                         "bytes_per_launch": 32.0 * (2 ** n) * count, "avg_launch_ms": dom_ms,
+                         "fusion_gain": gates_per_step / passes_per_step / count,
                          "peak_source": peak_src,
-                         "note": "algorithmic 32*2^n B per gate-update (SURVEY 8(d)) x "
-                                 "gate-updates per k_tile launch; physical_gbs = one "
-                                 "read+write of the pool per launch"},
+                         "note": "achieved = one read + write of this GPU's pool (32 B per "
+                                 "amplitude) / the dominant pass kernel's average launch time; "
+                                 "fusion_gain = gate-updates per state per pass"},
             "kernel_share": {LAUNCH_KINDS.get(k, str(k)): {"launches": len(v),
                                                            "share": float(np.sum(v) / dev_ms)}
                              for k, v in kinds.items()},

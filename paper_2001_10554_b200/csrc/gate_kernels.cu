@@ -1595,6 +1595,11 @@ CUtensorMapL2promotion l2_promotion() {
 
 bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
     static const bool off = getenv("QSB_NO_TMA") != nullptr;
+    static const bool dbg = getenv("QSB_DEBUG_TMA") != nullptr;
+    if (dbg) {
+        fprintf(stderr, "tma_plan: m=%d low_run=%d rounds=%d tile_bits=", F.m, F.low_run, F.num_rounds);
+        for (int p = 0; p < kTileLog2; ++p) fprintf(stderr, "%d%s", F.tile_bits[p], p + 1 < kTileLog2 ? "," : "\n");
+    }
     if (off || F.low_run < 3 || !encode_fn()) return false;
     const int m = F.m;
     const uint64_t num_states = F.num_tiles / F.tiles_per_state;
@@ -1707,8 +1712,10 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
         }
         T->prefetch = pf_env >= 0 ? pf_env : (!contiguous && high <= 4 ? 1 : 0);
         F = G;
+        if (dbg) fprintf(stderr, "tma_plan: rank %d, prefetch %d\n", rank, T->prefetch);
         return true;
     }
+    if (dbg) fprintf(stderr, "tma_plan: no candidate (%zu tried)\n", cands.size());
     return false;
 }
 

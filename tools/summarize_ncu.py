@@ -29,7 +29,10 @@ KEYS = [
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "smsp__sass_inst_executed_op_global_ld.sum", "smsp__sass_inst_executed_op_global_st.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__inst_executed.sum",
+    "l1tex__throughput.avg.pct_of_peak_sustained_active",
 ]
+STALLS = "smsp__pcsamp_warps_issue_stalled_"
 
 
 def short(name):
@@ -71,8 +74,15 @@ def launches(rnd, path):
 
 
 def full(rnd, rep):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout.splitlines()
+    if rep.endswith(".raw.csv"):  # exported on the GPU box (ncu -i rep --page raw --csv)
+        raw = open(rep).read().splitlines()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout.splitlines()
+    # capture tag (r02b_qaoa.raw.csv -> qaoa): pool-mode captures get their own
+    # traffic keys (k_fact@qaoa), the config-2 sweep keeps the bare kernel name
+    tag = os.path.basename(rep).split(".")[0].split("_", 1)[-1]
+    suffix = "" if tag in ("fact", "tile", "other", rnd) else "@" + tag
     rows = list(csv.reader(raw))
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
@@ -83,11 +93,17 @@ def full(rnd, rep):
     for r in rows[2:]:
         if len(r) != len(hdr):
             continue
-        k = short(r[name_i])
+        k = short(r[name_i]) + suffix
         rec = {}
         for key in KEYS:
             if key in idx and r[idx[key]] not in ("", "n/a"):
                 rec[key] = (r[idx[key]], units[idx[key]])
+        st = {h[len(STALLS):]: float(r[i]) for h, i in idx.items()
+              if h.startswith(STALLS) and not h.endswith("not_issued") and r[i] not in ("", "n/a")}
+        tot = sum(st.values()) or 1.0
+        rec["stalls (share of pc samples)"] = (
+            " ".join(f"{k2}={v / tot:.2f}" for k2, v in sorted(st.items(), key=lambda kv: -kv[1])[:6]),
+            "")
         per_kernel[k].append(rec)
     for k, recs in per_kernel.items():
         lines = [f"# ncu --set full, round {rnd}: {os.path.basename(rep)}, kernel {k}"]
@@ -95,7 +111,7 @@ def full(rnd, rep):
         for i, rec in enumerate(recs):
             lines.append(f"launch {i}:")
             for key, (v, u) in rec.items():
-                lines.append(f"  {key:62s} {v:>16s} {u}")
+                lines.append(f"  {key:62s} {v:>16s} {u}" if u or len(v) < 17 else f"  {key}: {v}")
             try:
                 rd = float(rec["dram__bytes_read.sum"][0].replace(",", ""))
                 wr = float(rec["dram__bytes_write.sum"][0].replace(",", ""))
@@ -106,7 +122,7 @@ def full(rnd, rep):
                 pass
         open(os.path.join(PROF, f"ncu_{rnd}_{k}.txt"), "w").write("\n".join(lines) + "\n")
         if tb:
-            amps = AMPS.get(os.path.basename(rep))
+            amps = AMPS.get(os.path.basename(rep)) or AMPS.get(tag)
             traffic[k] = {"bytes_per_launch": sum(tb) / len(tb), "launches": len(tb),
                           "amplitudes_per_launch": amps,
                           "bytes_per_amplitude": (sum(tb) / len(tb) / amps) if amps else None,
@@ -126,7 +142,7 @@ if __name__ == "__main__":
             name, lg = a[len("--amps="):].split(":")
             AMPS[name] = 1 << int(lg)
             continue
-        if a.endswith(".csv"):
+        if a.endswith(".csv") and not a.endswith(".raw.csv"):
             launches(rnd, a)
         else:
             full(rnd, a)
