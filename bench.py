@@ -932,19 +932,11 @@ def run_qaoa(args, dist, comm, world, rank, local):
     for k, t in zip(launch_kind, launch_ms):
         kinds.setdefault(int(k), []).append(float(t))
     dev_ms = sum(sum(v) for v in kinds.values())
-    dom = max(kinds, key=lambda k: sum(kinds[k]))
-    dom_ms = float(np.mean(kinds[dom]))
     peak, peak_src = measured_peak()
     gates_per_step = count * len(circ.gates)
     pass_kinds = [k for k in kinds if LAUNCH_KINDS.get(k, "") in ("k_tile", "k_fact", "k_fact_tma")]
     passes_per_step = sum(len(kinds[k]) for k in pass_kinds) / args.steps
     pass_ms = sum(sum(kinds[k]) for k in pass_kinds) / args.steps
-    # one pass reads and writes this GPU's pool once (32 B per amplitude)
-    physical = 32.0 * (2 ** n) * count / (dom_ms / 1e3) / 1e9
-    tr = (ncu_traffic(LAUNCH_KINDS.get(dom, "") + "@qaoa") or
-          ncu_traffic(LAUNCH_KINDS.get(dom, "")))
-    traffic = (tr["bytes_per_amplitude"] * count * (2 ** n)
-               if tr and tr.get("bytes_per_amplitude") else None)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_baseline as cb
@@ -976,15 +968,8 @@ def run_qaoa(args, dist, comm, world, rank, local):
             "global_best_ratio": float(swarm.global_best_value),
             "host_pso_ms_per_step": float(np.mean(host_ms)) if host_ms else None,
             "pass_ms_per_step": pass_ms, "passes_per_step": passes_per_step,
-            "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
-                         "achieved": physical, "peak": peak, "unit": "GB/s",
-                         "frac": physical / peak, "traffic": traffic,
-                         "bytes_per_launch": 32.0 * (2 ** n) * count, "avg_launch_ms": dom_ms,
-                         "fusion_gain": gates_per_step / passes_per_step / count,
-                         "peak_source": peak_src,
-                         "note": "achieved = one read + write of this GPU's pool (32 B per "
-                                 "amplitude) / the dominant pass kernel's average launch time; "
-                                 "fusion_gain = gate-updates per state per pass"},
+            "roofline": pool_roofline(kinds, 32.0 * (2 ** n) * count, count * (2 ** n),
+                                      gates_per_step / count, peak, peak_src, "qaoa", args.steps),
             "kernel_share": {LAUNCH_KINDS.get(k, str(k)): {"launches": len(v),
                                                            "share": float(np.sum(v) / dev_ms)}
                              for k, v in kinds.items()},
@@ -999,6 +984,34 @@ def run_qaoa(args, dist, comm, world, rank, local):
         print(json.dumps(line))
     barrier(dist)
     return 0
+
+
+PASS_KINDS = ("k_tile", "k_fact")
+
+
+def pool_roofline(kinds, pass_bytes, amps, gates_per_state, peak, peak_src, tag, steps):
+    """Roofline of a pool step's fused passes (every k_fact / k_tile launch):
+    achieved = one read + write of this GPU's pool per pass (32 B per
+    amplitude) x passes / their summed launch time; traffic = ncu dram bytes
+    per amplitude of the same workload's capture (profiles/ncu_traffic.json,
+    key kernel@tag) x amplitudes; fusion_gain = gate-updates per state per pass."""
+    passes = {LAUNCH_KINDS.get(k, str(k)): v for k, v in kinds.items()
+              if LAUNCH_KINDS.get(k, "") in PASS_KINDS}
+    n = sum(len(v) for v in passes.values())
+    ms = sum(sum(v) for v in passes.values())
+    dom = max(passes, key=lambda k: sum(passes[k])) if passes else None
+    achieved = pass_bytes * n / (ms / 1e3) / 1e9 if ms else None
+    tr = ncu_traffic(f"{dom}@{tag}") if dom else None
+    traffic = tr["bytes_per_amplitude"] * amps if tr and tr.get("bytes_per_amplitude") else None
+    return {"kernel": "+".join(sorted(passes)), "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak if achieved else None, "traffic": traffic,
+            "bytes_per_launch": pass_bytes, "avg_launch_ms": ms / n if n else None,
+            "launches": n, "fusion_gain": gates_per_state * steps / (n or 1),
+            "per_kernel_ms": {k: float(np.mean(v)) for k, v in passes.items()},
+            "peak_source": peak_src,
+            "note": "achieved = 32 B per amplitude of this GPU's pool per pass (one read + "
+                    "write) x pass launches / their summed device time (CUDA events on "
+                    "the library stream); fusion_gain = gate-updates per state per pass"}
 
 
 NOISE_T1, NOISE_T2 = 500.0, 250.0  # the reference's noise study defaults (noise_convergence_study.py)
@@ -1115,15 +1128,8 @@ def run_noise(args, dist, comm, world, rank, local):
     for k, t in zip(launch_kind, launch_ms):
         kinds.setdefault(int(k), []).append(float(t))
     dev_ms = sum(sum(v) for v in kinds.values())
-    dom = max(kinds, key=lambda k: sum(kinds[k]))
-    dom_ms = float(np.mean(kinds[dom]))
     peak, peak_src = measured_peak()
-    # algorithmic bytes (32*2^n B per gate per state) x the
-    # gate-updates one k_tile launch processes on average
     gates_per_step = count * len(circ.gates)
-    launches_per_step = len(kinds[dom]) / args.steps
-    bytes_per_launch = 32.0 * (2 ** n) * gates_per_step / launches_per_step
-    physical = 32.0 * (2 ** n) * count / (dom_ms / 1e3) / 1e9
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_baseline as cb
@@ -1149,17 +1155,8 @@ def run_noise(args, dist, comm, world, rank, local):
                        "numerics": args.numerics},
             "trajectories_per_s": trajectories / wall,
             "mean_cut": float(np.mean(values)),
-            "roofline": {"kernel": LAUNCH_KINDS.get(dom, str(dom)), "bound": "hbm",
-                         "achieved": bytes_per_launch / (dom_ms / 1e3) / 1e9, "peak": peak,
-                         "unit": "GB/s", "frac": bytes_per_launch / (dom_ms / 1e3) / 1e9 / peak,
-                         "traffic": None, "bytes_per_launch": bytes_per_launch,
-                         "units_per_launch": gates_per_step / launches_per_step,
-                         "bytes_per_unit": 32.0 * (2 ** n), "avg_launch_ms": dom_ms,
-                         "physical_gbs": physical, "physical_frac": physical / peak,
-                         "peak_source": peak_src,
-                         "note": "algorithmic 32*2^n B per gate-update (SURVEY 8(d)) x "
-                                 "gate-updates per k_tile launch; physical_gbs = one "
-                                 "read+write of the pool per launch"},
+            "roofline": pool_roofline(kinds, 32.0 * (2 ** n) * count, count * (2 ** n),
+                                      gates_per_step / count, peak, peak_src, "noise", args.steps),
             "kernel_share": {LAUNCH_KINDS.get(k, str(k)): {"launches": len(v),
                                                            "share": float(np.sum(v) / dev_ms)}
                              for k, v in kinds.items()},

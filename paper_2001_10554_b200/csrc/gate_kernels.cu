@@ -941,6 +941,31 @@ __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass
         default: fact_body<TB, 1, 1, 1, 1, MI>(__VA_ARGS__); break;               \
     }
 
+// QSB_FB with the pre-diagonal bodies compiled only when PREOK and the
+// product-diagonal bodies only when DIAGOK (passes without them -- every
+// config-2 sweep pass has no pre-diagonal, the middle one no product diagonal
+// -- get a smaller kernel whose registers are not shared with bodies they
+// never run: config-2 pass 1 6.7 -> 6.1 ms without the 20-byte spills)
+#define QSB_FBP(TB, MI, PREOK, DIAGOK, sel, ...)                                            \
+    switch (sel) {                                                                            \
+        case 0: fact_body<TB, 0, 0, 0, 0, MI>(__VA_ARGS__); break;                          \
+        case 1: if (DIAGOK) fact_body<TB, DIAGOK, 0, 0, 0, MI>(__VA_ARGS__); break;         \
+        case 2: if (PREOK) fact_body<TB, 0, PREOK, 0, 0, MI>(__VA_ARGS__); break;           \
+        case 3: if (PREOK && DIAGOK) fact_body<TB, DIAGOK, PREOK, 0, 0, MI>(__VA_ARGS__); break;\
+        case 4: if (DIAGOK) fact_body<TB, 0, 0, DIAGOK, 0, MI>(__VA_ARGS__); break;         \
+        case 5: if (DIAGOK) fact_body<TB, DIAGOK, 0, DIAGOK, 0, MI>(__VA_ARGS__); break;    \
+        case 6: if (PREOK && DIAGOK) fact_body<TB, 0, PREOK, DIAGOK, 0, MI>(__VA_ARGS__); break;\
+        case 7: if (PREOK && DIAGOK) fact_body<TB, DIAGOK, PREOK, DIAGOK, 0, MI>(__VA_ARGS__); break;\
+        case 8: fact_body<TB, 0, 0, 0, 1, MI>(__VA_ARGS__); break;                          \
+        case 9: if (DIAGOK) fact_body<TB, DIAGOK, 0, 0, 1, MI>(__VA_ARGS__); break;         \
+        case 10: if (PREOK) fact_body<TB, 0, PREOK, 0, 1, MI>(__VA_ARGS__); break;          \
+        case 11: if (PREOK && DIAGOK) fact_body<TB, DIAGOK, PREOK, 0, 1, MI>(__VA_ARGS__); break;\
+        case 12: if (DIAGOK) fact_body<TB, 0, 0, DIAGOK, 1, MI>(__VA_ARGS__); break;        \
+        case 13: if (DIAGOK) fact_body<TB, DIAGOK, 0, DIAGOK, 1, MI>(__VA_ARGS__); break;   \
+        case 14: if (PREOK && DIAGOK) fact_body<TB, 0, PREOK, DIAGOK, 1, MI>(__VA_ARGS__); break;\
+        default: if (PREOK && DIAGOK) fact_body<TB, DIAGOK, PREOK, DIAGOK, 1, MI>(__VA_ARGS__); break;\
+    }
+
 template <bool TABLES, bool PHASE>
 __global__ void __launch_bounds__(kTileThreads, QSB_TILE_MINB)
     k_fact(double2* __restrict__ psi, const __grid_constant__ FactPass P,
@@ -1222,9 +1247,11 @@ struct alignas(64) TmaPass {
     CUtensorMap map;             // 128 bytes, 64-byte aligned
     int32_t rank;                // tensor dims (2..5)
     int32_t ncoord;              // dims whose coordinate comes from the tile index
-    int32_t coord_dim[4];
-    int32_t coord_shift[4];
-    uint64_t coord_mask[4];      // ~0 for the top field
+    int32_t coord_dim[5];
+    int32_t coord_shift[5];      // first tile-index bit of the field
+    int32_t coord_lsh[5];        // the field sits above the dim's box bits
+    int32_t pad_;
+    uint64_t coord_mask[5];      // ~0 for the top field
     int32_t sig[kTileLog2];      // smem index of each tile-position basis vector
     int32_t prefetch;            // L2 prefetch distance in tiles of this CTA
 };
@@ -1254,8 +1281,9 @@ __device__ __forceinline__ void tma_load_tile(const TmaPass& T, uint64_t tile, d
                                               uint64_t* bar) {
     int c[5] = {0, 0, 0, 0, 0};
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-        if (i < T.ncoord) c[T.coord_dim[i]] = int((tile >> T.coord_shift[i]) & T.coord_mask[i]);
+    for (int i = 0; i < 5; ++i)
+        if (i < T.ncoord)
+            c[T.coord_dim[i]] = int(((tile >> T.coord_shift[i]) & T.coord_mask[i]) << T.coord_lsh[i]);
     const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kTileBytes)
@@ -1297,8 +1325,9 @@ __device__ __forceinline__ void tma_load_tile(const TmaPass& T, uint64_t tile, d
 __device__ __forceinline__ void tma_prefetch_tile(const TmaPass& T, uint64_t tile) {
     int c[5] = {0, 0, 0, 0, 0};
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-        if (i < T.ncoord) c[T.coord_dim[i]] = int((tile >> T.coord_shift[i]) & T.coord_mask[i]);
+    for (int i = 0; i < 5; ++i)
+        if (i < T.ncoord)
+            c[T.coord_dim[i]] = int(((tile >> T.coord_shift[i]) & T.coord_mask[i]) << T.coord_lsh[i]);
     const void* map = &T.map;
     switch (T.rank) {
         case 2:
@@ -1326,7 +1355,7 @@ __device__ __forceinline__ void tma_prefetch_tile(const TmaPass& T, uint64_t til
     }
 }
 
-template <bool TABLES, bool PHASE>
+template <bool TABLES, bool PHASE, bool PREOK, bool DIAGOK>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     k_fact_tma(double2* __restrict__ psi, const __grid_constant__ FactPass P,
                const double* __restrict__ mats, const __grid_constant__ CutTerms ct,
@@ -1464,9 +1493,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             for (int j = 0; j < kRegLog2; ++j) okb[j] = gstore ? goff(R.dk[1 << j]) : 0;
             double2* gb = gbase + (gstore ? goff(eb) : 0);
             if (PHASE && F.mid) {
-                QSB_FB(TABLES, (PHASE && true), sel, a, P, R, F, ct, mats, st, il, W, sb, skb, gb, okb)
+                QSB_FBP(TABLES, (PHASE && true), PREOK, DIAGOK, sel, a, P, R, F, ct, mats, st, il, W, sb, skb, gb, okb)
             } else {
-                QSB_FB(TABLES, false, sel, a, P, R, F, ct, mats, st, il, W, sb, skb, gb, okb)
+                QSB_FBP(TABLES, false, PREOK, DIAGOK, sel, a, P, R, F, ct, mats, st, il, W, sb, skb, gb, okb)
             }
             if (gstore) break;
             named_sync(gbar, kTileThreads);
@@ -1660,8 +1689,32 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
         push_tile(R0.lo, c.start - R0.lo);
         for (int i = 0; i < (int)tile_runs.size(); ++i)
             if (i != c.run) push_tile(tile_runs[i].lo, tile_runs[i].len);
-        for (const TmaDim& d : nontile) dims.push_back(d);
-        if (1 + dims.size() > 5) continue;
+        // every non-tile run rides on the dim just below it in qubit order
+        // (box = that dim's tile bits, the run's field is the coordinate above
+        // them), so the map has one dim per tile piece: dim0 (qubits 0..2) and
+        // the pieces above
+        // (measured slower than separate box-1 dims -- config-2 pass 2 6.6 ->
+        // 7.4 ms -- so only when the separate dims would exceed rank 5)
+        std::vector<int> absorbed(dims.size() + 1, -1);  // index into nontile, per dim (0 = dim0)
+        bool merged_all = true;
+        const bool merge = 1 + dims.size() + nontile.size() > 5;
+        for (int j = 0; merge && j < (int)nontile.size(); ++j) {
+            const TmaDim& N = nontile[j];
+            int host = -1;
+            const int below_q = N.len == 0 ? m : N.lo;  // the state index alone sits above m-1
+            if (below_q == 3) host = 0;
+            for (int i = 0; i < (int)dims.size() && host < 0; ++i)
+                if (dims[i].lo + dims[i].len == below_q) host = i + 1;
+            if (host < 0 || absorbed[host] >= 0) {
+                merged_all = false;
+                break;
+            }
+            absorbed[host] = j;
+        }
+        if (!merged_all || 1 + dims.size() > 5) continue;
+        std::vector<int> own_dim(nontile.size(), -1);  // unmerged: the run's own dim after the pieces
+        if (!merge)
+            for (int j = 0; j < (int)nontile.size(); ++j) own_dim[j] = int(dims.size()) + 1 + j;
         // smem bit of each tile position: dim0 = qubits 0..2, then dim order
         int pos_bit[kTileLog2], bit = 3;
         for (int p = 0; p < 3; ++p) pos_bit[p] = p;
@@ -1675,23 +1728,49 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
         // the tensor map
         cuuint64_t gdim[5], gstride[4];
         cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
-        gdim[0] = 2u << 3;  // re/im doubles of qubits 0..2
-        box[0] = 16;
         T->ncoord = 0;
+        auto field = [&](int di, int box_lsh, uint64_t* extent) {
+            const int j = absorbed[di];
+            if (j < 0) return;
+            const TmaDim& N = nontile[j];
+            *extent *= (uint64_t(1) << N.len) * (N.states ? num_states : 1);
+            const int k = T->ncoord++;
+            T->coord_dim[k] = di;
+            T->coord_shift[k] = N.field_shift;
+            T->coord_lsh[k] = box_lsh;
+            T->coord_mask[k] = N.states ? ~uint64_t(0) : (uint64_t(1) << N.len) - 1;
+        };
+        uint64_t ext0 = 16;  // re/im doubles of qubits 0..2
+        field(0, 4, &ext0);
+        gdim[0] = ext0;
+        box[0] = 16;
+        bool fits = ext0 <= (uint64_t(1) << 31);
         for (size_t i = 0; i < dims.size(); ++i) {
             const TmaDim& d = dims[i];
-            const uint64_t extent = (uint64_t(1) << d.len) * (d.states ? num_states : 1);
+            uint64_t extent = uint64_t(1) << d.len;
+            field(int(i + 1), d.len, &extent);
             gdim[i + 1] = extent;
             gstride[i] = uint64_t(sizeof(double2)) << d.lo;
-            box[i + 1] = d.tile ? (1u << d.len) : 1u;
-            if (!d.tile) {
-                const int k = T->ncoord++;
-                T->coord_dim[k] = int(i + 1);
-                T->coord_shift[k] = d.field_shift;
-                T->coord_mask[k] = d.states ? ~uint64_t(0) : (uint64_t(1) << d.len) - 1;
-            }
+            box[i + 1] = 1u << d.len;
+            fits &= extent <= (uint64_t(1) << 31);
         }
-        const int rank = int(dims.size()) + 1;
+        for (int j = 0; j < (int)nontile.size(); ++j) {
+            if (own_dim[j] < 0) continue;
+            const TmaDim& N = nontile[j];
+            const int di = own_dim[j];
+            const uint64_t extent = (uint64_t(1) << N.len) * (N.states ? num_states : 1);
+            gdim[di] = extent;
+            gstride[di - 1] = uint64_t(sizeof(double2)) << (N.len == 0 ? m : N.lo);
+            box[di] = 1;
+            fits &= extent <= (uint64_t(1) << 31);
+            const int k = T->ncoord++;
+            T->coord_dim[k] = di;
+            T->coord_shift[k] = N.field_shift;
+            T->coord_lsh[k] = 0;
+            T->coord_mask[k] = N.states ? ~uint64_t(0) : (uint64_t(1) << N.len) - 1;
+        }
+        if (!fits) continue;
+        const int rank = int(dims.size()) + 1 + (merge ? 0 : int(nontile.size()));
         if (rank < 2) continue;
         const CUresult rc = encode_fn()(&T->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, cuuint32_t(rank),
                                         psi, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1700,17 +1779,14 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
         if (rc != CUDA_SUCCESS) continue;
         T->rank = rank;
         for (int p = 0; p < kTileLog2; ++p) T->sig[p] = sig[p];
-        // L2 prefetch of this CTA's tile after next: measured to help tiles of
-        // 128-byte rows spread over a few 2 MiB pages (config-2 pass 2: 7.2 ->
-        // 6.6 ms) and to hurt contiguous tiles and tiles spread over hundreds of
-        // pages (pass 3: 8.1 -> 11.2 ms); QSB_TMA_PF overrides
-        static const int pf_env = getenv("QSB_TMA_PF") ? atoi(getenv("QSB_TMA_PF")) : -1;
-        int high = 0, contiguous = 1;
-        for (int p = 0; p < kTileLog2; ++p) {
-            high += F.tile_bits[p] >= 17;
-            contiguous &= F.tile_bits[p] == p;
-        }
-        T->prefetch = pf_env >= 0 ? pf_env : (!contiguous && high <= 4 ? 1 : 0);
+        // L2 prefetch of this CTA's tile after next (QSB_TMA_PF=d: d tiles
+        // ahead): measured with the round-1 kernel to help tiles of 128-byte
+        // rows over a few 2 MiB pages (config-2 pass 2: 7.2 -> 6.6 ms) and to
+        // hurt contiguous tiles and tiles over hundreds of pages (pass 3: 8.1
+        // -> 11.2 ms); with the spill-free lean kernels it hurts pass 2 too
+        // (6.5 -> 7.5 ms), so it is off by default
+        static const int pf_env = getenv("QSB_TMA_PF") ? atoi(getenv("QSB_TMA_PF")) : 0;
+        T->prefetch = pf_env;
         F = G;
         if (dbg) fprintf(stderr, "tma_plan: rank %d, prefetch %d\n", rank, T->prefetch);
         return true;
@@ -1719,7 +1795,7 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
     return false;
 }
 
-template <bool TB, bool PH>
+template <bool TB, bool PH, bool PO, bool DG>
 void launch_fact_tma_variant(double2* psi, const FactPass& F, const double* mats,
                              const CutTerms& ct, const TmaPass& T, cudaStream_t s) {
     constexpr int kMaxDevices = 64;
@@ -1730,7 +1806,7 @@ void launch_fact_tma_variant(double2* psi, const FactPass& F, const double* mats
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= kMaxDevices) dev = 0;
     if (configured[dev].load(std::memory_order_acquire) == 0) {
-        cudaFuncSetAttribute(k_fact_tma<TB, PH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_fact_tma<TB, PH, PO, DG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(smem));
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1740,19 +1816,25 @@ void launch_fact_tma_variant(double2* psi, const FactPass& F, const double* mats
     uint64_t grid = uint64_t(sms_of[dev]);
     const uint64_t need = (F.num_tiles + 1) / 2;
     if (grid > need) grid = need;
-    k_fact_tma<TB, PH><<<unsigned(grid), kTmaThreads, smem, s>>>(psi, F, mats, ct, T);
+    k_fact_tma<TB, PH, PO, DG><<<unsigned(grid), kTmaThreads, smem, s>>>(psi, F, mats, ct, T);
 }
 
 bool launch_fact_tma(double2* psi, FactPass& F, const double* mats, const CutTerms& ct,
                      bool tables, bool phase, cudaStream_t s) {
     static thread_local TmaPass T;
     if (!tma_plan(F, psi, &T)) return false;
-    if (tables) {
-        if (phase) launch_fact_tma_variant<true, true>(psi, F, mats, ct, T, s);
-        else launch_fact_tma_variant<true, false>(psi, F, mats, ct, T, s);
-    } else {
-        if (phase) launch_fact_tma_variant<false, true>(psi, F, mats, ct, T, s);
-        else launch_fact_tma_variant<false, false>(psi, F, mats, ct, T, s);
+    bool pre = false;
+    for (int r = 0; r < F.num_rounds; ++r) pre |= F.fr[r].pre_any != 0;
+    const bool diag = F.has_din || F.has_dout;
+    const int v = int(tables) | int(phase) << 1 | int(pre) << 2 | int(diag) << 3;
+    switch (v) {
+#define QSB_TMA_CASE(V) \
+    case V: launch_fact_tma_variant<(V & 1) != 0, (V & 2) != 0, (V & 4) != 0, (V & 8) != 0>(psi, F, mats, ct, T, s); break;
+        QSB_TMA_CASE(0) QSB_TMA_CASE(1) QSB_TMA_CASE(2) QSB_TMA_CASE(3)
+        QSB_TMA_CASE(4) QSB_TMA_CASE(5) QSB_TMA_CASE(6) QSB_TMA_CASE(7)
+        QSB_TMA_CASE(8) QSB_TMA_CASE(9) QSB_TMA_CASE(10) QSB_TMA_CASE(11)
+        QSB_TMA_CASE(12) QSB_TMA_CASE(13) QSB_TMA_CASE(14) QSB_TMA_CASE(15)
+#undef QSB_TMA_CASE
     }
     return true;
 }
