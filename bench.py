@@ -377,6 +377,9 @@ def physical_devices(dist, local: int) -> int:
 def run_ours(args):
     world, rank, local = dist_env()
     emulated = bool(os.environ.get("QSB_ALL_RANKS_ON_DEVICE0"))
+    if emulated and world > 1 and args.exchange == "nccl":
+        raise SystemExit("bench.py: NCCL refuses two ranks on one GPU (ncclCommInitRank: invalid "
+                         "usage); the emulated run uses --exchange peer")
     if emulated:
         local = 0  # functional multi-rank run on one GPU (exchange kernels never wait on each other)
     dist = init_dist(world)

@@ -78,6 +78,11 @@ int         qs_device_count(int32_t* out);
 /* Per-thread byte/message counters of the global-qubit exchange, mirroring
  * TransportCounters (transport.py:49-65): amplitudes moved between ranks. */
 int         qs_counters(const qs_state* st, uint64_t* messages, uint64_t* amplitudes);
+/* Process-wide count of host-blocking CUDA calls the library has made
+ * (stream/event/device synchronisations).  No reference counterpart: it makes
+ * the asynchrony of the global-qubit path testable (distribution.py:121-178
+ * blocks in MPI-style send/recv; the B200 path must not block the host). */
+uint64_t    qs_host_sync_count(void);
 
 /* ---- state lifetime: replaces StatePartition + allocate_partition
  *      (statevector.py:74-115) ------------------------------------------- */

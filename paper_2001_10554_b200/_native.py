@@ -22,7 +22,7 @@ QS_OBS_NORM, QS_OBS_PROB, QS_OBS_Z, QS_OBS_MAXCUT = 0, 1, 2, 3
 
 # Every symbol include/qsb200.h declares (checked by tests/test_abi.py).
 EXPORTS = (
-    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_counters",
+    "qs_abi_version", "qs_last_error", "qs_device_count", "qs_counters", "qs_host_sync_count",
     "qs_state_create", "qs_state_destroy", "qs_state_info", "qs_state_device_ptr",
     "qs_synchronize", "qs_state_upload", "qs_state_download", "qs_state_exchange_host",
     "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
@@ -76,6 +76,7 @@ _SIGNATURES = {
     "qs_last_error": ([], ctypes.c_char_p),
     "qs_device_count": ([_IP], ctypes.c_int),
     "qs_counters": ([_P, _UP, _UP], ctypes.c_int),
+    "qs_host_sync_count": ([], ctypes.c_uint64),
     "qs_state_create": ([_I, _I, _I, _I, _I, ctypes.POINTER(_P)], ctypes.c_int),
     "qs_state_destroy": ([_P], ctypes.c_int),
     "qs_state_info": ([_P, _IP, _IP, _IP, _IP, _UP], ctypes.c_int),
@@ -163,6 +164,12 @@ def check(rc: int) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args))
+
+
+def host_sync_count() -> int:
+    """Host-blocking CUDA calls the library has made in this process
+    (qs_host_sync_count): stream/event/device synchronisations."""
+    return int(load().qs_host_sync_count())
 
 
 def device_count() -> int:

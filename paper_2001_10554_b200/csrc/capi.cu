@@ -15,7 +15,29 @@
 
 #include "common.cuh"
 
+#include <atomic>
+
 using namespace qsb;
+
+// Every host-blocking CUDA call of the library goes through these; the count
+// is exported (qs_host_sync_count) so tests can show that the global-qubit
+// path never blocks the host between gates (its exchange kernels are ordered
+// by CUDA events, not host syncs).
+namespace {
+std::atomic<uint64_t> g_host_syncs{0};
+inline cudaError_t host_sync_stream(cudaStream_t s) {
+    g_host_syncs.fetch_add(1, std::memory_order_relaxed);
+    return cudaStreamSynchronize(s);
+}
+inline cudaError_t host_sync_event(cudaEvent_t e) {
+    g_host_syncs.fetch_add(1, std::memory_order_relaxed);
+    return cudaEventSynchronize(e);
+}
+inline cudaError_t host_sync_device() {
+    g_host_syncs.fetch_add(1, std::memory_order_relaxed);
+    return cudaDeviceSynchronize();
+}
+}  // namespace
 
 namespace qsb {
 size_t tile_smem_bytes();
@@ -168,7 +190,7 @@ template <typename T>
 int grow(T** p, size_t* cap, size_t need) {
     if (*cap >= need) return QS_OK;
     if (*p) {
-        cudaDeviceSynchronize();  // queued kernels may still read the old buffer
+        host_sync_device();  // queued kernels may still read the old buffer
         cudaError_t e = cudaFree(*p);
         if (e != cudaSuccess) return fail(QS_ERR_CUDA, "cudaFree: %s", cudaGetErrorString(e));
     }
@@ -587,6 +609,8 @@ int qs_device_count(int32_t* out) {
     return QS_OK;
 }
 
+uint64_t qs_host_sync_count(void) { return g_host_syncs.load(std::memory_order_relaxed); }
+
 int qs_counters(const qs_state* st, uint64_t* messages, uint64_t* amplitudes) {
     if (!st) return fail(QS_ERR_VALUE, "null state");
     *messages = st->messages;
@@ -647,7 +671,7 @@ int qs_state_create(int32_t num_qubits, int32_t num_local_qubits, int32_t rank_i
 int qs_state_destroy(qs_state* st) {
     if (!st) return QS_OK;
     cudaSetDevice(st->device);
-    if (st->stream) cudaStreamSynchronize(st->stream);
+    if (st->stream) host_sync_stream(st->stream);
     if (st->comm && g_nccl.loaded) g_nccl.CommDestroy(st->comm);
     for (auto& r : st->recs) cudaEventDestroy(r.start), cudaEventDestroy(r.stop);
     for (auto& ev : st->ev)
@@ -689,7 +713,7 @@ int qs_state_device_ptr(const qs_state* st, void** out) {
 
 int qs_synchronize(qs_state* st) {
     if (int rc = ensure_device(st)) return rc;
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(host_sync_stream(st->stream));
     return QS_OK;
 }
 
@@ -703,7 +727,7 @@ int qs_state_upload(qs_state* st, const double* host, uint64_t offset, uint64_t 
     if (count == 0) return QS_OK;
     CUDA_TRY(cudaMemcpyAsync(st->psi + offset, host, count * sizeof(double2),
                              cudaMemcpyHostToDevice, st->stream));
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(host_sync_stream(st->stream));
     return QS_OK;
 }
 
@@ -715,7 +739,7 @@ int qs_state_download(qs_state* st, double* host, uint64_t offset, uint64_t coun
     if (count == 0) return QS_OK;
     CUDA_TRY(cudaMemcpyAsync(host, st->psi + offset, count * sizeof(double2),
                              cudaMemcpyDeviceToHost, st->stream));
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(host_sync_stream(st->stream));
     return QS_OK;
 }
 
@@ -749,7 +773,7 @@ int qs_state_exchange_host(qs_state* st, const double* host_in, double* host_out
     CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
     CUDA_TRY(cudaEventRecord(done, st->comm_stream));
     CUDA_TRY(cudaStreamWaitEvent(st->stream, done, 0));
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(host_sync_stream(st->stream));
     for (auto e : evs) cudaEventDestroy(e);
     cudaEventDestroy(start);
     cudaEventDestroy(done);
@@ -776,7 +800,7 @@ int qs_init_basis(qs_state* st, uint64_t index) {
         for (int s = 0; s < st->num_states; ++s)
             CUDA_TRY(cudaMemcpyAsync(st->psi + uint64_t(s) * st->amps_per_state + off, &one,
                                      sizeof(one), cudaMemcpyHostToDevice, st->stream));
-        CUDA_TRY(cudaStreamSynchronize(st->stream));
+        CUDA_TRY(host_sync_stream(st->stream));
     }
     return QS_OK;
 }
@@ -822,7 +846,7 @@ int qs_state_diff(qs_state* a, const qs_state* b, double* out) {
     CHECK_LAUNCH();
     double h[4];
     CUDA_TRY(cudaMemcpyAsync(h, a->d_scratch, sizeof(h), cudaMemcpyDeviceToHost, a->stream));
-    CUDA_TRY(cudaStreamSynchronize(a->stream));
+    CUDA_TRY(host_sync_stream(a->stream));
     out[0] = h[0];
     out[1] = h[2];
     out[2] = h[3];
@@ -849,7 +873,7 @@ int qs_apply_diagonal(qs_state* st, const double* factors, uint64_t offset, uint
         CHECK_LAUNCH();
     }
     // the host buffer may be released when we return
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(host_sync_stream(st->stream));
     return QS_OK;
 }
 
@@ -1010,7 +1034,7 @@ int qs_observable(qs_state* st, int32_t kind, int32_t q, const int32_t* edges, i
     CHECK_LAUNCH();
     CUDA_TRY(cudaMemcpyAsync(st->h_out, out_dev, sizeof(double) * st->num_states,
                              cudaMemcpyDeviceToHost, st->stream));
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(host_sync_stream(st->stream));
     memcpy(out, st->h_out, sizeof(double) * st->num_states);
     return QS_OK;
 }
@@ -1106,7 +1130,7 @@ int qs_marginals(qs_state* st, double* out) {
     std::vector<double> local(size_t(S) * m);
     CUDA_TRY(cudaMemcpyAsync(local.data(), dev_out, sizeof(double) * local.size(),
                              cudaMemcpyDeviceToHost, st->stream));
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(host_sync_stream(st->stream));
     std::vector<double> norms;
     if (n > m) {  // global qubits: the whole slice or nothing (statevector.py:225-228)
         norms.resize(S);
@@ -1428,7 +1452,7 @@ int qs_event_record(qs_state* st, int32_t slot) {
 int qs_event_elapsed_ms(qs_state* st, int32_t a, int32_t b, float* ms) {
     if (!st || a < 0 || a >= 8 || b < 0 || b >= 8) return fail(QS_ERR_VALUE, "bad event slot");
     if (int rc = ensure_device(st)) return rc;
-    CUDA_TRY(cudaEventSynchronize(st->ev[b]));
+    CUDA_TRY(host_sync_event(st->ev[b]));
     CUDA_TRY(cudaEventElapsedTime(ms, st->ev[a], st->ev[b]));
     return QS_OK;
 }
@@ -1444,7 +1468,7 @@ int qs_launch_log(qs_state* st, int32_t enable) {
 int qs_launch_log_read(qs_state* st, float* ms, int32_t* kinds, int32_t cap, int32_t* count) {
     if (!st) return fail(QS_ERR_VALUE, "null state");
     if (int rc = ensure_device(st)) return rc;
-    CUDA_TRY(cudaStreamSynchronize(st->stream));
+    CUDA_TRY(host_sync_stream(st->stream));
     int k = 0;
     for (auto& r : st->recs) {
         if (k < cap) {

@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "qsb200.h")
 
 def header_functions():
     text = open(HEADER).read()
-    return set(re.findall(r"^(?:int|const char\*)\s+(qs_\w+)\s*\(", text, flags=re.M))
+    return set(re.findall(r"^(?:int|const char\*|uint64_t)\s+(qs_\w+)\s*\(", text, flags=re.M))
 
 
 def test_library_loads_and_version():
