@@ -4,6 +4,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -795,12 +796,10 @@ int qs_init_basis(qs_state* st, uint64_t index) {
                     (unsigned long long)index, st->n);
     if (int rc = qs_init_zero(st)) return rc;
     if ((index >> st->m) == uint64_t(st->rank)) {
-        const double2 one = make_double2(1.0, 0.0);
-        const uint64_t off = index & (st->amps_per_state - 1);
-        for (int s = 0; s < st->num_states; ++s)
-            CUDA_TRY(cudaMemcpyAsync(st->psi + uint64_t(s) * st->amps_per_state + off, &one,
-                                     sizeof(one), cudaMemcpyHostToDevice, st->stream));
-        CUDA_TRY(host_sync_stream(st->stream));
+        // stream-ordered, no host sync (a pool reset used to block ~2 ms here)
+        launch_set_basis(st->psi, st->amps_per_state, uint64_t(st->num_states),
+                         index & (st->amps_per_state - 1), st->stream);
+        CUDA_TRY(cudaGetLastError());
     }
     return QS_OK;
 }
@@ -899,6 +898,10 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
         if (int rc = validate_gate(st, gates[i], mats_len, num_edges)) return rc;
     static thread_local FactoredProgram fp;
     static thread_local std::vector<double> all;
+    // QSB_DEBUG_TIME: host time of each phase on stderr
+    static const bool dbg_time = getenv("QSB_DEBUG_TIME") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t_start = now(), t_factor = t_start, t_upload = t_start;
     if (fuse == QS_FUSE_FACTORED && st->m >= kTileLog2) {
         // rewrite, then plan the rewritten program; its parameters and diagonal
         // tables follow the caller's table in one upload.  Programs where fewer
@@ -919,10 +922,12 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
             mats_len = all.size();
         }
     }
+    t_factor = now();
     if (int rc = grow(&st->d_mats, &st->mats_cap, mats_len ? mats_len : 1)) return rc;
     if (mats_len)
         CUDA_TRY(cudaMemcpyAsync(st->d_mats, mats, mats_len * sizeof(double),
                                  cudaMemcpyHostToDevice, st->stream));
+    t_upload = now();
     std::vector<PassPlan> plan = plan_passes(gates, count, st->m, fuse != 0);
     int passes = 0;
     for (const PassPlan& pp : plan) {
@@ -934,6 +939,13 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
         ++passes;
     }
     st->last_passes = passes;
+    if (dbg_time) {
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        const auto t_end = now();
+        fprintf(stderr, "qs_apply_program: %d gates, %d passes, %.1f KB tables: factor+schedule %.3f ms, "
+                "upload %.3f ms, plan+launch %.3f ms\n", count, passes, mats_len * 8.0 / 1024,
+                ms(t_start, t_factor), ms(t_factor, t_upload), ms(t_upload, t_end));
+    }
     // no host sync: pageable H2D copies are staged before cudaMemcpyAsync returns,
     // so the caller may reuse `mats`, and the device tables are stream-ordered.
     return QS_OK;

@@ -182,6 +182,7 @@ bool tile_pass_in_params();  // k_tile takes the pass as a kernel parameter
 bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                       const double* mats, const CutTerms& ct, cudaStream_t s);
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s);
+void launch_set_basis(double2* psi, uint64_t stride, uint64_t states, uint64_t off, cudaStream_t s);
 void launch_gaussian(double2* psi, uint64_t count_per_state, int num_states, uint64_t rank_offset,
                      uint64_t seed, cudaStream_t s);
 void launch_scale(double2* psi, uint64_t count, double factor, cudaStream_t s);

@@ -1839,6 +1839,14 @@ bool launch_fact_tma(double2* psi, FactPass& F, const double* mats, const CutTer
     return true;
 }
 
+// |index> in every state of a pool after a zero fill: one amplitude per state
+__global__ void k_set_basis(double2* __restrict__ psi, uint64_t stride, uint64_t states,
+                            uint64_t off) {
+    for (uint64_t s = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; s < states;
+         s += uint64_t(gridDim.x) * blockDim.x)
+        psi[s * stride + off] = make_double2(1.0, 0.0);
+}
+
 __global__ void k_fill(double2* __restrict__ psi, uint64_t count, double2 value) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
          i += uint64_t(gridDim.x) * blockDim.x)
@@ -2031,6 +2039,12 @@ int prof_read(unsigned long long* out) {
     (void)out;
     return 0;
 #endif
+}
+
+void launch_set_basis(double2* psi, uint64_t stride, uint64_t states, uint64_t off,
+                      cudaStream_t s) {
+    const unsigned grid = unsigned(std::min<uint64_t>((states + 255) / 256, 1024));
+    k_set_basis<<<grid, 256, 0, s>>>(psi, stride, states, off);
 }
 
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s) {
