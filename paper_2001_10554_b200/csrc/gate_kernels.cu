@@ -341,6 +341,19 @@ __device__ __forceinline__ void reg_shear_seq_full(double2 (&a)[kRegAmps], const
 // are 0); register index k adds R[k] = prod_j z_{q_j}^{k_j}, precomputed by the
 // host for the round (the same for every thread and tile).  Two complex
 // products per amplitude.
+// the tile-element part of a product diagonal: one byte-table entry per 8
+// non-register qubits (loaded early by the lean kernels: its latency hides
+// behind the smem reads / the round's shears)
+__device__ __forceinline__ double2 diag_factor(const double2* T, int ntab, uint64_t il) {
+    double2 f = __ldg(T + (il & 255));
+    for (int c = 1; c < ntab; ++c) f = cmul(f, __ldg(T + (c << 8) + ((il >> (8 * c)) & 255)));
+    return f;
+}
+__device__ __forceinline__ void reg_diag_apply(double2 (&a)[kRegAmps], double2 f, const double2* R) {
+    a[0] = cmul(a[0], f);
+#pragma unroll
+    for (int k = 1; k < kRegAmps; ++k) a[k] = cmul(a[k], cmul(f, R[k]));
+}
 __device__ __forceinline__ void reg_diag_n(double2 (&a)[kRegAmps], const double2* T, int ntab,
                                            uint64_t il, const double2* R) {
     double2 f = __ldg(T + (il & 255));
@@ -879,21 +892,20 @@ __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass
                                           const double* __restrict__ mats, uint64_t st,
                                           uint64_t il, double2* tile, int sb,
                                           const int (&skb)[kRegLog2], double2* gb,
-                                          const uint64_t (&okb)[kRegLog2]) {
-    if (DIN) {
-        const double2* T = reinterpret_cast<const double2*>(mats + P.din_off);
-        reg_diag_n(a, T, P.ntab, il, P.din_r);
-    }
+                                          const uint64_t (&okb)[kRegLog2], int acq = 0) {
+    if (DIN) reg_diag_apply(a, diag_factor(reinterpret_cast<const double2*>(mats + P.din_off), P.ntab, il),
+                            P.din_r);
     fact_run<PRE, TABLES>(a, F, 0, mats, st);
     if (MID) {
         fact_cut_phase(a, P, R, ct,
                        reinterpret_cast<const double2*>(mats + F.lut_off + st * F.lut_stride), il);
         fact_run<PRE, TABLES>(a, F, 1, mats, st);
     }
-    if (DOUT) {
-        const double2* T = reinterpret_cast<const double2*>(mats + P.dout_off);
-        reg_diag_n(a, T, P.ntab, il, P.dout_r);
-    }
+    // (loading the product-diagonal factors early -- before the tile reads or
+    // the shears -- measured slower: pass 1 6.35 -> 6.9 ms)
+    if (DOUT)
+        reg_diag_apply(a, diag_factor(reinterpret_cast<const double2*>(mats + P.dout_off), P.ntab, il),
+                       P.dout_r);
     if (GSTORE) {
 #pragma unroll
         for (int k = 0; k < kRegAmps; ++k) {
@@ -908,6 +920,9 @@ __device__ __forceinline__ void fact_body(double2 (&a)[kRegAmps], const FactPass
 #endif
         }
     } else {
+        // k_fact_pair: the two groups share one reslice buffer; take it now
+        // (after the round's arithmetic) from the other group
+        if (acq) named_sync(acq, 2 * kTileThreads);
         int sbs = sb;
         asm volatile("" : "+r"(sbs));
 #pragma unroll
@@ -1254,6 +1269,11 @@ struct alignas(64) TmaPass {
     uint64_t coord_mask[5];      // ~0 for the top field
     int32_t sig[kTileLog2];      // smem index of each tile-position basis vector
     int32_t prefetch;            // L2 prefetch distance in tiles of this CTA
+};
+// host only: the tile pieces above qubits 0..2 in the map's dim order (the
+// pair plan rebuilds a 13-bit map from them)
+struct TmaPieces {
+    int32_t npieces, piece_lo[kTileLog2], piece_len[kTileLog2];
 };
 
 constexpr int kTmaThreads = 2 * kTileThreads;
@@ -1622,7 +1642,7 @@ CUtensorMapL2promotion l2_promotion() {
                     : v >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
 }
 
-bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
+bool tma_plan(FactPass& F, double2* psi, TmaPass* T, TmaPieces* pieces = nullptr) {
     static const bool off = getenv("QSB_NO_TMA") != nullptr;
     static const bool dbg = getenv("QSB_DEBUG_TMA") != nullptr;
     if (dbg) {
@@ -1779,6 +1799,11 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T) {
         if (rc != CUDA_SUCCESS) continue;
         T->rank = rank;
         for (int p = 0; p < kTileLog2; ++p) T->sig[p] = sig[p];
+        if (pieces) {
+            pieces->npieces = int(dims.size());
+            for (size_t i = 0; i < dims.size(); ++i)
+                pieces->piece_lo[i] = dims[i].lo, pieces->piece_len[i] = dims[i].len;
+        }
         // L2 prefetch of this CTA's tile after next (QSB_TMA_PF=d: d tiles
         // ahead): measured with the round-1 kernel to help tiles of 128-byte
         // rows over a few 2 MiB pages (config-2 pass 2: 7.2 -> 6.6 ms) and to
@@ -1819,13 +1844,389 @@ void launch_fact_tma_variant(double2* psi, const FactPass& F, const double* mats
     k_fact_tma<TB, PH, PO, DG><<<unsigned(grid), kTmaThreads, smem, s>>>(psi, F, mats, ct, T);
 }
 
+// ---- lean factored pass over tile PAIRS (256-byte rows) ---------------------------
+// k_fact_pair: a 2^12 tile with 128-byte rows (qubits 0..2 + 9 targets, the
+// middle and last passes of the config-2 sweep) moves at the copy speed of
+// 128-byte rows at large strides (profiles/r02_notes.md: 6.9-8.2 ms per pass
+// with no arithmetic); rows of 256 bytes copy in 5.8-6.0 ms.  Here one CTA
+// processes the two tiles that differ in the lowest non-tile qubit p (p = 3:
+// the rows become 256 bytes) as ONE 128 KiB TMA box: group g (256 threads)
+// owns the tile with qubit p = g and runs k_fact's rounds on it.  Shared memory
+// holds the 128 KiB landing buffer L and ONE 64 KiB reslice buffer W, which
+// the groups take in turns: a group's data lives in registers between rounds
+// and occupies W only from the write at the end of a round to the read at the
+// start of the next (named-barrier hand-over, turn barriers 3/4).  L is
+// re-filled as soon as both groups have read the pair out of it in round 0,
+// so 128 KiB per SM are in flight during the whole pair.
+struct alignas(64) PairPass {
+    CUtensorMap map;             // the 13-bit box
+    int32_t ncoord;
+    int32_t coord_dim[5], coord_shift[5], coord_lsh[5];
+    uint64_t coord_mask[5];
+    int32_t gx;                  // smem index of the pair bit (group 1's XOR offset in L)
+    uint16_t slo0[1 << kLaneLoBits], shi0[1 << kLaneHiBits], sk0[1 << kRegLog2];  // round 0 in L
+};
+
+__device__ __forceinline__ void tma_load_pair(const PairPass& X, uint64_t pair, double2* dst,
+                                              uint64_t* bar) {
+    int c[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+        if (i < X.ncoord)
+            c[X.coord_dim[i]] = int(((pair >> X.coord_shift[i]) & X.coord_mask[i]) << X.coord_lsh[i]);
+    const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(2 * kTileBytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(d), "l"(&X.map), "r"(c[0]), "r"(c[1]),
+        "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b)
+        : "memory");
+}
+
+template <bool PREOK, bool DIAGOK>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    k_fact_pair(double2* __restrict__ psi, const __grid_constant__ FactPass P,
+                const double* __restrict__ mats, const __grid_constant__ CutTerms ct,
+                const __grid_constant__ TmaPass T, const __grid_constant__ PairPass X) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    double2* Lbuf = reinterpret_cast<double2*>(smem_raw);
+    double2* W = Lbuf + 2 * kTileAmps;
+    uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem_raw + 3 * kTileBytes);
+    uint64_t* dep = rowoff + (kTileAmps >> kLowBits);
+    uint32_t* rlo = reinterpret_cast<uint32_t*>(dep + 256 * kDepTables);
+    uint32_t* rhi = rlo + kMaxRounds * (1 << kLaneLoBits);
+    uint32_t* rlo0 = rhi + kMaxRounds * (1 << kLaneHiBits);
+    uint32_t* rhi0 = rlo0 + (1 << kLaneLoBits);
+    uint64_t* full = reinterpret_cast<uint64_t*>(rhi0 + (1 << kLaneHiBits));
+    unsigned* consumed = reinterpret_cast<unsigned*>(full + 1);
+    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneLoBits); i += kTmaThreads) {
+        const Round& R = P.rounds[i >> kLaneLoBits];
+        const int v = i & ((1 << kLaneLoBits) - 1);
+        rlo[i] = uint32_t(R.dlo[v]) | (uint32_t(R.slo[v]) << 16);
+    }
+    for (int i = threadIdx.x; i < P.num_rounds * (1 << kLaneHiBits); i += kTmaThreads) {
+        const Round& R = P.rounds[i >> kLaneHiBits];
+        const int v = i & ((1 << kLaneHiBits) - 1);
+        rhi[i] = uint32_t(R.dhi[v]) | (uint32_t(R.shi[v]) << 16);
+    }
+    if (threadIdx.x < (1 << kLaneLoBits)) rlo0[threadIdx.x] = X.slo0[threadIdx.x];
+    if (threadIdx.x < (1 << kLaneHiBits)) rhi0[threadIdx.x] = X.shi0[threadIdx.x];
+    const int low_run = P.low_run;
+    const int nrows = kTileAmps >> low_run;
+    const uint64_t lowmask = (uint64_t(1) << low_run) - 1;
+    for (int r = threadIdx.x; r < nrows; r += kTmaThreads) {
+        uint64_t off = 0;
+        for (int k = 0; k < kTileLog2 - low_run; ++k)
+            if ((r >> k) & 1) off |= uint64_t(1) << P.tile_bits[low_run + k];
+        rowoff[r] = off;
+    }
+    for (int i = threadIdx.x; i < kDepTables * 256; i += kTmaThreads) {
+        const int c = i >> 8, v = i & 255;
+        uint64_t out = 0;
+        for (int b = 0; b < 8; ++b) {
+            if (!((v >> b) & 1)) continue;
+            int want = 8 * c + b, cnt = 0;
+            for (int q = 0, k = 0; q < P.m; ++q) {
+                if (k < kTileLog2 && P.tile_bits[k] == q) {
+                    ++k;
+                    continue;
+                }
+                if (cnt++ == want) {
+                    out |= uint64_t(1) << q;
+                    break;
+                }
+            }
+        }
+        dep[i] = out;
+    }
+    const uint64_t num_pairs = P.num_tiles >> 1;
+    if (threadIdx.x == 0) {
+        mbar_init(full, 1);
+        *consumed = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < num_pairs) tma_load_pair(X, blockIdx.x, Lbuf, full);
+
+    const int group = threadIdx.x / kTileThreads;  // warp-uniform: the pair bit of its tile
+    const int tid = threadIdx.x % kTileThreads;
+    const int gbar = 1 + group;
+    const int turn_me = 3 + group, turn_other = 4 - group;
+    const int m = P.m;
+    const int tps_log2 = m - kTileLog2;
+    auto tile_base = [&](uint64_t t) {
+        const uint64_t x = t & (P.tiles_per_state - 1);
+        uint64_t out = 0;
+#pragma unroll
+        for (int c = 0; c < kDepTables; ++c) out |= dep[(c << 8) | ((x >> (8 * c)) & 255)];
+        return out;
+    };
+    auto goff = [&](int e) { return rowoff[e >> low_run] + (uint64_t(e) & lowmask); };
+    auto sig_of = [&](int e) {
+        int v = 0;
+#pragma unroll
+        for (int b = 0; b < kTileLog2; ++b)
+            if ((e >> b) & 1) v ^= T.sig[b];
+        return v;
+    };
+    const bool direct = P.direct_store != 0;
+    const int gxg = group ? X.gx : 0;
+    bool skip_acq = group == 0;  // group 0 takes W first, without a hand-over
+    bool used_w = false;
+    unsigned parity = 0;
+    for (uint64_t k = 0;; ++k, parity ^= 1) {
+        const uint64_t pair = blockIdx.x + k * gridDim.x;
+        if (pair >= num_pairs) break;
+        const uint64_t tile_id = (pair << 1) | uint64_t(group);
+        const uint64_t st = tile_id >> tps_log2;
+        const uint64_t base_local = tile_base(tile_id);
+        double2* gbase = psi + ((st << m) | base_local);
+        mbar_wait(full, parity);
+        for (int r = 0; r < P.num_rounds; ++r) {
+            const Round& R = P.rounds[r];
+            const bool last = r == P.num_rounds - 1;
+            const uint32_t lo = rlo[(r << kLaneLoBits) | (tid & ((1 << kLaneLoBits) - 1))];
+            const uint32_t hi = rhi[(r << kLaneHiBits) | (tid >> kLaneLoBits)];
+            const int eb = int((lo | hi) & 0xffff);
+            const int sb = int((lo ^ hi) >> 16);
+            int skb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) skb[j] = R.sk[1 << j];
+            double2 a[kRegAmps];
+            if (r == 0) {
+                // the pair's half of this group, in the 13-bit layout of L
+                const int sb0 = int(rlo0[tid & ((1 << kLaneLoBits) - 1)] ^ rhi0[tid >> kLaneLoBits]) ^ gxg;
+                int sk0[kRegLog2];
+#pragma unroll
+                for (int j = 0; j < kRegLog2; ++j) sk0[j] = X.sk0[1 << j];
+#pragma unroll
+                for (int kk = 0; kk < kRegAmps; ++kk) {
+                    int v = 0;
+#pragma unroll
+                    for (int j = 0; j < kRegLog2; ++j)
+                        if ((kk >> j) & 1) v ^= sk0[j];
+                    a[kk] = Lbuf[sb0 ^ v];
+                }
+                named_sync(gbar, kTileThreads);
+                if (tid == 0) {
+                    // the second group to finish reading requests the next pair
+                    __threadfence_block();
+                    if (atomicAdd(consumed, 1u) & 1u) {
+                        const uint64_t next = pair + gridDim.x;
+                        if (next < num_pairs) {
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            tma_load_pair(X, next, Lbuf, full);
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < kRegAmps; ++kk) {
+                    int v = 0;
+#pragma unroll
+                    for (int j = 0; j < kRegLog2; ++j)
+                        if ((kk >> j) & 1) v ^= skb[j];
+                    a[kk] = W[sb ^ v];
+                }
+                // every thread of the group has its data: W goes to the other group
+                named_sync(gbar, kTileThreads);
+                named_arrive(turn_other, 2 * kTileThreads);
+            }
+            const FactRound& F = P.fr[r];
+            const bool gstore = last && direct;
+            const int sel = int(r == 0 && P.has_din) | (F.pre_any ? 2 : 0) |
+                            int(last && P.has_dout) << 2 | int(gstore) << 3;
+            const uint64_t il = base_local + rowoff[eb >> low_run] + (uint64_t(eb) & lowmask);
+            uint64_t okb[kRegLog2];
+#pragma unroll
+            for (int j = 0; j < kRegLog2; ++j) okb[j] = gstore ? goff(R.dk[1 << j]) : 0;
+            double2* gb = gbase + (gstore ? goff(eb) : 0);
+            const int acq = gstore || skip_acq ? 0 : turn_me;
+            if (!gstore) skip_acq = false, used_w = true;
+            QSB_FBP(false, false, PREOK, DIAGOK, sel, a, P, R, F, ct, mats, st, il, W, sb, skb, gb, okb, acq)
+            if (gstore) break;
+            named_sync(gbar, kTileThreads);
+        }
+        if (!direct) {
+            double2* gb = gbase + goff(tid);
+            const int s_tid = sig_of(tid);
+#pragma unroll
+            for (int i = 0; i < kLoadsPerThread; ++i)
+                gb[goff(i * kTileThreads)] = W[s_tid ^ sig_of(i * kTileThreads)];
+            named_sync(gbar, kTileThreads);
+            named_arrive(turn_other, 2 * kTileThreads);
+        }
+    }
+    // group 1's last hand-over has no taker: consume it
+    if (group == 0 && used_w) named_sync(turn_me, 2 * kTileThreads);
+}
+
+size_t fact_pair_smem_bytes() {
+    return 3 * size_t(kTileBytes) + sizeof(uint64_t) * (kTileAmps >> kLowBits) +
+           sizeof(uint64_t) * 256 * kDepTables +
+           sizeof(uint32_t) * (kMaxRounds + 1) * ((1 << kLaneLoBits) + (1 << kLaneHiBits)) +
+           sizeof(uint64_t) + sizeof(unsigned) + 8;
+}
+
+// The 13-bit map of a pair: the 12-bit plan's tile pieces in its order, the
+// pair bit p as its own dim -- dim 1 when p = 3 (256-byte rows), the last dim
+// when p is above every tile qubit -- and every non-tile run riding on the dim
+// just below it in qubit order.  Round 0's deposits re-swizzled for L.
+bool pair_plan(const FactPass& F, const TmaPieces& T, double2* psi, PairPass* X) {
+    static const bool off = getenv("QSB_NO_PAIR") != nullptr;
+    if (off || F.low_run < 3 || (F.num_tiles & 1)) return false;
+    const int m = F.m;
+    uint32_t is_tile = 0;
+    for (int q = 0; q < kTileLog2; ++q) is_tile |= 1u << F.tile_bits[q];
+    int p = 0;
+    while (p < m && ((is_tile >> p) & 1)) ++p;
+    if (p >= m || p >= 31) return false;
+    // only where the pair doubles 128-byte rows: contiguous tiles (pass 1 of the
+    // sweep) measured slower paired (6.2 -> 6.8 ms)
+    const bool pair_row = p == 3;
+    static const bool any_pair = getenv("QSB_PAIR_ALL") != nullptr;
+    if (!pair_row && (!any_pair || p < F.tile_bits[kTileLog2 - 1])) return false;
+    if (uint64_t(1) << (m - kTileLog2) < 2) return false;
+    const uint64_t num_states = F.num_tiles / F.tiles_per_state;
+    // dims: (lo, len, box bits); the pair dim first or last among the pieces
+    struct D { int lo, len; };
+    std::vector<D> dims;  // tile dims after dim0, in smem order
+    if (pair_row) dims.push_back({3, 1});
+    for (int i = 0; i < T.npieces; ++i) dims.push_back({T.piece_lo[i], T.piece_len[i]});
+    if (!pair_row) dims.push_back({p, 1});
+    if (1 + dims.size() > 5) return false;
+    // non-tile runs of the 13-bit set, each on the dim below it
+    const uint32_t set13 = is_tile | (1u << p);
+    struct N { int lo, len, field_shift; bool states; };
+    std::vector<N> nontile;
+    int below = 0;
+    for (int q = 0; q < m;) {
+        if ((set13 >> q) & 1) { ++q; continue; }
+        int e = q;
+        while (e + 1 < m && !((set13 >> (e + 1)) & 1)) ++e;
+        nontile.push_back({q, e - q + 1, below, false});
+        below += e - q + 1;
+        q = e + 1;
+    }
+    if (num_states > 1) {
+        if (!nontile.empty() && nontile.back().lo + nontile.back().len == m) nontile.back().states = true;
+        else nontile.push_back({m, 0, below, true});
+    }
+    cuuint64_t gdim[5], gstride[4];
+    cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+    uint64_t ext[5];
+    ext[0] = 16;
+    box[0] = 16;
+    for (size_t i = 0; i < dims.size(); ++i) {
+        ext[i + 1] = uint64_t(1) << dims[i].len;
+        gstride[i] = uint64_t(sizeof(double2)) << dims[i].lo;
+        box[i + 1] = 1u << dims[i].len;
+    }
+    X->ncoord = 0;
+    for (const N& n : nontile) {
+        int host = -1;
+        for (size_t i = 0; i < dims.size() && host < 0; ++i)
+            if (dims[i].lo + dims[i].len == n.lo) host = int(i) + 1;
+        if (host < 0 && n.lo == 3) host = 0;
+        if (host < 0 || X->ncoord >= 5) return false;
+        const int lsh = host == 0 ? 4 : dims[host - 1].len;
+        ext[host] *= (uint64_t(1) << n.len) * (n.states ? num_states : 1);
+        const int k = X->ncoord++;
+        X->coord_dim[k] = host;
+        X->coord_shift[k] = n.field_shift;
+        X->coord_lsh[k] = lsh;
+        X->coord_mask[k] = n.states ? ~uint64_t(0) : (uint64_t(1) << n.len) - 1;
+    }
+    const int rank = int(dims.size()) + 1;
+    for (int i = 0; i < rank; ++i) {
+        if (ext[i] > (uint64_t(1) << 31)) return false;
+        gdim[i] = ext[i];
+    }
+    for (int i = rank; i < 5; ++i) {  // 5-d map: unit dims on top
+        gdim[i] = 1;
+        gstride[i - 1] = gstride[i - 2] * 2;
+        box[i] = 1;
+    }
+    if (encode_fn()(&X->map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, psi, gdim, gstride, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    // smem bit of each tile position in L: 0..2 for qubits 0..2, then the dims in order
+    auto pos_of = [&](int q) {
+        for (int i = 0; i < kTileLog2; ++i)
+            if (F.tile_bits[i] == q) return i;
+        return -1;
+    };
+    int pos_bit[kTileLog2], bit = 3, pbit = -1;
+    for (int i = 0; i < 3; ++i) pos_bit[i] = i;
+    for (const D& d : dims)
+        for (int q = d.lo; q < d.lo + d.len; ++q) {
+            if (q == p) pbit = bit++;
+            else pos_bit[pos_of(q)] = bit++;
+        }
+    if (bit != kTileLog2 + 1 || pbit < 0) return false;
+    auto sigma = [&](int e) {
+        int v = 0;
+        for (int i = 0; i < kTileLog2; ++i)
+            if ((e >> i) & 1) v |= 1 << pos_bit[i];
+        return v ^ ((v >> 3) & 7);
+    };
+    X->gx = (1 << pbit) ^ (((1 << pbit) >> 3) & 7);
+    const Round& R0 = F.rounds[0];
+    for (int v = 0; v < (1 << kLaneLoBits); ++v) X->slo0[v] = uint16_t(sigma(R0.dlo[v]));
+    for (int v = 0; v < (1 << kLaneHiBits); ++v) X->shi0[v] = uint16_t(sigma(R0.dhi[v]));
+    for (int v = 0; v < (1 << kRegLog2); ++v) X->sk0[v] = uint16_t(sigma(R0.dk[v]));
+    return true;
+}
+
+template <bool PO, bool DG>
+void launch_fact_pair_variant(double2* psi, const FactPass& F, const double* mats,
+                              const CutTerms& ct, const TmaPass& T, const PairPass& X,
+                              cudaStream_t s) {
+    constexpr int kMaxDevices = 64;
+    static std::atomic<int> configured[kMaxDevices];
+    static int sms_of[kMaxDevices];
+    const size_t smem = fact_pair_smem_bytes();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (configured[dev].load(std::memory_order_acquire) == 0) {
+        cudaFuncSetAttribute(k_fact_pair<PO, DG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        sms_of[dev] = sms;
+        configured[dev].store(1, std::memory_order_release);
+    }
+    uint64_t grid = uint64_t(sms_of[dev]);
+    const uint64_t need = F.num_tiles / 2;
+    if (grid > need) grid = need;
+    k_fact_pair<PO, DG><<<unsigned(grid), kTmaThreads, smem, s>>>(psi, F, mats, ct, T, X);
+}
+
 bool launch_fact_tma(double2* psi, FactPass& F, const double* mats, const CutTerms& ct,
                      bool tables, bool phase, cudaStream_t s) {
     static thread_local TmaPass T;
-    if (!tma_plan(F, psi, &T)) return false;
+    static thread_local TmaPieces pieces;
+    if (!tma_plan(F, psi, &T, &pieces)) return false;
     bool pre = false;
     for (int r = 0; r < F.num_rounds; ++r) pre |= F.fr[r].pre_any != 0;
     const bool diag = F.has_din || F.has_dout;
+    if (!tables && !phase) {
+        static thread_local PairPass X;
+        if (pair_plan(F, pieces, psi, &X)) {
+            if (pre) {
+                if (diag) launch_fact_pair_variant<true, true>(psi, F, mats, ct, T, X, s);
+                else launch_fact_pair_variant<true, false>(psi, F, mats, ct, T, X, s);
+            } else {
+                if (diag) launch_fact_pair_variant<false, true>(psi, F, mats, ct, T, X, s);
+                else launch_fact_pair_variant<false, false>(psi, F, mats, ct, T, X, s);
+            }
+            return true;
+        }
+    }
     const int v = int(tables) | int(phase) << 1 | int(pre) << 2 | int(diag) << 3;
     switch (v) {
 #define QSB_TMA_CASE(V) \
