@@ -92,7 +92,10 @@ class GateQueue:
         self._add(_native.QS_KIND_CTRL, t, c, u.view(np.float64), u.ndim == 3)
         self.touched.update((c, t))
 
-    def cut_phase(self, graph, gamma) -> None:
+    def cut_phase(self, graph, gamma, luts=None) -> None:
+        """`luts`: the (S, |E|+1) per-state LUTs of phase_lut_batch(gamma), when
+        the caller built them already (run_circuit_pool builds all of a
+        circuit's LUT batches concurrently)."""
         edges = edge_array(graph)
         if self.edges is not None and not np.array_equal(self.edges, edges):
             self.flush()
@@ -103,7 +106,8 @@ class GateQueue:
             lut = phase_lut(float(gam), len(edges))
             self._add(_native.QS_KIND_CUTPHASE, 0, -1, lut.view(np.float64), False)
         else:
-            luts = phase_lut_batch(gam, len(edges))
+            if luts is None:
+                luts = phase_lut_batch(gam, len(edges))
             self._add(_native.QS_KIND_CUTPHASE, 0, -1, luts.view(np.float64), True)
 
     def flush(self) -> int:
@@ -633,6 +637,18 @@ class PoolState:
         return self.state.download().reshape(self.num_states, -1)
 
 
+_LUT_POOL = None
+
+
+def _lut_pool():
+    global _LUT_POOL
+    if _LUT_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _LUT_POOL = ThreadPoolExecutor(max_workers=4, thread_name_prefix="qsb-lut")
+    return _LUT_POOL
+
+
 def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
                      noise_stream=None) -> None:
     """Every pool state runs `circuit`; state s binds slot_tables[name][s]
@@ -659,6 +675,16 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
     q = ctx.queue
     pre = _circuit_noise(ctx, circuit.gates, noise_stream)
     rot_cache: dict = {}
+    # the per-state cut-phase LUTs (S x (|E|+1) complex exps per slot, ~0.4 ms
+    # each for 512 states) are built concurrently: numpy releases the GIL
+    lut_jobs = {(g.slot, len(g.graph.edges)) for g in circuit.gates
+                if g.kind == "diagcost" and isinstance(getattr(g, "param", None), str)
+                and g.slot in tables}
+    lut_cache = {}
+    if len(lut_jobs) > 1 and ctx.batch and len(next(iter(tables.values()))) >= 64:
+        jobs = sorted(lut_jobs)
+        lut_cache = dict(zip(jobs, _lut_pool().map(
+            lambda j: phase_lut_batch(tables[j[0]], j[1]), jobs)))
     for gate in circuit.gates:
         slot = gate.slot if isinstance(getattr(gate, "param", None), str) else None
         if slot is None:
@@ -671,7 +697,7 @@ def run_circuit_pool(ctx: RankContext, circuit, slot_tables: dict | None = None,
             raise ValueError(f"gate {gate.kind} has unbound slot ${slot}")
         vals = tables[slot]
         if gate.kind == "diagcost":
-            q.cut_phase(gate.graph, vals)
+            q.cut_phase(gate.graph, vals, lut_cache.get((slot, len(gate.graph.edges))))
         elif gate.kind in gates_mod.ROTATION_GATES:
             # one table per (rotation, slot): every gate bound to the slot shares it
             key = ("rot", gate.kind, slot)

@@ -59,7 +59,8 @@ T.clear()
 prof = cProfile.Profile()
 t0 = time.perf_counter()
 for k in range(10):
-    step(prof if k == 0 else None)
+    step(prof)
 wall = 1e3 * (time.perf_counter() - t0) / 10
 print({k: round(float(np.mean(v)), 3) for k, v in T.items()}, "wall/step", round(wall, 3))
-pstats.Stats(prof).sort_stats("cumulative").print_stats(18)
+pstats.Stats(prof).sort_stats("cumulative").print_stats(25)
+pstats.Stats(prof).sort_stats("tottime").print_stats(15)
