@@ -54,7 +54,7 @@ def parse():
                     help="factored: QS_FUSE_FACTORED (Euler-factored 1q gates, within 1e-12 "
                          "of the reference); exact: QS_FUSE_EXACT (bit-identical)")
     ap.add_argument("--workload", default=None,
-                    choices=["sweep", "qaoa", "cfg3", "cfg4", "noise"],
+                    choices=["sweep", "qaoa", "cfg1", "cfg3", "cfg4", "noise"],
                     help="default: sweep (config 2) at N=1, cfg4 (config 4, weak-scaled) at N>1")
     ap.add_argument("--ref-local-qubits", type=int, default=23,
                     help="reference arm at N>1: amplitudes per thread-rank (host RAM bound)")
@@ -210,6 +210,49 @@ def cpu_sweep_sample(m: int, gates: int, seed: int) -> dict:
             "sample": f"{len(targets)} single-gate applications (targets {targets}) on a "
                       f"2^{m} complex128 state, oracle/cpu_baseline.py (numpy, "
                       f"{cb.threads()} threads), {dt:.2f} s"}
+
+
+def cpu_controlled_sample(m: int, pair, phi_u, seed: int) -> dict:
+    """Config 3's CPU baseline: the reference's controlled-gate kernel
+    (statevector.py:180-195, oracle/cpu_baseline.py threaded port) for the
+    first seeded pair's CNOT, CPhase and controlled Haar on a 2^m state."""
+    from oracle import cpu_baseline as cb
+
+    c, t = pair
+    phi, u = phi_u
+    psi = np.full(1 << m, 2.0 ** (-m / 2.0), dtype=np.complex128)
+    mats = [np.array([[0, 1], [1, 0]], dtype=np.complex128),
+            np.diag([1.0, np.exp(1j * phi)]).astype(np.complex128), u]
+    cb.apply_1q_threaded(psi, 0, np.eye(2, dtype=np.complex128))  # warm (page faults)
+    t0 = time.perf_counter()
+    for mat in mats:
+        cb.apply_controlled_threaded(psi, c, t, mat)
+    dt = time.perf_counter() - t0
+    units = len(mats) * (2.0 ** m) / 2.0 ** 30
+    return {"value": units / dt, "unit": UNIT, "cores": cb.threads(), "kind": "port",
+            "sample": f"CNOT, CPhase and controlled Haar on pair (c={c}, t={t}) of a 2^{m} "
+                      f"complex128 state, oracle/cpu_baseline.py (numpy, {cb.threads()} "
+                      f"threads), {dt:.2f} s"}
+
+
+def cpu_layer_sample(m: int, cx, seed: int) -> dict:
+    """Config 4's CPU baseline at one GPU (every qubit local): two Haar gates
+    of the layer and its first CX(q, n-1-q), reference kernels, threaded port."""
+    from oracle import cpu_baseline as cb
+
+    rng = np.random.default_rng(seed)
+    psi = np.full(1 << m, 2.0 ** (-m / 2.0), dtype=np.complex128)
+    X = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+    cb.apply_1q_threaded(psi, 0, np.eye(2, dtype=np.complex128))  # warm (page faults)
+    t0 = time.perf_counter()
+    cb.apply_1q_threaded(psi, 0, haar(rng))
+    cb.apply_1q_threaded(psi, m - 1, haar(rng))
+    cb.apply_controlled_threaded(psi, cx[0], cx[1], X)
+    dt = time.perf_counter() - t0
+    units = 3 * (2.0 ** m) / 2.0 ** 30
+    return {"value": units / dt, "unit": UNIT, "cores": cb.threads(), "kind": "port",
+            "sample": f"Haar on qubits 0 and {m - 1} + CX{tuple(cx)} of a 2^{m} complex128 "
+                      f"state, oracle/cpu_baseline.py (numpy, {cb.threads()} threads), {dt:.2f} s"}
 
 
 def haar(rng):
@@ -400,6 +443,8 @@ def run_ours(args):
     transport = qtp.TorchTransport(exchange_mode=args.exchange) if world > 1 else None
     if args.workload == "qaoa":
         return run_qaoa(args, dist, transport, world, rank, local)
+    if args.workload == "cfg1":
+        return run_cfg1(args, dist, world, rank, local)
     if args.workload == "noise":
         return run_noise(args, dist, transport, world, rank, local)
     ctx = runtime.make_context(transport, n, 1, device=local, fuse=fuse_mode(args),
@@ -536,7 +581,12 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and m <= 30:
-        cpu = cpu_sweep_sample(m, 3, args.seed)
+        if cfg3:
+            cpu = cpu_controlled_sample(m, pairs[0], sweeps[0][0], args.seed)
+        elif cx_pairs:
+            cpu = cpu_layer_sample(m, cx_pairs[0], args.seed)
+        else:
+            cpu = cpu_sweep_sample(m, 3, args.seed)
 
     # config 2's per-target table: each target as a single unfused gate kernel
     per_target = (per_target_table(st, m, args.seed)
@@ -988,6 +1038,84 @@ def run_qaoa(args, dist, comm, world, rank, local):
     barrier(dist)
     return 0
 
+
+
+def run_cfg1(args, dist, world, rank, local):
+    """BASELINE config 1 (n=20, 10 layers of H/RX/RZ + brick CNOTs, 295 gates,
+    |0...0>), the reference's CPU-runnable case, through the public API: a
+    step is one runtime.simulate_circuit call -- context, the fused program,
+    and the download of the full 2^20-amplitude state, as the reference
+    returns it (runtime.py:291-302).  Every rank runs its own replica."""
+    from paper_2001_10554_b200 import runtime
+    from paper_2001_10554_b200.circuit import Circuit
+    from paper_2001_10554_b200.workloads import config1_gates
+
+    n = 20
+    circ = Circuit(n, tuple(config1_gates(n, 10, args.seed)))
+    psi = None
+    for _ in range(args.warmup):
+        psi = runtime.simulate_circuit(circ, device=local)
+    barrier(dist)
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        psi = runtime.simulate_circuit(circ, device=local)
+    wall = time.perf_counter() - t0
+    clock = clocks.stop()
+    wall = max_over_ranks(dist, wall)
+    gates = len(circ.gates)
+    units = world * args.steps * gates * (2.0 ** n) / 2.0 ** 30
+    # kernels one call launches (a context made the way simulate_circuit makes it)
+    cctx = runtime.make_context(None, n, 1, 0, device=local)
+    cctx.state.launch_log(True)
+    runtime.run_circuit(cctx, circ)
+    cctx.flush()
+    cctx.state.synchronize()
+    cctx.state.launch_log(False)
+    launches = len(cctx.state.read_launch_log()[0])
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import circuit as ocirc
+
+        prog = [{"kind": g.kind, "qubits": g.qubits, "param": g.param} for g in circ.gates]
+        t1 = time.perf_counter()
+        ref = ocirc.run(n, prog)
+        dt = time.perf_counter() - t1
+        cpu = {"value": gates * (2.0 ** n) / 2.0 ** 30 / dt, "unit": UNIT, "cores": 1,
+               "kind": "port",
+               "sample": f"one config-1 circuit ({gates} gates, n={n}) through the oracle's "
+                         f"gate-by-gate restatement of run_circuit (numpy, 1 thread), {dt:.2f} s",
+               "max_abs_diff_vs_ours": float(np.max(np.abs(ref - psi))),
+               "bit_identical_to_ours": bool(np.array_equal(ref.view(np.uint64),
+                                                            np.asarray(psi).view(np.uint64)))}
+    if rank == 0:
+        value = units / wall
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "c128 (f64 pairs)", "data": "synthetic",
+            "config": {"workload": f"config 1: n={n}, 10 layers of H/RX(theta)/RZ(theta) per qubit "
+                                   f"+ brick CNOTs ({gates} gates) from |0...0>, one "
+                                   "runtime.simulate_circuit call per step (exact numerics, "
+                                   "full state downloaded)",
+                       "gates_per_step": gates, "replicas": world,
+                       "l2": "state (16 MiB) fits in L2: an API-latency workload, not a "
+                             "roofline run"},
+            "circuits_per_s": world * args.steps / wall,
+            "roofline": None,
+            "gpu_launches": int(launches * args.steps),
+            "clocks": clock,
+            "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 16 * (2 ** n),
+                    "note": "the step is the public API call itself: gate list in, the "
+                            "full state out"},
+        }
+        print(json.dumps(line))
+    barrier(dist)
+    return 0
 
 PASS_KINDS = ("k_tile", "k_fact")
 

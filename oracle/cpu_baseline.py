@@ -56,3 +56,58 @@ def apply_1q_threaded(psi: np.ndarray, q: int, u: np.ndarray, block: int = 1 << 
         for i in range(0, nb, rows):
             tasks.append((slice(i, min(nb, i + rows)), slice(0, step)))
     list(_pool().map(lambda t: work(*t), tasks))
+
+
+def apply_controlled_threaded(psi: np.ndarray, control: int, target: int, u: np.ndarray,
+                              block: int = 1 << 18) -> None:
+    """In-place 2x2 on `target` over the amplitudes with `control` = 1
+    (statevector.py:180-195: the same ufunc expression on the control=1
+    pairs), on strided views split over host threads."""
+    hi, lo = max(control, target), min(control, target)
+    n = int(np.log2(psi.size))
+    v = psi.reshape(1 << (n - hi - 1), 2, 1 << (hi - lo - 1), 2, 1 << lo)
+    sub = v[:, 1] if control == hi else v[:, :, :, 1]  # control = 1
+    # target axis: 2 (lo) of (A, M, L, B) or 1 (hi) of (A, H, M, B)
+    tax = 2 if control == hi else 1
+    u00, u01, u10, u11 = u[0, 0], u[0, 1], u[1, 0], u[1, 1]
+
+    def work(sl):
+        s = sub[sl]
+        a = s.take(0, axis=tax)
+        b = s.take(1, axis=tax)
+        na = u00 * a + u01 * b
+        nb = u10 * a + u11 * b
+        idx0 = [slice(None)] * 4
+        idx1 = [slice(None)] * 4
+        idx0[tax], idx1[tax] = 0, 1
+        s[tuple(idx0)] = na
+        s[tuple(idx1)] = nb
+
+    # split the outermost axis (or the middle one when it is short)
+    A = sub.shape[0]
+    if A >= threads():
+        step = max(1, A // (4 * threads()))
+        tasks = [slice(i, min(A, i + step)) for i in range(0, A, step)]
+        list(_pool().map(work, tasks))
+    else:
+        for i in range(A):
+            s = sub[i:i + 1]
+            M = s.shape[1] if tax == 2 else s.shape[2]
+            ax = 1 if tax == 2 else 2
+            step = max(1, M // (4 * threads()))
+
+            def work_m(j, s=s, ax=ax, step=step):
+                sl = [slice(None)] * 4
+                sl[ax] = slice(j, min(M, j + step))
+                t = s[tuple(sl)]
+                a = t.take(0, axis=tax)
+                b = t.take(1, axis=tax)
+                na = u00 * a + u01 * b
+                nb = u10 * a + u11 * b
+                i0 = [slice(None)] * 4
+                i1 = [slice(None)] * 4
+                i0[tax], i1[tax] = 0, 1
+                t[tuple(i0)] = na
+                t[tuple(i1)] = nb
+
+            list(_pool().map(work_m, range(0, M, step)))
