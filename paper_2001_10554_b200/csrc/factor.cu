@@ -40,6 +40,15 @@ using cd = std::complex<double>;
 
 cd unit(cd z) { return z / std::abs(z); }
 
+// K * (re + i im) without libgcc's IEEE-special-case complex multiply
+// (__muldc3), and max(|Re|, |Im|) for the rescale trigger instead of a hypot:
+// the per-state loops of a 512-state QAOA program (80 gates x 512 states)
+// run 1.1 ms -> less on the host
+inline cd scale_by(cd k, double re, double im) {
+    return cd(k.real() * re - k.imag() * im, k.real() * im + k.imag() * re);
+}
+inline double mag_bound(cd k) { return std::max(std::fabs(k.real()), std::fabs(k.imag())); }
+
 cd entry(const double* u, int i) { return cd(u[2 * i], u[2 * i + 1]); }
 
 bool is_unitary(const cd u[4]) {
@@ -271,8 +280,8 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
                 any_pre |= pre[st] != 1.0;
                 za_s[st] = cd(f[2], f[3]);
                 t[st] = f[7];
-                Ks[st] *= cd(f[0], f[1]) * f[8];
-                small = std::min(small, std::abs(Ks[st]));
+                Ks[st] = scale_by(Ks[st], f[0] * f[8], f[1] * f[8]);
+                small = std::min(small, mag_bound(Ks[st]));
             }
             per_state_rows(kKindShear, q, t, pre, any_pre);
             out->factored++;
@@ -297,8 +306,8 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             const double p[8] = {f[7], 0, has_pre ? 1.0 : 0.0, 0, has_pre ? pre.real() : 1.0,
                                  has_pre ? pre.imag() : 0.0, 0, 0};
             out->extra.insert(out->extra.end(), p, p + 8);
-            Ks[st] *= cd(f[0], f[1]) * f[8];
-            small = std::min(small, std::abs(Ks[st]));
+            Ks[st] = scale_by(Ks[st], f[0] * f[8], f[1] * f[8]);
+            small = std::min(small, mag_bound(Ks[st]));
         }
         qs_gate s8;
         memset(&s8, 0, sizeof(s8));
