@@ -816,7 +816,11 @@ struct alignas(16) FactPass {
 template <int J, bool PRE, bool TABLES>
 __device__ __forceinline__ void fact_shear(double2 (&a)[kRegAmps], const FactRound& F, int grp,
                                            const double* __restrict__ mats, uint64_t st) {
+#ifdef QSB_EXP_SHARED_T  // diagnostics build: per-state t replaced by the shared one
+    const double t = F.t[grp][J];
+#else
     const double t = TABLES ? __ldg(mats + F.toff[grp][J] + st * F.tstride[grp][J]) : F.t[grp][J];
+#endif
     if (PRE) {
         // pool passes read the state's pre-diagonal from its row (per-state
         // diagonals of noise trajectories; (1, 0) where there is none)
@@ -854,6 +858,9 @@ __device__ __forceinline__ void fact_run(double2 (&a)[kRegAmps], const FactRound
 __device__ __forceinline__ void fact_cut_phase(double2 (&a)[kRegAmps], const FactPass& P,
                                                const Round& R, const CutTerms& ct,
                                                const double2* lut, uint64_t il) {
+#ifdef QSB_EXP_NOCUT  // diagnostics build: no cut phase arithmetic
+    return;
+#endif
     const uint64_t i = P.rank_offset | il;
     const int cut0 = cut_of(i, ct);
     int rq[kRegLog2], d[kRegLog2], bq[kRegLog2];

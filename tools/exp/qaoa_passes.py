@@ -17,6 +17,7 @@ for s in range(S):
         tables.setdefault(k, np.empty(S))[s] = v
 fuse = "factored" if (sys.argv[1] if len(sys.argv) > 1 else "exact") == "factored" else True
 ctx = runtime.make_context(None, n, num_states=S, fuse=fuse)
+ctx.norm_check_interval = 0  # diagnostics builds (QSB_EXP_*) break the norm on purpose
 runtime.run_circuit_pool(ctx, circ, tables)
 ctx.state.synchronize()
 ctx.state.launch_log(True)
