@@ -36,7 +36,7 @@ METRIC = "gate-updates/s and achieved HBM GB/s (n=30 c128); weak-scaled n=33-36 
 UNIT = "gate-updates/s (n=30-equivalent: 1 unit = one 2x2 gate on 2^30 c128 amplitudes)"
 FP64_PEAK_TOPS = 62 * 148 * 1.965e9 / 1e12  # measured on B200 (tools/exp/fp64.cu)
 LAUNCH_KINDS = {1: "k_gate1q", 2: "k_controlled", 3: "k_cut_phase", 4: "k_tile",
-                5: "k_exchange_peer", 6: "k_tree", 7: "k_fact"}
+                5: "k_exchange_peer", 6: "k_tree", 7: "k_fact", 8: "k_fact_gen"}
 
 
 def parse():
@@ -62,6 +62,11 @@ def parse():
                     help="N=1 sweep: skip the config-4 n=33 point of the weak-scaling curve")
     ap.add_argument("--seed", type=int, default=20260809)
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--pool-chunks", type=int, default=1,
+                    help="qaoa: the GPU's share of the pool as this many batched sub-pools, so "
+                         "the host builds chunk k+1's program while chunk k runs (each chunk "
+                         "has its own stream: per-launch times overlap, so the pass roofline "
+                         "is only meaningful with 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"])
     ap.add_argument("--no-per-target", action="store_true")
@@ -933,9 +938,10 @@ def run_qaoa(args, dist, comm, world, rank, local):
     circ = build_qaoa_circuit(graph, depth)
     exact = qopt.exact_maxcut(graph)
     swarm = qopt.init_swarm(S, 2 * depth, stream=pool_stream.split(1))
-    ctx = runtime.make_context(None, n, count, args.seed, device=local, fuse=fuse_mode(args))
-    ctx.norm_check_interval = 0
-    st = ctx.state
+    ctxs = qopt.pool_contexts(n, count, args.pool_chunks, args.seed, device=local,
+                              fuse=fuse_mode(args))
+    for c in ctxs:
+        c.norm_check_interval = 0
     edges = np.asarray(graph.edges, dtype=np.int32)
     host_ms = []
 
@@ -951,9 +957,7 @@ def run_qaoa(args, dist, comm, world, rank, local):
 
     def step():
         pos = np.stack([swarm.particles[k].position for k in range(first, first + count)])
-        runtime.reset_state(ctx)
-        runtime.run_circuit_pool(ctx, circ, qopt.qaoa_slot_tables(pos, depth))
-        mine = ctx.pool.observable(3, 0, edges) / exact
+        mine = qopt.evaluate_swarm(ctxs, circ, pos, depth, edges) / exact
         values = share(np.asarray(mine, dtype=np.float64))
         t = time.perf_counter()
         qopt.step_swarm(swarm, values)
@@ -962,19 +966,27 @@ def run_qaoa(args, dist, comm, world, rank, local):
 
     for _ in range(args.warmup):
         step()
-    st.synchronize()
+    for c in ctxs:
+        c.state.synchronize()
     barrier(dist)
     host_ms.clear()
     clocks = ClockSampler(local)
     clocks.start()
-    st.launch_log(True)
+    for c in ctxs:
+        c.state.launch_log(True)
+    folds0 = {id(c): c.pool.state.uniform_folds for c in ctxs}
     t0 = time.perf_counter()
     for _ in range(args.steps):
         values = step()
-    st.synchronize()
+    for c in ctxs:
+        c.state.synchronize()
     wall = time.perf_counter() - t0
-    st.launch_log(False)
-    launch_ms, launch_kind = st.read_launch_log()
+    logs = []
+    for c in ctxs:
+        c.state.launch_log(False)
+        logs.append(c.state.read_launch_log())
+    launch_ms = np.concatenate([l[0] for l in logs])
+    launch_kind = np.concatenate([l[1] for l in logs])
     clock = clocks.stop()
     wall = max_over_ranks(dist, wall)
     gates_per_circuit = len(circ.gates)
@@ -987,7 +999,22 @@ def run_qaoa(args, dist, comm, world, rank, local):
     dev_ms = sum(sum(v) for v in kinds.values())
     peak, peak_src = measured_peak()
     gates_per_step = count * len(circ.gates)
-    pass_kinds = [k for k in kinds if LAUNCH_KINDS.get(k, "") in ("k_tile", "k_fact", "k_fact_tma")]
+    pass_kinds = [k for k in kinds if LAUNCH_KINDS.get(k, "") in PASS_KINDS]
+    # bytes the pass launches move: a read + write of the chunk's states (32 B per
+    # amplitude); a pass that generates its uniform input in registers
+    # (k_fact_gen) only writes; in the exact mode the uniform state is filled
+    # (16 B per amplitude) inside the first pass's launch scope
+    pass_bytes_total = 0.0
+    folds = 0
+    for c, (_, lk) in zip(ctxs, logs):
+        amps_c = c.num_states * 2.0 ** n
+        for k in lk:
+            name = LAUNCH_KINDS.get(int(k), "")
+            if name in PASS_KINDS:
+                pass_bytes_total += (16.0 if name == "k_fact_gen" else 32.0) * amps_c
+        filled = c.pool.state.uniform_folds - folds0[id(c)] - int(np.sum(np.asarray(lk) == 8))
+        pass_bytes_total += 16.0 * amps_c * max(0, filled)
+        folds += c.pool.state.uniform_folds - folds0[id(c)]
     passes_per_step = sum(len(kinds[k]) for k in pass_kinds) / args.steps
     pass_ms = sum(sum(kinds[k]) for k in pass_kinds) / args.steps
     cpu = None
@@ -1011,7 +1038,9 @@ def run_qaoa(args, dist, comm, world, rank, local):
                                    f"--particles {S} --seed {args.seed}: keyed random 3-regular "
                                    "graph (pool_stream.split(0)), keyed swarm "
                                    "(pool_stream.split(1)), one swarm step = the 512 "
-                                   "circuits as one pool program + <C> + step_swarm",
+                                   "circuits as pool programs (one per sub-pool chunk, the "
+                                   "reset + Hadamard layer folded into a uniform start) + <C> "
+                                   "+ step_swarm",
                        "pool": S, "per_gpu": count, "swarm_steps": args.steps,
                        "gates_per_circuit": gates_per_circuit, "fused": not args.no_fuse,
                        "numerics": args.numerics,
@@ -1021,8 +1050,12 @@ def run_qaoa(args, dist, comm, world, rank, local):
             "global_best_ratio": float(swarm.global_best_value),
             "host_pso_ms_per_step": float(np.mean(host_ms)) if host_ms else None,
             "pass_ms_per_step": pass_ms, "passes_per_step": passes_per_step,
-            "roofline": pool_roofline(kinds, 32.0 * (2 ** n) * count, count * (2 ** n),
-                                      gates_per_step / count, peak, peak_src, "qaoa", args.steps),
+            "roofline": pool_roofline(kinds, 32.0 * (2 ** n) * count / len(ctxs),
+                                      count * (2 ** n) / len(ctxs),
+                                      gates_per_step / count, peak, peak_src, "qaoa",
+                                      args.steps * len(ctxs), total_bytes=pass_bytes_total),
+            "pool_chunks": len(ctxs),
+            "uniform_start_folds_per_step": folds / args.steps,
             "kernel_share": {LAUNCH_KINDS.get(k, str(k)): {"launches": len(v),
                                                            "share": float(np.sum(v) / dev_ms)}
                              for k, v in kinds.items()},
@@ -1117,10 +1150,11 @@ def run_cfg1(args, dist, world, rank, local):
     barrier(dist)
     return 0
 
-PASS_KINDS = ("k_tile", "k_fact")
+PASS_KINDS = ("k_tile", "k_fact", "k_fact_gen")
 
 
-def pool_roofline(kinds, pass_bytes, amps, gates_per_state, peak, peak_src, tag, steps):
+def pool_roofline(kinds, pass_bytes, amps, gates_per_state, peak, peak_src, tag, steps,
+                  total_bytes=None):
     """Roofline of a pool step's fused passes (every k_fact / k_tile launch):
     achieved = one read + write of this GPU's pool per pass (32 B per
     amplitude) x passes / their summed launch time; traffic = ncu dram bytes
@@ -1131,7 +1165,8 @@ def pool_roofline(kinds, pass_bytes, amps, gates_per_state, peak, peak_src, tag,
     n = sum(len(v) for v in passes.values())
     ms = sum(sum(v) for v in passes.values())
     dom = max(passes, key=lambda k: sum(passes[k])) if passes else None
-    achieved = pass_bytes * n / (ms / 1e3) / 1e9 if ms else None
+    moved = pass_bytes * n if total_bytes is None else total_bytes
+    achieved = moved / (ms / 1e3) / 1e9 if ms else None
     tr = ncu_traffic(f"{dom}@{tag}") if dom else None
     traffic = tr["bytes_per_amplitude"] * amps if tr and tr.get("bytes_per_amplitude") else None
     return {"kernel": "+".join(sorted(passes)), "bound": "hbm", "achieved": achieved, "peak": peak,

@@ -159,6 +159,19 @@ int qs_apply_cut_phase(qs_state* st, const int32_t* edges, int32_t num_edges,
 int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count,
                      const double* mats, uint64_t mats_len,
                      const int32_t* edges, int32_t num_edges, int32_t fuse);
+/* init_uniform-style start (statevector.py:137-141) fused with the program:
+ * every amplitude of every state is (re, im) before the first gate, whatever
+ * the state held.  The result equals qs_init_constant followed by
+ * qs_apply_program bit for bit; lean pool passes generate the constant in
+ * registers instead of reading it (no fill, no tile loads in the first pass).
+ * The Python runtime calls it for a program that starts with H on every qubit
+ * of a freshly reset |0..0> (the QAOA pool circuits of optimize.py:172-216):
+ * H^(x)n |0..0> is the constant fl(..fl(fl(1*h)*h)..*h), h = fl(1/sqrt 2), in
+ * the reference's own arithmetic, so the fold keeps the exact mode bit-identical. */
+int qs_apply_program_on_constant(qs_state* st, double re, double im,
+                                 const qs_gate* gates, int32_t count,
+                                 const double* mats, uint64_t mats_len,
+                                 const int32_t* edges, int32_t num_edges, int32_t fuse);
 /* Planner only, no device needed: first gate index of every pass the fused
  * program would launch (starts[0..min(cap, *npasses))).  QS_FUSE_FACTORED is
  * planned as QS_FUSE_EXACT here (its rewrite needs the matrices). */
@@ -252,8 +265,9 @@ int qs_event_record(qs_state* st, int32_t slot);
 int qs_event_elapsed_ms(qs_state* st, int32_t slot_a, int32_t slot_b, float* ms);
 /* Per-launch log: with enable != 0 every kernel launch is bracketed by CUDA
  * events; qs_launch_log_read returns (and clears) durations in ms and kind
- * codes (1 gate1q, 2 controlled, 3 cut phase, 4 tile pass, 5 exchange,
- * 6 reduction). */
+ * codes (1 gate1q, 2 controlled, 3 cut phase, 4 tile pass (k_tile), 5 exchange,
+ * 6 reduction, 7 lean factored pass (k_fact*), 8 lean factored pass with a
+ * generated constant input -- write-only, qs_apply_program_on_constant). */
 int qs_launch_log(qs_state* st, int32_t enable);
 int qs_launch_log_read(qs_state* st, float* ms, int32_t* kinds, int32_t cap, int32_t* count);
 

@@ -28,7 +28,7 @@ EXPORTS = (
     "qs_init_zero", "qs_init_basis", "qs_init_constant", "qs_init_gaussian", "qs_scale",
     "qs_apply_diagonal", "qs_state_diff",
     "qs_apply_1q", "qs_apply_controlled", "qs_apply_cut_phase", "qs_apply_program",
-    "qs_plan_program", "qs_last_program_passes", "qs_observable", "qs_marginals",
+    "qs_apply_program_on_constant", "qs_plan_program", "qs_last_program_passes", "qs_observable", "qs_marginals",
     "qs_exchange_gate_peer", "qs_exchange_gate_nccl", "qs_swap_qubits_peer",
     "qs_swap_qubits_local", "qs_state_ipc_handle", "qs_peer_open",
     "qs_peer_close", "qs_nccl_unique_id", "qs_comm_init", "qs_comm_destroy",
@@ -96,6 +96,8 @@ _SIGNATURES = {
     "qs_apply_controlled": ([_P, _I, _I, _DP, _U], ctypes.c_int),
     "qs_apply_cut_phase": ([_P, _IP, _I, _DP, _U], ctypes.c_int),
     "qs_apply_program": ([_P, ctypes.POINTER(QsGate), _I, _DP, _U, _IP, _I, _I], ctypes.c_int),
+    "qs_apply_program_on_constant": ([_P, _D, _D, ctypes.POINTER(QsGate), _I, _DP, _U, _IP, _I, _I],
+                                     ctypes.c_int),
     "qs_plan_program": ([_I, ctypes.POINTER(QsGate), _I, _I, _IP, _I, _IP], ctypes.c_int),
     "qs_last_program_passes": ([_P, _IP], ctypes.c_int),
     "qs_observable": ([_P, _I, _I, _IP, _I, _DP], ctypes.c_int),
@@ -237,6 +239,37 @@ def u64ptr(a: np.ndarray):
     return a.ctypes.data_as(_U64P)
 
 
+_H_BITS = (np.array([[1, 1], [1, -1]], dtype=np.complex128) / np.sqrt(2.0)).tobytes()
+
+
+def leading_hadamard_layer(gates, mats: np.ndarray, num_qubits: int) -> int:
+    """num_qubits when the program starts with one shared-matrix H (the bits of
+    gates.HADAMARD, gates.py:15) on every qubit, in any order; 0 otherwise."""
+    if len(gates) < num_qubits:
+        return 0
+    seen = 0
+    for k in range(num_qubits):
+        g = gates[k]
+        if g.kind != QS_KIND_1Q or g.stride != 0 or not (0 <= g.target < num_qubits):
+            return 0
+        if (seen >> g.target) & 1:
+            return 0
+        if mats[g.offset:g.offset + 8].tobytes() != _H_BITS:
+            return 0
+        seen |= 1 << g.target
+    return num_qubits
+
+
+def hadamard_chain(num_qubits: int) -> float:
+    """The amplitude of H^(x)n |0..0> as statevector.pair_update computes it
+    gate by gate (statevector.py:144-150): n roundings of v * fl(1/sqrt 2)."""
+    h = float(np.frombuffer(_H_BITS, dtype=np.float64)[0])
+    v = 1.0
+    for _ in range(num_qubits):
+        v = v * h
+    return v
+
+
 class DeviceState:
     """Owning handle of one qs_state (num_states partitions of 2^m amplitudes)."""
 
@@ -253,12 +286,30 @@ class DeviceState:
         self.num_states = num_states
         self.device = device
         self.amps_per_state = 1 << num_local_qubits
+        self._pending_basis = None
 
     @property
     def handle(self):
+        """The qs_state pointer for a native call.  A deferred basis-state
+        reset (defer_basis) is carried out first, so every access to the
+        device state -- whatever the entry point -- sees the reset state."""
         if self._h is None:
             raise ValueError("state was destroyed")
+        if self._pending_basis is not None:
+            index, self._pending_basis = self._pending_basis, None
+            check(load().qs_init_basis(self._h, index))
         return self._h
+
+    def defer_basis(self, index: int = 0) -> None:
+        """init_basis_state(index), carried out at the next access.  A program
+        that arrives first and starts with H on every qubit of |0..0> runs from
+        the uniform state instead (apply_program), and the reset is never
+        written to HBM."""
+        if self._h is None:
+            raise ValueError("state was destroyed")
+        if not (0 <= index < (1 << self.num_qubits)):
+            raise ValueError(f"basis index {index} out of range for {self.num_qubits} qubits")
+        self._pending_basis = int(index)
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None:
@@ -273,6 +324,7 @@ class DeviceState:
 
     # ---- data movement --------------------------------------------------------
     uploads = 0  # amplitudes uploaded through this handle (host -> device)
+    uniform_folds = 0  # programs run from the uniform state (reset + Hadamard layer folded)
 
     def upload(self, amps: np.ndarray, offset: int = 0) -> None:
         a = np.ascontiguousarray(amps, dtype=np.complex128).ravel()
@@ -354,8 +406,20 @@ class DeviceState:
     def apply_program(self, gates: list[QsGate] | ctypes.Array, mats: np.ndarray,
                       edges: np.ndarray | None = None, fuse: bool = True) -> int:
         n = len(gates)
-        arr = gates if isinstance(gates, ctypes.Array) else (QsGate * n)(*gates)
         mats = np.ascontiguousarray(mats, dtype=np.float64)
+        uniform = None
+        if self._pending_basis == 0 and self.num_qubits == self.num_local_qubits:
+            lead = leading_hadamard_layer(gates, mats, self.num_qubits)
+            if lead:
+                # H^(x)n |0..0>: every amplitude is the same product chain in the
+                # reference's arithmetic (each H multiplies the one non-zero
+                # amplitude of its pair by fl(1/sqrt 2) and adds a signed zero)
+                self._pending_basis = None
+                self.uniform_folds += 1
+                gates = list(gates)[lead:]
+                n = len(gates)
+                uniform = hadamard_chain(self.num_qubits)
+        arr = gates if isinstance(gates, ctypes.Array) else (QsGate * n)(*gates)
         if edges is None:
             e = np.zeros(2, dtype=np.int32)
             ne = 0
@@ -364,8 +428,12 @@ class DeviceState:
             ne = e.size // 2
             if ne == 0:
                 e = np.zeros(2, dtype=np.int32)
-        call("qs_apply_program", self.handle, arr, n, dptr(mats), mats.size, iptr(e), ne,
-             fuse_code(fuse))
+        if uniform is not None:
+            call("qs_apply_program_on_constant", self.handle, uniform, 0.0, arr, n, dptr(mats),
+                 mats.size, iptr(e), ne, fuse_code(fuse))
+        else:
+            call("qs_apply_program", self.handle, arr, n, dptr(mats), mats.size, iptr(e), ne,
+                 fuse_code(fuse))
         passes = ctypes.c_int32(0)
         call("qs_last_program_passes", self.handle, ctypes.byref(passes))
         return passes.value

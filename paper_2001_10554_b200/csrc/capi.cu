@@ -251,7 +251,8 @@ struct LaunchScope {
 };
 
 enum { kLaunchGate1q = 1, kLaunchControlled = 2, kLaunchPhase = 3, kLaunchTile = 4,
-       kLaunchExchange = 5, kLaunchReduce = 6, kLaunchFact = 7 };
+       kLaunchExchange = 5, kLaunchReduce = 6, kLaunchFact = 7,
+       kLaunchFactGen = 8 /* lean pass with a generated (constant) input: write-only */ };
 
 bool is_diag_one(const double* e) {
     return e[0] == 1.0 && e[1] == 0.0 && e[2] == 0.0 && e[3] == 0.0 && e[4] == 0.0 && e[5] == 0.0;
@@ -499,8 +500,8 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     }
     {
         LaunchScope ls(st, kLaunchTile);
-        if (launch_tile_pass(st->psi, P, st->d_pass, st->d_mats, ct, st->stream))
-            ls.rec.kind = kLaunchFact;
+        const int lean = launch_tile_pass(st->psi, P, st->d_pass, st->d_mats, ct, st->stream);
+        if (lean) ls.rec.kind = lean == 2 ? kLaunchFactGen : kLaunchFact;
     }
     CHECK_LAUNCH();
     return QS_OK;
@@ -876,12 +877,17 @@ int qs_apply_diagonal(qs_state* st, const double* factors, uint64_t offset, uint
     return QS_OK;
 }
 
-int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const double* mats,
-                     uint64_t mats_len, const int32_t* edges, int32_t num_edges, int32_t fuse) {
+namespace {
+// const_in: every amplitude of the state is (re, im) before the program (the
+// first pass generates it or a fill precedes it); nullptr: the state as it is.
+int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const double* mats,
+                       uint64_t mats_len, const int32_t* edges, int32_t num_edges, int32_t fuse,
+                       const double* const_in) {
     if (!st) return fail(QS_ERR_VALUE, "null state");
     if (count < 0) return fail(QS_ERR_VALUE, "negative gate count");
     if (count == 0) {
         st->last_passes = 0;
+        if (const_in) return qs_init_constant(st, const_in[0], const_in[1]);
         return QS_OK;
     }
     if (int rc = ensure_device(st)) return rc;
@@ -931,12 +937,22 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
     t_upload = now();
     std::vector<PassPlan> plan = plan_passes(gates, count, st->m, fuse != 0);
     int passes = 0;
+    if (const_in)
+        g_const_in = {true, make_double2(const_in[0], const_in[1]),
+                      st->amps_per_state * uint64_t(st->num_states)};
     for (const PassPlan& pp : plan) {
         // the internal kinds of a factored program only exist as tile-pass gates
         const bool single = pp.count == 1 && gates[pp.first].kind <= QS_KIND_CUTPHASE;
+        if (single && g_const_in.on) {  // the streaming kernels read their input from HBM
+            launch_fill(st->psi, g_const_in.total, g_const_in.v, st->stream);
+            g_const_in.on = false;
+        }
         int rc = single ? launch_single(st, gates[pp.first], ct, mats)
                         : launch_tile(st, gates, pp.first, pp.count, ct, mats);
-        if (rc) return rc;
+        if (rc) {
+            g_const_in.on = false;
+            return rc;
+        }
         ++passes;
     }
     st->last_passes = passes;
@@ -951,6 +967,19 @@ int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const do
     // no host sync: pageable H2D copies are staged before cudaMemcpyAsync returns,
     // so the caller may reuse `mats`, and the device tables are stream-ordered.
     return QS_OK;
+}
+}  // namespace
+
+int qs_apply_program(qs_state* st, const qs_gate* gates, int32_t count, const double* mats,
+                     uint64_t mats_len, const int32_t* edges, int32_t num_edges, int32_t fuse) {
+    return apply_program_impl(st, gates, count, mats, mats_len, edges, num_edges, fuse, nullptr);
+}
+
+int qs_apply_program_on_constant(qs_state* st, double re, double im, const qs_gate* gates,
+                                 int32_t count, const double* mats, uint64_t mats_len,
+                                 const int32_t* edges, int32_t num_edges, int32_t fuse) {
+    const double c[2] = {re, im};
+    return apply_program_impl(st, gates, count, mats, mats_len, edges, num_edges, fuse, c);
 }
 
 // Planning only (no device needed): writes the first gate index of every

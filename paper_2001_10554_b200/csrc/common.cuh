@@ -177,10 +177,20 @@ void launch_controlled(double2* psi, int m, int num_states, int c, int t, const 
 void launch_cut_phase(double2* psi, int m, int num_states, uint64_t rank_offset,
                       const CutTerms& ct, const double* mats, uint64_t offset, uint64_t stride,
                       cudaStream_t s);
+// qs_apply_program_on_constant: the program's input is `v` in every amplitude
+// (`total` amplitudes).  The first pass either generates it in registers (lean
+// pool passes on the TMA kernel) or is preceded by a fill; whoever does clears `on`.
+struct ConstIn {
+    bool on;
+    double2 v;
+    uint64_t total;
+};
+extern thread_local ConstIn g_const_in;
 bool tile_pass_in_params();  // k_tile takes the pass as a kernel parameter
-// returns true when the pass ran on the lean factored kernel (k_fact)
-bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
-                      const double* mats, const CutTerms& ct, cudaStream_t s);
+// returns 0: k_tile, 1: the lean factored kernels (k_fact*), 2: a lean pass that
+// generated a constant input (g_const_in) instead of loading its tiles
+int launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
+                     const double* mats, const CutTerms& ct, cudaStream_t s);
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s);
 void launch_set_basis(double2* psi, uint64_t stride, uint64_t states, uint64_t off, cudaStream_t s);
 void launch_gaussian(double2* psi, uint64_t count_per_state, int num_states, uint64_t rank_offset,

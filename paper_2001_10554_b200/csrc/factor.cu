@@ -233,11 +233,20 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         out->gates.push_back(g);
     };
     std::vector<double> fs;
+    // the 20 mixers of a QAOA layer share one per-state table (GateQueue keys):
+    // its factorisation is computed once, and the shear rows are emitted once
+    // per (table, pre-diagonal)
+    uint64_t fs_off = ~uint64_t(0), fs_stride = 0;
+    bool fs_same = true;
+    struct RowKey { uint64_t off, stride, at; bool has_pre; cd pre; };
+    std::vector<RowKey> row_cache;
     auto per_state_shear = [&](const qs_gate& g) {
         const int q = g.target;
         fs.resize(size_t(num_states) * 10);
         bool same = true;
-        for (int st = 0; st < num_states; ++st) {
+        const bool cached = g.offset == fs_off && g.stride == fs_stride && g.offset < mats_len;
+        if (cached) same = fs_same;
+        for (int st = 0; st < num_states && !cached; ++st) {
             double* f = fs.data() + 10 * st;
             const double* u = mat(g, st);
             // RX(theta) = [[c, -is], [-is, c]] = c * diag(1, i) [[1,-t],[t,1]] diag(1, -i)
@@ -248,6 +257,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
                 f[2] = 0.0, f[3] = 1.0, f[4] = 0.0, f[5] = -1.0;
                 f[6] = 0.0, f[7] = u[3] / u[0], f[8] = std::abs(u[0]), f[9] = 0.0;
             } else if (!decompose_2x2(u, f)) {
+                fs_off = ~uint64_t(0);  // fs is partly overwritten
                 return false;
             }
             if (st == 0 && (f[3] < 0 || (f[3] == 0 && f[2] < 0))) {
@@ -266,6 +276,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             }
             same = false;
         }
+        fs_off = g.offset, fs_stride = g.stride, fs_same = same;
         if (!same || !psp[q].empty()) {
             // per-state diagonals: every state's pre-diagonal and pending za
             // are its own (no product diagonal at the program ends)
@@ -297,15 +308,28 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         bool has_pre = false;
         if (!mixed[q]) din[q] *= pre;
         else has_pre = pre != 1.0;
-        while (out->extra.size() % 2) out->extra.push_back(0.0);
-        const uint64_t off = mats_len + out->extra.size();
+        uint64_t off = ~uint64_t(0);
+        if (g.offset < mats_len)
+            for (const RowKey& k : row_cache)
+                if (k.off == g.offset && k.stride == g.stride && k.has_pre == has_pre &&
+                    (!has_pre || k.pre == pre))
+                    off = k.at;
+        const bool emit = off == ~uint64_t(0);
+        if (emit) {
+            while (out->extra.size() % 2) out->extra.push_back(0.0);
+            off = mats_len + out->extra.size();
+            if (g.offset < mats_len) row_cache.push_back({g.offset, g.stride, off, has_pre, pre});
+            out->extra.reserve(out->extra.size() + size_t(num_states) * 8);
+        }
         double small = 1.0;
         for (int st = 0; st < num_states; ++st) {
             const double* f = fs.data() + 10 * st;
-            // z is (1, 0) without a pre-diagonal: lean pool passes read it per state
-            const double p[8] = {f[7], 0, has_pre ? 1.0 : 0.0, 0, has_pre ? pre.real() : 1.0,
-                                 has_pre ? pre.imag() : 0.0, 0, 0};
-            out->extra.insert(out->extra.end(), p, p + 8);
+            if (emit) {
+                // z is (1, 0) without a pre-diagonal: lean pool passes read it per state
+                const double p[8] = {f[7], 0, has_pre ? 1.0 : 0.0, 0, has_pre ? pre.real() : 1.0,
+                                     has_pre ? pre.imag() : 0.0, 0, 0};
+                out->extra.insert(out->extra.end(), p, p + 8);
+            }
             Ks[st] = scale_by(Ks[st], f[0] * f[8], f[1] * f[8]);
             small = std::min(small, mag_bound(Ks[st]));
         }

@@ -804,9 +804,12 @@ struct FactRound {
 struct alignas(16) FactPass {
     int32_t m, num_rounds, low_run, direct_store;
     int32_t tile_bits[kTileLog2];
-    int32_t ntab, has_din, has_dout, pad;
+    int32_t ntab, has_din, has_dout;
+    int32_t const_in;            // the pass input is the constant `cin` (no tile loads): a
+                                 // program that starts from a uniform state (TABLES kernels)
     uint64_t tiles_per_state, num_tiles, rank_offset;
     uint64_t din_off, dout_off;  // DiagN tables in mats (doubles)
+    double2 cin;
     double2 din_r[1 << kRegLog2], dout_r[1 << kRegLog2];  // register parts (TilePass::diag_r)
     uint64_t nbr[64];            // cut-phase graph (TilePass::nbr)
     Round rounds[kMaxRounds];
@@ -1438,7 +1441,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (threadIdx.x == 0 && blockIdx.x < P.num_tiles) {
+    // pool programs that start from a uniform state (H on every qubit of |0..0>,
+    // folded by the host): the first pass takes its input from P.cin, no loads
+    const bool const_in = TABLES && P.const_in != 0;
+    if (threadIdx.x == 0 && blockIdx.x < P.num_tiles && !const_in) {
         tma_load_tile(T, blockIdx.x, Lbuf, full);
         for (int d = 1; d <= T.prefetch; ++d) {
             const uint64_t t = blockIdx.x + uint64_t(d) * gridDim.x;
@@ -1475,7 +1481,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const uint64_t st = tile_id >> tps_log2;
         const uint64_t base_local = tile_base(tile_id);
         double2* gbase = psi + ((st << m) | base_local);
-        mbar_wait(full + group, parity);
+        if (!const_in) mbar_wait(full + group, parity);
         for (int r = 0; r < P.num_rounds; ++r) {
             const Round& R = P.rounds[r];
             const bool last = r == P.num_rounds - 1;
@@ -1495,9 +1501,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             };
             const double2* src = r == 0 ? Lbuf : W;
             double2 a[kRegAmps];
+            if (r == 0 && const_in) {
+                const double2 c = P.cin;
 #pragma unroll
-            for (int kk = 0; kk < kRegAmps; ++kk) a[kk] = src[sb ^ sk_of(kk)];
-            if (r == 0) {
+                for (int kk = 0; kk < kRegAmps; ++kk) a[kk] = c;
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < kRegAmps; ++kk) a[kk] = src[sb ^ sk_of(kk)];
+            }
+            if (r == 0 && !const_in) {
                 // the group has read L: request the next tile (the other group's)
                 named_sync(gbar, kTileThreads);
                 if (tid == 0) {
@@ -2382,8 +2394,8 @@ void launch_tile_variant(double2* psi, const TilePass& pass, const TilePass* pas
 #endif
 }
 
-bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
-                      const double* mats, const CutTerms& ct, cudaStream_t s) {
+int launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
+                     const double* mats, const CutTerms& ct, cudaStream_t s) {
     bool phase = false, generic = false, tables = false, fact = false;
     for (int r = 0; r < pass.num_rounds; ++r) {
         const Round& R = pass.rounds[r];
@@ -2407,18 +2419,35 @@ bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_d
     }
     const uint64_t nt = pass.num_tiles;
     static const bool lean_ok = getenv("QSB_NO_LEAN") == nullptr;
+    ConstIn& cin = g_const_in;
+    auto fill_now = [&] {  // the constant input written out (no kernel takes it virtually)
+        if (cin.on) launch_fill(psi, cin.total, cin.v, s);
+        cin.on = false;
+    };
     if (fact && !generic && kGroups == 1 && lean_ok) {
         static thread_local FactPass F;
         bool tb = false, ph = false;
         if (fact_pass_from(pass, &F, &tb, &ph)) {
-            if (!launch_fact_tma(psi, F, mats, ct, tb, ph, s)) launch_fact(psi, F, mats, ct, tb, ph, s);
-            return true;
+            // a pool pass on the TMA kernel generates a constant input in
+            // registers (no fill, no tile loads); everything else fills first
+            const bool virt = cin.on && tb;
+            if (!virt) fill_now();
+            if (virt) F.const_in = 1, F.cin = cin.v;
+            if (launch_fact_tma(psi, F, mats, ct, tb, ph, s)) {
+                cin.on = false;
+                return virt ? 2 : 1;
+            }
+            F.const_in = 0;
+            fill_now();
+            launch_fact(psi, F, mats, ct, tb, ph, s);
+            return 1;
         }
     }
+    fill_now();
 #define QSB_TILE_CASE(PH, GE, TB, FA) \
     if (phase == PH && generic == GE && tables == TB && fact == FA) {       \
         launch_tile_variant<PH, GE, TB, FA>(psi, pass, pass_dev, mats, ct, nt, s); \
-        return false;                                                        \
+        return 0;                                                            \
     }
 #define QSB_TILE_CASES(FA)               \
     QSB_TILE_CASE(false, false, false, FA) \
@@ -2433,8 +2462,10 @@ bool launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_d
     QSB_TILE_CASES(true)
 #undef QSB_TILE_CASES
 #undef QSB_TILE_CASE
-    return false;
+    return 0;
 }
+
+thread_local ConstIn g_const_in = {false, {0.0, 0.0}, 0};
 
 int prof_read(unsigned long long* out) {
 #ifdef QSB_PROF

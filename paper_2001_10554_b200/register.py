@@ -33,7 +33,7 @@ class QubitRegister:
         if kind == "base":
             if not (0 <= index < (1 << self.num_qubits)):
                 raise ValueError(f"basis index {index} out of range")
-            _native.call("qs_init_basis", self.state.handle, index)
+            self.state.defer_basis(index)
         elif kind == "uniform":
             _native.call("qs_init_constant", self.state.handle,
                          2.0 ** (-self.num_qubits / 2.0), 0.0)

@@ -338,7 +338,10 @@ def reset_state(ctx: RankContext, index: int = 0) -> None:
     if ctx.partition is not None:
         sv.init_basis_state(ctx.partition, index)
     else:
-        _native.call("qs_init_basis", ctx.pool.state.handle, index)
+        # deferred to the next access: a program of H on every qubit first (the
+        # QAOA pool circuits) starts from the uniform state and the reset is
+        # never written (DeviceState.defer_basis)
+        ctx.pool.state.defer_basis(index)
     ctx.gates_applied = 0
 
 
@@ -626,7 +629,7 @@ class PoolState:
         self.num_states = num_states
         self.state = _native.DeviceState(num_qubits, num_qubits, 0, num_states, device)
         self.queue = GateQueue(self.state, fuse)
-        _native.call("qs_init_basis", self.state.handle, 0)
+        self.state.defer_basis(0)
 
     def observable(self, kind: int, q: int = 0, edges=None) -> np.ndarray:
         self.queue.flush()

@@ -248,7 +248,10 @@ def init_basis_state(partition: StatePartition, index: int) -> StatePartition:
         raise ValueError(
             f"basis index {index} out of range for {partition.num_qubits} qubits")
     partition._drop_mirror()
-    _native.call("qs_init_basis", partition.state.handle, index)
+    if partition.num_local_qubits == partition.num_qubits:
+        partition.state.defer_basis(index)  # carried out at the next access of the device state
+    else:
+        _native.call("qs_init_basis", partition.state.handle, index)
     return partition
 
 
