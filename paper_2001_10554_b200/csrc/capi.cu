@@ -517,7 +517,8 @@ struct PassPlan {
     int first, count;
 };
 
-std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool fuse) {
+std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool fuse,
+                                  bool lean_first = false) {
     std::vector<PassPlan> out;
     const bool tile_ok = fuse && m >= kTileLog2;
     int i = 0;
@@ -529,9 +530,13 @@ std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool f
             uint64_t round_set = kind_has_target(gates[i].kind) ? (uint64_t(1) << gates[i].target) : 0;
             int rounds = 1;
             int diags = gates[i].kind == kKindDiagN;
+            bool pass_lean = kind_is_lean(gates[i].kind);
             while (j < count && j - i < kMaxPassGates) {
                 const qs_gate& g = gates[j];
                 if (g.kind == kKindDiagN && diags >= kMaxPassDiags) break;
+                // a pass of lean kinds stays on the lean kernels (schedule_program)
+                if (lean_first && pass_lean && !kind_is_lean(g.kind)) break;
+                pass_lean = pass_lean && kind_is_lean(g.kind);
                 diags += g.kind == kKindDiagN;
                 uint64_t nn = need, rs = round_set;
                 int nr = rounds;
@@ -908,6 +913,7 @@ int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const 
     static const bool dbg_time = getenv("QSB_DEBUG_TIME") != nullptr;
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto t_start = now(), t_factor = t_start, t_upload = t_start, t_fp = t_start;
+    bool lean_first = false;
     if (fuse == QS_FUSE_FACTORED && st->m >= kTileLog2) {
         // rewrite, then plan the rewritten program; its parameters and diagonal
         // tables follow the caller's table in one upload.  Programs where fewer
@@ -915,18 +921,26 @@ int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const 
         // rewrite does not pay there.
         uint64_t support = 0;
         for (int e = 0; e < 2 * num_edges; ++e) support |= uint64_t(1) << edges[e];
-        factor_program(gates, count, mats, mats_len, st->m, st->num_states, num_edges, support, &fp);
+        // large states: an extra pass costs less than moving a lean pass to k_tile
+        // (QSB_LEAN_FIRST_M moves the threshold; read per call so tests can set it)
+        const char* lf = getenv("QSB_LEAN_FIRST_M");
+        lean_first = st->m >= (lf ? atoi(lf) : 24);
+        factor_program(gates, count, mats, mats_len, st->m, st->num_states, num_edges, support, &fp,
+                       lean_first);
         t_fp = now();
         if (2 * fp.factored >= count) {
             all.assign(mats, mats + mats_len);
             all.insert(all.end(), fp.extra.begin(), fp.extra.end());
             static const bool reorder = getenv("QSB_NO_REORDER") == nullptr;
-            if (reorder) schedule_program(fp.gates, st->m, support, all.data(), st->num_states);
+            if (reorder)
+                schedule_program(fp.gates, st->m, support, all.data(), st->num_states, lean_first);
             g_zero_off = fp.zero_off;
             gates = fp.gates.data();
             count = int(fp.gates.size());
             mats = all.data();
             mats_len = all.size();
+        } else {
+            lean_first = false;  // the program runs exact: the plain planner
         }
     }
     t_factor = now();
@@ -935,7 +949,7 @@ int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const 
         CUDA_TRY(cudaMemcpyAsync(st->d_mats, mats, mats_len * sizeof(double),
                                  cudaMemcpyHostToDevice, st->stream));
     t_upload = now();
-    std::vector<PassPlan> plan = plan_passes(gates, count, st->m, fuse != 0);
+    std::vector<PassPlan> plan = plan_passes(gates, count, st->m, fuse != 0, lean_first);
     int passes = 0;
     if (const_in)
         g_const_in = {true, make_double2(const_in[0], const_in[1]),

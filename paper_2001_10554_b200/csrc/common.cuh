@@ -147,6 +147,10 @@ constexpr int kKindDiag1 = 17;  // params [0, 0, 0, 0, z.re, z.im, 0, 0]: amplit
 constexpr int kKindDiagN = 18;  // psi_i *= prod_c T_c[byte c of i]; `reserved` = table count;
                                 // offset -> ntab*256 complex byte tables, then 64 complex z_q
 constexpr int kKindScalar = 19; // per-state scalar (stride 8): psi_s *= (params[0], params[1])
+// kinds a lean factored pass (k_fact*) can hold; everything else runs on k_tile
+inline bool kind_is_lean(int kind) {
+    return kind == kKindShear || kind == kKindDiagN || kind == QS_KIND_CUTPHASE;
+}
 inline bool kind_has_target(int kind) {
     return kind != QS_KIND_CUTPHASE && kind != kKindDiagN && kind != kKindScalar;
 }
@@ -159,12 +163,19 @@ struct FactoredProgram {
 };
 // Rewrites gates[0..count) (validated, all local) into `out`.  mats_len is the
 // size of the caller's table (the extra entries are appended after it).
+// batch_flush (large states, with schedule_program's lean_first): the pending
+// diagonals of the targets of a run of controlled gates leave as one product
+// diagonal before the run instead of one Diag1 per target.
 void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
-                    int num_states, int num_edges, uint64_t phase_support, FactoredProgram* out);
+                    int num_states, int num_edges, uint64_t phase_support, FactoredProgram* out,
+                    bool batch_flush = false);
 // Commutation-aware re-order of a factored program for the pass planner
 // (phase_support: the cut-phase graph's vertices).
+// lean_first: passes of lean kinds only are kept free of the other kinds (which
+// would move the whole pass from k_fact* to k_tile); worth an extra pass on
+// large states.
 void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support,
-                      const double* mats, int num_states);
+                      const double* mats, int num_states, bool lean_first = false);
 // U = k diag(1,za) R diag(1,zb): out = [k, za, zb] (complex), 0, t, scale (= c).
 // Returns false when U is not unitary to 1e-12, exactly diagonal or c < 1e-9.
 bool decompose_2x2(const double* u, double out[10]);

@@ -109,7 +109,8 @@ bool decompose_2x2(const double* m, double out[10]) {
 }
 
 void factor_program(const qs_gate* gates, int count, const double* mats, uint64_t mats_len, int m,
-                    int num_states, int num_edges, uint64_t phase_support, FactoredProgram* out) {
+                    int num_states, int num_edges, uint64_t phase_support, FactoredProgram* out,
+                    bool batch_flush) {
     out->gates.clear();
     out->extra.clear();
     out->factored = 0;
@@ -414,8 +415,14 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
                 continue;
             }
             if (g.kind == QS_KIND_CTRL) {
-                emit_acc(g.target);
-                emit_acc(g.control);
+                // batch_flush: the 1q gates of every qubit the run of controlled
+                // gates touches come before its first gate, so that their
+                // pending diagonals can leave as ONE product diagonal
+                for (int j = i; j < count && gates[j].kind == QS_KIND_CTRL; ++j) {
+                    emit_acc(gates[j].target);
+                    emit_acc(gates[j].control);
+                    if (!batch_flush) break;
+                }
             } else {  // cut phase: every vertex of the graph
                 for (int q = 0; q < m; ++q)
                     if ((phase_support >> q) & 1) emit_acc(q);
@@ -433,6 +440,24 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
         const int q = g.target;
         if (g.kind == QS_KIND_CTRL) {
             if (!diagonal_for_all_states(g)) {
+                if (batch_flush) {
+                    // the pending diagonals of every target this run of controlled
+                    // gates mixes: one product diagonal (a lean op, 2 complex
+                    // products per amplitude) instead of a Diag1 per target on k_tile
+                    std::vector<int> ts;
+                    for (size_t j = i; j < prog.size() && prog[j].kind == QS_KIND_CTRL; ++j) {
+                        const int t = prog[j].target;
+                        if (diagonal_for_all_states(prog[j]) || !psp[t].empty() || !mixed[t] ||
+                            pending[t] == 1.0 || std::find(ts.begin(), ts.end(), t) != ts.end())
+                            continue;
+                        ts.push_back(t);
+                    }
+                    if (ts.size() >= 4) {
+                        std::vector<cd> z(m, cd(1.0));
+                        for (int t : ts) z[t] = pending[t], pending[t] = 1.0;
+                        out->gates.push_back(diag_tables(z, cd(1.0)));
+                    }
+                }
                 flush(q);
                 mixed[q] = 1;
             }
@@ -584,7 +609,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
 // pair [RX(0..11), cut, RX(0..11)] then shares one pass: the config-5 pool
 // circuit needs 6 passes instead of 10.
 void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support,
-                      const double* mats, int num_states) {
+                      const double* mats, int num_states, bool lean_first) {
     const int n = int(gates.size());
     if (n < 3) return;
     const uint64_t all = m >= 64 ? ~uint64_t(0) : (uint64_t(1) << m) - 1;
@@ -632,15 +657,28 @@ void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support
     while (!ready.empty()) {
         uint64_t need = low, round_set = 0;
         int rounds = 1, count = 0, diags = 0;
+        bool pass_lean = true;
         for (;;) {
             int pick = -1;
             uint64_t pick_need = 0, pick_rs = 0;
             int pick_nr = 0;
+            // lean_first: a pass opens with a lean gate when one is ready, and a
+            // pass of lean gates takes no other kind (config 4: the Haar layer
+            // stays on the lean kernels, the CNOTs get their own k_tile passes)
+            bool lean_ready = false;
+            if (lean_first && count == 0)
+                for (int gi : ready) lean_ready |= kind_is_lean(gates[gi].kind);
             // preference: no new register round and no new tile bit, then no
             // new tile bit, then program order
             for (int tier = 0; tier < 3 && pick < 0; ++tier) {
                 for (size_t k = 0; k < ready.size(); ++k) {
                     const qs_gate& g = gates[ready[k]];
+                    if (lean_first) {
+                        const bool lean = kind_is_lean(g.kind);
+                        if (count == 0 && lean_ready && !lean) continue;
+                        if (count > 0 && pass_lean && !lean) continue;
+                        if (count > 0 && !pass_lean && lean && tier == 2) continue;
+                    }
                     uint64_t nn = need, rs = round_set;
                     int nr = rounds;
                     if (kind_has_target(g.kind)) {
@@ -671,6 +709,7 @@ void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support
             out.push_back(gates[gi]);
             need = pick_need, round_set = pick_rs, rounds = pick_nr;
             ++count;
+            pass_lean = pass_lean && kind_is_lean(gates[gi].kind);
             diags += gates[gi].kind == kKindDiagN;
             for (int j : succ[gi])
                 if (--npred[j] == 0) ready.insert(std::lower_bound(ready.begin(), ready.end(), j), j);

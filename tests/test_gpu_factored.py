@@ -482,3 +482,31 @@ def test_factored_pool_two_rescales_keep_their_place():
     assert np.all(np.isfinite(got))
     assert np.max(np.abs(got)) > 1e-6
     assert max_dev(got, expected) <= TOL
+
+
+def test_factored_lean_first_schedule(monkeypatch):
+    """Large states keep passes of lean kinds (shears, product diagonals, cut
+    phases) free of controlled gates, which would move the whole pass to k_tile
+    (QSB_LEAN_FIRST_M lowers the m >= 24 threshold for this test): same results
+    within tolerance as the mixed schedule, on config-4-like layers and random
+    mixed programs."""
+    rng = np.random.default_rng(4242)
+    n = 14
+    progs = []
+    layer = [{"kind": "custom", "qubits": (q,), "matrix": ogates.random_unitary_2x2(rng)}
+             for q in range(n)]
+    layer += [{"kind": "cu", "qubits": (q, n - 1 - q), "matrix": X} for q in range(n // 2)]
+    layer2 = [{"kind": "custom", "qubits": (q,), "matrix": ogates.random_unitary_2x2(rng)}
+              for q in range(n)]
+    progs.append((layer + layer2 + layer, [(0, 3)]))
+    progs.append(mixed_program(n, 120, rng))
+    for prog, edges in progs:
+        psi0 = ogates.random_state(n, rng)
+        expect = ocirc.run(n, prog, psi0)
+        monkeypatch.setenv("QSB_LEAN_FIRST_M", "12")
+        got, passes_lean = run_queue(n, prog, edges, psi0, FACT)
+        assert max_dev(got, expect) <= TOL
+        monkeypatch.setenv("QSB_LEAN_FIRST_M", "99")
+        got2, passes_mixed = run_queue(n, prog, edges, psi0, FACT)
+        assert max_dev(got2, expect) <= TOL
+        assert passes_lean >= passes_mixed
