@@ -36,7 +36,7 @@ METRIC = "gate-updates/s and achieved HBM GB/s (n=30 c128); weak-scaled n=33-36 
 UNIT = "gate-updates/s (n=30-equivalent: 1 unit = one 2x2 gate on 2^30 c128 amplitudes)"
 FP64_PEAK_TOPS = 62 * 148 * 1.965e9 / 1e12  # measured on B200 (tools/exp/fp64.cu)
 LAUNCH_KINDS = {1: "k_gate1q", 2: "k_controlled", 3: "k_cut_phase", 4: "k_tile",
-                5: "k_exchange_peer", 6: "k_tree", 7: "k_fact", 8: "k_fact_gen"}
+                5: "k_exchange_peer", 6: "k_tree", 7: "k_fact", 8: "k_fact_gen", 9: "k_perm"}
 
 
 def parse():

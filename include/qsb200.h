@@ -267,7 +267,8 @@ int qs_event_elapsed_ms(qs_state* st, int32_t slot_a, int32_t slot_b, float* ms)
  * events; qs_launch_log_read returns (and clears) durations in ms and kind
  * codes (1 gate1q, 2 controlled, 3 cut phase, 4 tile pass (k_tile), 5 exchange,
  * 6 reduction, 7 lean factored pass (k_fact*), 8 lean factored pass with a
- * generated constant input -- write-only, qs_apply_program_on_constant). */
+ * generated constant input -- write-only, qs_apply_program_on_constant,
+ * 9 CNOT-only pass of a factored program as one permutation (k_perm)). */
 int qs_launch_log(qs_state* st, int32_t enable);
 int qs_launch_log_read(qs_state* st, float* ms, int32_t* kinds, int32_t cap, int32_t* count);
 

@@ -236,6 +236,7 @@ int build_cut_terms(const int32_t* edges, int32_t num_edges, int n, CutTerms* ct
 struct LaunchScope {
     qs_state* st;
     LaunchRec rec{};
+    bool cancelled = false;  // nothing was launched: no record
     LaunchScope(qs_state* s, int kind) : st(s) {
         if (!st->launch_log) return;
         rec.kind = kind;
@@ -245,6 +246,11 @@ struct LaunchScope {
     }
     ~LaunchScope() {
         if (!st->launch_log) return;
+        if (cancelled) {
+            cudaEventDestroy(rec.start);
+            cudaEventDestroy(rec.stop);
+            return;
+        }
         cudaEventRecord(rec.stop, st->stream);
         st->recs.push_back(rec);
     }
@@ -252,7 +258,8 @@ struct LaunchScope {
 
 enum { kLaunchGate1q = 1, kLaunchControlled = 2, kLaunchPhase = 3, kLaunchTile = 4,
        kLaunchExchange = 5, kLaunchReduce = 6, kLaunchFact = 7,
-       kLaunchFactGen = 8 /* lean pass with a generated (constant) input: write-only */ };
+       kLaunchFactGen = 8 /* lean pass with a generated (constant) input: write-only */,
+       kLaunchPerm = 9 /* CNOT-only pass of a factored program as one permutation (k_perm) */ };
 
 bool is_diag_one(const double* e) {
     return e[0] == 1.0 && e[1] == 0.0 && e[2] == 0.0 && e[3] == 0.0 && e[4] == 0.0 && e[5] == 0.0;
@@ -260,6 +267,7 @@ bool is_diag_one(const double* e) {
 
 // ---- the fusion planner ----------------------------------------------------
 thread_local uint64_t g_zero_off = 0;  // factored program being launched: a 0.0 in mats
+thread_local bool g_factored = false;  // the program being launched is a factored rewrite
 struct PlannedPass {
     int first, count;  // range in the program
 };
@@ -290,6 +298,33 @@ int launch_single(qs_state* st, const qs_gate& g, const CutTerms& ct, const doub
 int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const CutTerms& ct,
                 const double* mats_host) {
     if (count > kMaxPassGates) return fail(QS_ERR_VALUE, "planner: pass too long");
+    if (g_factored && st->num_states == 1) {
+        // a pass of CNOTs only is a permutation of the index bits: one gather
+        // per 2^13-amplitude box at copy speed, whatever the number of gates
+        // (factored programs: the exact mode keeps numpy's signed zeros)
+        static const double kX[8] = {0, 0, 1, 0, 1, 0, 0, 0};
+        int cs[kMaxPassGates], ts[kMaxPassGates];
+        bool all_x = true;
+        for (int i = 0; i < count && all_x; ++i) {
+            const qs_gate& g = prog[first + i];
+            all_x = g.kind == QS_KIND_CTRL && g.stride == 0 &&
+                    memcmp(mats_host + g.offset, kX, sizeof(kX)) == 0;
+            cs[i] = g.control;
+            ts[i] = g.target;
+        }
+        if (all_x) {
+            if (g_const_in.on) {  // the permutation reads its input from HBM
+                launch_fill(st->psi, g_const_in.total, g_const_in.v, st->stream);
+                g_const_in.on = false;
+            }
+            LaunchScope ls(st, kLaunchPerm);
+            if (launch_perm(st->psi, st->m, cs, ts, count, st->stream)) {
+                CHECK_LAUNCH();
+                return QS_OK;
+            }
+            ls.cancelled = true;
+        }
+    }
     // tile bits: the targets, plus qubits 0..2 for 128-byte rows, filled upward
     uint64_t need = kLowMask;
     for (int i = 0; i < count; ++i)
@@ -518,7 +553,7 @@ struct PassPlan {
 };
 
 std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool fuse,
-                                  bool lean_first = false) {
+                                  bool lean_first = false, const double* mats = nullptr) {
     std::vector<PassPlan> out;
     const bool tile_ok = fuse && m >= kTileLog2;
     int i = 0;
@@ -530,13 +565,13 @@ std::vector<PassPlan> plan_passes(const qs_gate* gates, int count, int m, bool f
             uint64_t round_set = kind_has_target(gates[i].kind) ? (uint64_t(1) << gates[i].target) : 0;
             int rounds = 1;
             int diags = gates[i].kind == kKindDiagN;
-            bool pass_lean = kind_is_lean(gates[i].kind);
+            int pass_class = lean_first ? gate_class(gates[i], mats) : 2;
             while (j < count && j - i < kMaxPassGates) {
                 const qs_gate& g = gates[j];
                 if (g.kind == kKindDiagN && diags >= kMaxPassDiags) break;
-                // a pass of lean kinds stays on the lean kernels (schedule_program)
-                if (lean_first && pass_lean && !kind_is_lean(g.kind)) break;
-                pass_lean = pass_lean && kind_is_lean(g.kind);
+                // passes of lean kinds stay on the lean kernels, passes of CNOTs
+                // on k_perm (schedule_program's classes)
+                if (lean_first && pass_class < 2 && gate_class(g, mats) != pass_class) break;
                 diags += g.kind == kKindDiagN;
                 uint64_t nn = need, rs = round_set;
                 int nr = rounds;
@@ -935,6 +970,7 @@ int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const 
             if (reorder)
                 schedule_program(fp.gates, st->m, support, all.data(), st->num_states, lean_first);
             g_zero_off = fp.zero_off;
+            g_factored = true;
             gates = fp.gates.data();
             count = int(fp.gates.size());
             mats = all.data();
@@ -943,13 +979,16 @@ int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const 
             lean_first = false;  // the program runs exact: the plain planner
         }
     }
+    struct FactoredScope {  // cleared on every exit
+        ~FactoredScope() { g_factored = false; }
+    } factored_scope;
     t_factor = now();
     if (int rc = grow(&st->d_mats, &st->mats_cap, mats_len ? mats_len : 1)) return rc;
     if (mats_len)
         CUDA_TRY(cudaMemcpyAsync(st->d_mats, mats, mats_len * sizeof(double),
                                  cudaMemcpyHostToDevice, st->stream));
     t_upload = now();
-    std::vector<PassPlan> plan = plan_passes(gates, count, st->m, fuse != 0, lean_first);
+    std::vector<PassPlan> plan = plan_passes(gates, count, st->m, fuse != 0, lean_first, mats);
     int passes = 0;
     if (const_in)
         g_const_in = {true, make_double2(const_in[0], const_in[1]),

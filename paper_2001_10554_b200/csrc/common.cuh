@@ -151,6 +151,17 @@ constexpr int kKindScalar = 19; // per-state scalar (stride 8): psi_s *= (params
 inline bool kind_is_lean(int kind) {
     return kind == kKindShear || kind == kKindDiagN || kind == QS_KIND_CUTPHASE;
 }
+// a CNOT with one matrix for all states (exactly X): k_perm runs passes of these
+inline bool gate_is_cnot(const qs_gate& g, const double* mats) {
+    if (g.kind != QS_KIND_CTRL || g.stride != 0 || !mats) return false;
+    const double* u = mats + g.offset;
+    return u[0] == 0 && u[1] == 0 && u[2] == 1 && u[3] == 0 && u[4] == 1 && u[5] == 0 && u[6] == 0 &&
+           u[7] == 0;
+}
+// pass classes of the lean-first schedule: 0 lean (k_fact*), 1 CNOT (k_perm), 2 other (k_tile)
+inline int gate_class(const qs_gate& g, const double* mats) {
+    return kind_is_lean(g.kind) ? 0 : gate_is_cnot(g, mats) ? 1 : 2;
+}
 inline bool kind_has_target(int kind) {
     return kind != QS_KIND_CUTPHASE && kind != kKindDiagN && kind != kKindScalar;
 }
@@ -202,6 +213,11 @@ bool tile_pass_in_params();  // k_tile takes the pass as a kernel parameter
 // generated a constant input (g_const_in) instead of loading its tiles
 int launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_dev,
                      const double* mats, const CutTerms& ct, cudaStream_t s);
+// A pass of CNOTs only (factored programs, one state): one gather per
+// 2^13-amplitude box (k_perm).  False when the targets do not fit one box;
+// nothing is launched then.
+bool launch_perm(double2* psi, int m, const int* controls, const int* targets, int count,
+                 cudaStream_t s);
 void launch_fill(double2* psi, uint64_t count, double2 value, cudaStream_t s);
 void launch_set_basis(double2* psi, uint64_t stride, uint64_t states, uint64_t off, cudaStream_t s);
 void launch_gaussian(double2* psi, uint64_t count_per_state, int num_states, uint64_t rank_offset,

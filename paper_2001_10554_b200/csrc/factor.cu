@@ -418,10 +418,13 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
                 // batch_flush: the 1q gates of every qubit the run of controlled
                 // gates touches come before its first gate, so that their
                 // pending diagonals can leave as ONE product diagonal
-                for (int j = i; j < count && gates[j].kind == QS_KIND_CTRL; ++j) {
-                    emit_acc(gates[j].target);
-                    emit_acc(gates[j].control);
-                    if (!batch_flush) break;
+                // (and every other accumulated gate: left behind, a qubit the run
+                // does not touch would get a pass of its own after the run)
+                if (batch_flush) {
+                    for (int q = 0; q < m; ++q) emit_acc(q);
+                } else {
+                    emit_acc(g.target);
+                    emit_acc(g.control);
                 }
             } else {  // cut phase: every vertex of the graph
                 for (int q = 0; q < m; ++q)
@@ -453,9 +456,14 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
                         ts.push_back(t);
                     }
                     if (ts.size() >= 4) {
+                        // ... and with them every other pending diagonal and the
+                        // scalar: nothing is left for a D_out behind the run
                         std::vector<cd> z(m, cd(1.0));
-                        for (int t : ts) z[t] = pending[t], pending[t] = 1.0;
-                        out->gates.push_back(diag_tables(z, cd(1.0)));
+                        for (int t = 0; t < m; ++t)
+                            if (psp[t].empty() && mixed[t] && pending[t] != 1.0)
+                                z[t] = pending[t], pending[t] = 1.0;
+                        out->gates.push_back(diag_tables(z, K));
+                        K = 1.0;
                     }
                 }
                 flush(q);
@@ -657,27 +665,28 @@ void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support
     while (!ready.empty()) {
         uint64_t need = low, round_set = 0;
         int rounds = 1, count = 0, diags = 0;
-        bool pass_lean = true;
+        int pass_class = 0;  // max class of the pass's gates (gate_class)
         for (;;) {
             int pick = -1;
             uint64_t pick_need = 0, pick_rs = 0;
             int pick_nr = 0;
-            // lean_first: a pass opens with a lean gate when one is ready, and a
-            // pass of lean gates takes no other kind (config 4: the Haar layer
-            // stays on the lean kernels, the CNOTs get their own k_tile passes)
-            bool lean_ready = false;
+            // lean_first: a pass opens with a lean gate when one is ready (else a
+            // CNOT, else anything), a pass of lean gates takes no other kind and
+            // a pass of CNOTs only CNOTs (config 4: the Haar layer stays on the
+            // lean kernels, the CNOT passes run as permutations on k_perm)
+            int open_class = 2;
             if (lean_first && count == 0)
-                for (int gi : ready) lean_ready |= kind_is_lean(gates[gi].kind);
+                for (int gi : ready) open_class = std::min(open_class, gate_class(gates[gi], mats));
             // preference: no new register round and no new tile bit, then no
             // new tile bit, then program order
             for (int tier = 0; tier < 3 && pick < 0; ++tier) {
                 for (size_t k = 0; k < ready.size(); ++k) {
                     const qs_gate& g = gates[ready[k]];
                     if (lean_first) {
-                        const bool lean = kind_is_lean(g.kind);
-                        if (count == 0 && lean_ready && !lean) continue;
-                        if (count > 0 && pass_lean && !lean) continue;
-                        if (count > 0 && !pass_lean && lean && tier == 2) continue;
+                        const int cls = gate_class(g, mats);
+                        if (count == 0 && cls != open_class) continue;
+                        if (count > 0 && pass_class < 2 && cls != pass_class) continue;
+                        if (count > 0 && pass_class == 2 && cls == 0 && tier == 2) continue;
                     }
                     uint64_t nn = need, rs = round_set;
                     int nr = rounds;
@@ -709,7 +718,7 @@ void schedule_program(std::vector<qs_gate>& gates, int m, uint64_t phase_support
             out.push_back(gates[gi]);
             need = pick_need, round_set = pick_rs, rounds = pick_nr;
             ++count;
-            pass_lean = pass_lean && kind_is_lean(gates[gi].kind);
+            pass_class = std::max(pass_class, gate_class(gates[gi], mats));
             diags += gates[gi].kind == kKindDiagN;
             for (int j : succ[gi])
                 if (--npred[j] == 0) ready.insert(std::lower_bound(ready.begin(), ready.end(), j), j);

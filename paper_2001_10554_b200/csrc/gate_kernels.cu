@@ -2200,6 +2200,274 @@ bool pair_plan(const FactPass& F, const TmaPieces& T, double2* psi, PairPass* X)
     return true;
 }
 
+// ---- permutation pass: CNOT-only passes of a factored program ---------------------
+// A run of CNOTs is a GF(2)-linear permutation of the index bits (bit t ^= bit
+// c per gate); when every target lies in one 2^13-amplitude box (qubits 0..3 =
+// 256-byte rows + 9 more bits) the whole run is ONE gather inside the box,
+// whatever the number of gates: out[i] = in[A i + B x] (i: box element, x: the
+// qubits outside the box, constant per box).  One CTA of 512 threads per SM:
+// TMA load of the 128 KiB box (SWIZZLE_128B), every thread reads its 16 source
+// elements into registers, the next box is requested, then the registers are
+// stored in 256-byte rows (the copy ceiling of these tiles, profiles/
+// r02_bigtile_copy.txt).  Factored programs only: the exact mode keeps numpy's
+// 0 * a + 1 * b (signed zeros).
+constexpr int kPermLog2 = 13;
+constexpr int kPermThreads = 512;
+constexpr int kPermMaxOut = 32;
+struct alignas(64) PermPass {
+    CUtensorMap map;
+    int32_t ncoord;
+    int32_t coord_dim[5], coord_shift[5], coord_lsh[5];
+    uint64_t coord_mask[5];
+    int32_t m, nout;
+    int32_t box_bits[kPermLog2];   // local qubit of each box position (0..3 = qubits 0..3)
+    uint64_t num_boxes;
+    uint16_t col_sig[kPermLog2];   // swizzled smem index of the SOURCE element of output bit p
+    int32_t out_bit[kPermMaxOut];  // qubits outside the box that control a target
+    uint16_t out_sig[kPermMaxOut];
+};
+
+__global__ void __launch_bounds__(kPermThreads, 1)
+    k_perm(double2* __restrict__ psi, const __grid_constant__ PermPass X) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const double2* L = reinterpret_cast<const double2*>(smem_raw);
+    uint64_t* dep = reinterpret_cast<uint64_t*>(smem_raw + (sizeof(double2) << kPermLog2));
+    uint64_t* full = dep + 256 * kDepTables;
+    const int tid = threadIdx.x;
+    // box index -> local offset of the box (its bits deposited into the qubits
+    // outside the box), one byte of the index per table
+    for (int i = tid; i < kDepTables * 256; i += kPermThreads) {
+        const int c = i >> 8, v = i & 255;
+        uint64_t out = 0;
+        for (int b = 0; b < 8; ++b) {
+            if (!((v >> b) & 1)) continue;
+            int want = 8 * c + b, cnt = 0;
+            for (int q = 0, k = 0; q < X.m; ++q) {
+                if (k < kPermLog2 && X.box_bits[k] == q) {
+                    ++k;
+                    continue;
+                }
+                if (cnt++ == want) {
+                    out |= uint64_t(1) << q;
+                    break;
+                }
+            }
+        }
+        dep[i] = out;
+    }
+    if (tid == 0) {
+        mbar_init(full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto load = [&](uint64_t box) {
+        int c[5] = {0, 0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+            if (i < X.ncoord)
+                c[X.coord_dim[i]] += int(((box >> X.coord_shift[i]) & X.coord_mask[i]) << X.coord_lsh[i]);
+        const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(full));
+        const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_raw));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                     "r"(unsigned(sizeof(double2)) << kPermLog2)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(d), "l"(&X.map), "r"(c[0]), "r"(c[1]),
+            "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(b)
+            : "memory");
+    };
+    if (tid == 0 && blockIdx.x < X.num_boxes) load(blockIdx.x);
+    // element e = tid + 512 k: positions 0..8 from the thread, 9..12 from k
+    int thr_sig = 0;
+    uint64_t thr_off = 0;
+#pragma unroll
+    for (int p = 0; p < 9; ++p)
+        if ((tid >> p) & 1) {
+            thr_sig ^= X.col_sig[p];
+            thr_off |= uint64_t(1) << X.box_bits[p];
+        }
+    int ksig[4];
+    uint64_t koff[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        ksig[j] = X.col_sig[9 + j];
+        koff[j] = uint64_t(1) << X.box_bits[9 + j];
+    }
+    unsigned parity = 0;
+    for (uint64_t box = blockIdx.x; box < X.num_boxes; box += gridDim.x, parity ^= 1) {
+        uint64_t base = 0;
+#pragma unroll
+        for (int c = 0; c < kDepTables; ++c) base |= dep[(c << 8) | ((box >> (8 * c)) & 255)];
+        int sig = thr_sig;
+        for (int j = 0; j < X.nout; ++j)
+            if ((base >> X.out_bit[j]) & 1) sig ^= X.out_sig[j];
+        mbar_wait(full, parity);
+        double2 a[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            int v = sig;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if ((k >> j) & 1) v ^= ksig[j];
+            a[k] = L[v];
+        }
+        __syncthreads();  // every thread holds its elements: the box buffer is free
+        const uint64_t next = box + gridDim.x;
+        if (tid == 0 && next < X.num_boxes) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            load(next);
+        }
+        double2* gb = psi + (base | thr_off);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            uint64_t o = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if ((k >> j) & 1) o |= koff[j];
+            gb[o] = a[k];
+        }
+    }
+}
+
+// Host plan of a permutation pass: gates = (control, target) pairs in program
+// order, all local, single state.  False when the targets do not fit one box
+// or the tensor map cannot be built (the caller falls back to k_tile).
+bool launch_perm_pass(double2* psi, int m, const int* controls, const int* targets, int count,
+                      cudaStream_t s) {
+    static const bool off = getenv("QSB_NO_PERM") != nullptr;
+    if (off || m < kPermLog2 + 1 || count < 1 || !encode_fn()) return false;
+    uint64_t boxset = 0xF;  // qubits 0..3: 256-byte rows
+    for (int i = 0; i < count; ++i) {
+        if (targets[i] < 0 || targets[i] >= m || controls[i] < 0 || controls[i] >= m) return false;
+        boxset |= uint64_t(1) << targets[i];
+    }
+    if (__builtin_popcountll(boxset) > kPermLog2) return false;
+    for (int q = 4; q < m && __builtin_popcountll(boxset) < kPermLog2; ++q) boxset |= uint64_t(1) << q;
+    if (__builtin_popcountll(boxset) != kPermLog2) return false;
+    static thread_local PermPass X;
+    memset(&X, 0, sizeof(X));
+    X.m = m;
+    X.num_boxes = uint64_t(1) << (m - kPermLog2);
+    // dims: d0 = qubits 0..2 (16 doubles), then the runs of box bits from qubit 3
+    // up, each at most 8 bits (box dims are limited to 256 elements)
+    struct D { int lo, len; };
+    std::vector<D> dims;
+    for (int q = 3; q < m;) {
+        if (!((boxset >> q) & 1)) { ++q; continue; }
+        int e = q;
+        while (e + 1 < m && ((boxset >> (e + 1)) & 1) && e + 1 - q < 8) ++e;
+        dims.push_back({q, e - q + 1});
+        q = e + 1;
+    }
+    if (1 + dims.size() > 5) return false;
+    cuuint64_t gdim[5], gstride[4];
+    cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+    uint64_t ext[5];
+    ext[0] = 16;
+    box[0] = 16;
+    for (size_t i = 0; i < dims.size(); ++i) {
+        ext[i + 1] = uint64_t(1) << dims[i].len;
+        gstride[i] = uint64_t(sizeof(double2)) << dims[i].lo;
+        box[i + 1] = 1u << dims[i].len;
+    }
+    // runs of qubits outside the box ride on the dim just below them; their
+    // field of the box index is the coordinate
+    int below = 0;
+    for (int q = 4; q < m;) {
+        if ((boxset >> q) & 1) { ++q; continue; }
+        int e = q;
+        while (e + 1 < m && !((boxset >> (e + 1)) & 1)) ++e;
+        const int len = e - q + 1;
+        int host = -1;
+        for (size_t i = 0; i < dims.size(); ++i)
+            if (dims[i].lo + dims[i].len == q) host = int(i) + 1;
+        if (host < 0 || X.ncoord >= 5) return false;
+        ext[host] <<= len;
+        const int k = X.ncoord++;
+        X.coord_dim[k] = host;
+        X.coord_shift[k] = below;
+        X.coord_lsh[k] = dims[host - 1].len;
+        X.coord_mask[k] = (uint64_t(1) << len) - 1;
+        below += len;
+        q = e + 1;
+    }
+    const int rank = int(dims.size()) + 1;
+    for (int i = 0; i < rank; ++i) {
+        if (ext[i] > (uint64_t(1) << 31)) return false;
+        gdim[i] = ext[i];
+    }
+    for (int i = rank; i < 5; ++i) {  // 5-d map: unit dims on top
+        gdim[i] = 1;
+        gstride[i - 1] = gstride[i - 2] * 2;
+        box[i] = 1;
+    }
+    if (encode_fn()(&X.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, psi, gdim, gstride, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, l2_promotion(),
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    // box positions in memory order: qubits 0..2, then the dims
+    int pos_of_qubit[64];
+    for (int q = 0; q < 64; ++q) pos_of_qubit[q] = -1;
+    int np = 0;
+    for (int q = 0; q < 3; ++q) X.box_bits[np] = q, pos_of_qubit[q] = np++;
+    for (const D& d : dims)
+        for (int q = d.lo; q < d.lo + d.len; ++q) X.box_bits[np] = q, pos_of_qubit[q] = np++;
+    if (np != kPermLog2) return false;
+    // the kernel deposits positions in qubit order (box_bits ascending): the dims
+    // are in ascending qubit order, so positions and qubits agree
+    // source index bits: out[i] = in[f_1(f_2(..f_k(i)))], f_j: bit t_j ^= bit c_j
+    uint64_t row[64];
+    for (int q = 0; q < m; ++q) row[q] = uint64_t(1) << q;
+    for (int j = count - 1; j >= 0; --j) row[targets[j]] ^= row[controls[j]];
+    auto sigma = [](int v) { return v ^ ((v >> 3) & 7); };
+    auto column = [&](int q) {  // source box positions whose bit depends on output qubit q
+        int v = 0;
+        for (int b = 0; b < m; ++b)
+            if ((row[b] >> q) & 1) {
+                if (pos_of_qubit[b] < 0) return -1;  // cannot happen: only targets change
+                v |= 1 << pos_of_qubit[b];
+            }
+        return v;
+    };
+    for (int p = 0; p < kPermLog2; ++p) {
+        const int v = column(X.box_bits[p]);
+        if (v < 0) return false;
+        X.col_sig[p] = uint16_t(sigma(v));
+    }
+    for (int q = 0; q < m; ++q) {
+        if (pos_of_qubit[q] >= 0) continue;
+        int v = 0;
+        for (int b = 0; b < m; ++b)
+            if (b != q && ((row[b] >> q) & 1)) {
+                if (pos_of_qubit[b] < 0) return false;
+                v |= 1 << pos_of_qubit[b];
+            }
+        if (!v) continue;
+        if (X.nout >= kPermMaxOut) return false;
+        X.out_bit[X.nout] = q;
+        X.out_sig[X.nout++] = uint16_t(sigma(v));
+    }
+    constexpr int kMaxDevices = 64;
+    static std::atomic<int> configured[kMaxDevices];
+    static int sms_of[kMaxDevices];
+    const size_t smem = (sizeof(double2) << kPermLog2) + sizeof(uint64_t) * (256 * kDepTables + 1);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (configured[dev].load(std::memory_order_acquire) == 0) {
+        cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        sms_of[dev] = sms;
+        configured[dev].store(1, std::memory_order_release);
+    }
+    uint64_t grid = uint64_t(sms_of[dev]);
+    if (grid > X.num_boxes) grid = X.num_boxes;
+    k_perm<<<unsigned(grid), kPermThreads, smem, s>>>(psi, X);
+    return true;
+}
+
 template <bool PO, bool DG>
 void launch_fact_pair_variant(double2* psi, const FactPass& F, const double* mats,
                               const CutTerms& ct, const TmaPass& T, const PairPass& X,
@@ -2466,6 +2734,11 @@ int launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_de
 }
 
 thread_local ConstIn g_const_in = {false, {0.0, 0.0}, 0};
+
+bool launch_perm(double2* psi, int m, const int* controls, const int* targets, int count,
+                 cudaStream_t s) {
+    return launch_perm_pass(psi, m, controls, targets, count, s);
+}
 
 int prof_read(unsigned long long* out) {
 #ifdef QSB_PROF

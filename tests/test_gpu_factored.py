@@ -510,3 +510,45 @@ def test_factored_lean_first_schedule(monkeypatch):
         got2, passes_mixed = run_queue(n, prog, edges, psi0, FACT)
         assert max_dev(got2, expect) <= TOL
         assert passes_lean >= passes_mixed
+
+
+@pytest.mark.parametrize("n", [14, 16, 19])
+def test_factored_cnot_passes_run_as_permutations(n, monkeypatch):
+    """A pass of CNOTs only in a factored program is one gather per
+    2^13-amplitude box (k_perm, launch kind 9): chains, repeated targets,
+    targets among qubits 0..3, controls inside and outside the box, several
+    layers -- against the oracle."""
+    monkeypatch.setenv("QSB_LEAN_FIRST_M", "12")
+    rng = np.random.default_rng(900 + n)
+    prog = []
+    for layer in range(3):
+        prog += [{"kind": "custom", "qubits": (q,), "matrix": ogates.random_unitary_2x2(rng)}
+                 for q in range(n)]
+        if layer == 0:    # config 4's pairs
+            pairs = [(q, n - 1 - q) for q in range(n // 2)]
+        elif layer == 1:  # a chain through low and high qubits, a repeated target
+            pairs = [(0, 5), (5, n - 1), (n - 1, 2), (2, n - 2), (7, n - 2), (n - 3, 1), (1, 9)]
+        else:
+            pairs = []
+            while len(pairs) < 12:
+                c, t = (int(x) for x in rng.integers(0, n, size=2))
+                if c != t:
+                    pairs.append((c, t))
+        prog += [{"kind": "cu", "qubits": p, "matrix": X} for p in pairs]
+    psi0 = ogates.random_state(n, rng)
+    expect = ocirc.run(n, prog, psi0)
+    st = N.DeviceState(n, n)
+    st.upload(psi0)
+    st.launch_log(True)
+    q = runtime.GateQueue(st, fuse=FACT)
+    for g in prog:
+        if g["kind"] == "custom":
+            q.one_qubit(g["qubits"][0], g["matrix"])
+        else:
+            q.controlled(*g["qubits"], g["matrix"])
+    q.flush()
+    got = st.download()
+    st.launch_log(False)
+    _, kinds = st.read_launch_log()
+    assert 9 in set(int(k) for k in kinds), kinds
+    assert max_dev(got, expect) <= TOL
