@@ -306,12 +306,17 @@ def test_factored_pool_per_state_gates():
 
 @pytest.mark.parametrize("P", [2, 4])
 @pytest.mark.parametrize("remap", [False, True])
-def test_factored_config4_distributed(P, remap):
+@pytest.mark.parametrize("large", [False, True])
+def test_factored_config4_distributed(P, remap, large, monkeypatch):
     """Config 4 recipe at n=14 over 2/4 emulated ranks (m = 13/12, so the local
     programs are factored): local shears, global-qubit exchanges (or qubit
-    remapping) and case-(c) CNOTs, against the oracle's full state."""
+    remapping) and case-(c) CNOTs, against the oracle's full state.  `large`:
+    the schedule of large states (lean-first passes, batched diagonal flush,
+    CNOT passes on k_perm) forced at n=16 (m = 15/14)."""
     from paper_2001_10554_b200.circuit import GateSpec
-    n = 14
+    n = 16 if large else 14
+    if large:
+        monkeypatch.setenv("QSB_LEAN_FIRST_M", "12")
     rng = np.random.default_rng(40 + P)
     psi0 = ogates.random_state(n, rng)
     seq, prog = [], []
