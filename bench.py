@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--no-config4-point", action="store_true",
                     help="N=1 sweep: skip the config-4 n=33 point of the weak-scaling curve")
     ap.add_argument("--seed", type=int, default=20260809)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--pool-chunks", type=int, default=1,
                     help="qaoa: the GPU's share of the pool as this many batched sub-pools, so "
                          "the host builds chunk k+1's program while chunk k runs (each chunk "
@@ -631,7 +631,7 @@ def run_ours(args):
         exact_cmp = {"value": units_per_step / (ms_exact / 1e3), "ms_per_step": ms_exact,
                      "numerics": "exact (QS_FUSE_EXACT: bit-identical to the reference's numpy "
                                  "arithmetic)"}
-        if world == 1 and not cx_pairs:
+        if world == 1:
             numerics_error = factored_vs_exact(args, ctx, sweeps, step, n)
     config4_point = None
     if args.workload == "sweep" and world == 1 and not args.no_config4_point:

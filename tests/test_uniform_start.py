@@ -203,3 +203,24 @@ def test_program_on_constant_equals_fill_then_program():
     N.call("qs_apply_program_on_constant", b.handle, c[0], c[1], arr, 0, N.dptr(mats), mats.size,
            N.iptr(e), 0, N.FUSE_EXACT)
     assert np.array_equal(b.download(), np.full(1 << n, complex(*c)))
+
+
+@pytest.mark.gpu
+def test_register_api_hadamard_layer_is_folded():
+    """The paper-style register: Initialize("base", 0) +
+    ApplyHadamard on every qubit runs from the uniform state; the amplitudes are
+    the reference's product chain bit for bit, and a later gate sees them."""
+    from paper_2001_10554_b200.register import QubitRegister
+
+    n = 13
+    reg = QubitRegister(n, "base", 0)
+    for q in range(n):
+        reg.ApplyHadamard(q)
+    reg.ApplyPauliZ(0)
+    reg.queue.flush()
+    assert reg.state.uniform_folds == 1
+    got = reg.state.download()
+    v = N.hadamard_chain(n)
+    want = np.full(1 << n, v + 0j)
+    want[1::2] = -v
+    assert np.array_equal(got.real, want.real) and not got.imag.any()

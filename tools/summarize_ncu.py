@@ -36,7 +36,7 @@ STALLS = "smsp__pcsamp_warps_issue_stalled_"
 
 
 def short(name):
-    for k in ("k_tile", "k_fact", "k_gate1q", "k_controlled", "k_cut_phase", "k_tree_wide", "k_tree",
+    for k in ("k_perm", "k_tile", "k_fact", "k_gate1q", "k_controlled", "k_cut_phase", "k_tree_wide", "k_tree",
               "k_marginals", "k_exchange_peer", "k_swap_peer", "k_swap_local", "k_fill",
               "k_gaussian", "k_scale", "k_pair_halves"):
         if k in name:
