@@ -1244,6 +1244,12 @@ def run_noise(args, dist, comm, world, rank, local):
     ctx = runtime.make_context(None, n, num_states=count, device=local, fuse=fuse_mode(args),
                                seed=args.seed, noise_model=model)
     ctx.norm_check_interval = 0
+    # a second pool of the same shape: round k+1's program is built and enqueued
+    # while round k runs (runtime.run_noise_ensemble(shadow=...) does the same)
+    shadow = runtime.make_context(None, n, num_states=count, device=local, fuse=fuse_mode(args),
+                                  seed=args.seed, noise_model=model)
+    shadow.norm_check_interval = 0
+    ctxs = [ctx, shadow]
     st = ctx.state
     edges = np.asarray(graph.edges, dtype=np.int32)
     durations = [g.duration for g in circ.gates if g.kind == "noise"]
@@ -1260,30 +1266,53 @@ def run_noise(args, dist, comm, world, rank, local):
     round_no = [0]
     pending = [pool.submit(draw, 0)]
 
+    behind = [None]  # the context whose round is still on the device
+
+    def drain():
+        c, behind[0] = behind[0], None
+        return c.pool.observable(3, 0, edges) if c is not None else None
+
     def step():
-        # the next round's host draws overlap this round's device work
+        # the next round's host draws (worker thread) and this round's program
+        # build overlap the previous round's device work; its <C> values are
+        # read back once this round is enqueued
         k = round_no[0]
         round_no[0] += 1
+        c = ctxs[k % 2]
         mats = pending[0].result()
-        runtime.reset_state(ctx)
-        runtime.run_circuit(ctx, circ, noise_matrices=mats)
+        if behind[0] is not None:  # no interleaving of the two pools' kernels
+            c.state.wait_event(behind[0].state.sync_event(0))
+        runtime.reset_state(c)
+        runtime.run_circuit(c, circ, noise_matrices=mats)
+        c.state.record_sync_event(0)
         pending[0] = pool.submit(draw, k + 1)
-        return ctx.pool.observable(3, 0, edges)
+        vals = drain()
+        behind[0] = c
+        return vals
 
     for _ in range(args.warmup):
         step()
-    st.synchronize()
+    drain()  # the timed region starts with an empty pipeline ...
+    for c in ctxs:
+        c.state.synchronize()
     barrier(dist)
     clocks = ClockSampler(local)
     clocks.start()
-    st.launch_log(True)
+    for c in ctxs:
+        c.state.launch_log(True)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        values = step()
-    st.synchronize()
+        step()
+    values = drain()  # ... and ends with the last round's values on the host
+    for c in ctxs:
+        c.state.synchronize()
     wall = time.perf_counter() - t0
-    st.launch_log(False)
-    launch_ms, launch_kind = st.read_launch_log()
+    logs = []
+    for c in ctxs:
+        c.state.launch_log(False)
+        logs.append(c.state.read_launch_log())
+    launch_ms = np.concatenate([l[0] for l in logs])
+    launch_kind = np.concatenate([l[1] for l in logs])
     clock = clocks.stop()
     wall = max_over_ranks(dist, wall)
     gates_per_circuit = len(circ.gates)

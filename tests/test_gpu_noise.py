@@ -74,6 +74,15 @@ def test_ensemble_is_layout_independent():
     ref3, v3 = runtime.run_noise_ensemble(pool, circ, model, T, z0)
     assert ref1 == ref3
     assert np.array_equal(v1, v3)
+    # two pools in turns (round k's values read back after round k+1 is enqueued):
+    # the same values, for pool sizes that do and do not divide the ensemble
+    for S in (3, 2):
+        a = runtime.make_context(None, 12, S, seed=seed)
+        b = runtime.make_context(None, 12, S, seed=seed)
+        refp, vp = runtime.run_noise_ensemble(a, circ, model, T, z0, shadow=b)
+        assert refp == ref1 and np.array_equal(vp, v1)
+    with pytest.raises(ValueError):
+        runtime.run_noise_ensemble(single, circ, model, T, z0, shadow=pool)
     # against the oracle's scalar path for two trajectories
     sched = N.schedule_noise(circ)
     glist_s = [{"kind": g.kind, "qubits": g.qubits, "param": g.param, "duration": g.duration}
