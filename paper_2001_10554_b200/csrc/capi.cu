@@ -963,7 +963,12 @@ int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const 
         factor_program(gates, count, mats, mats_len, st->m, st->num_states, num_edges, support, &fp,
                        lean_first);
         t_fp = now();
-        if (2 * fp.factored >= count) {
+        // CNOTs count as factored: their passes run as permutations (k_perm), so a
+        // program of CNOTs between two exchanges does not fall back to k_tile
+        int cnots = 0;
+        if (st->num_states == 1 && st->m > 13)
+            for (int i = 0; i < count; ++i) cnots += gate_is_cnot(gates[i], mats);
+        if (2 * (fp.factored + cnots) >= count) {
             all.assign(mats, mats + mats_len);
             all.insert(all.end(), fp.extra.begin(), fp.extra.end());
             static const bool reorder = getenv("QSB_NO_REORDER") == nullptr;

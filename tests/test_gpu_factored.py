@@ -557,3 +557,27 @@ def test_factored_cnot_passes_run_as_permutations(n, monkeypatch):
     _, kinds = st.read_launch_log()
     assert 9 in set(int(k) for k in kinds), kinds
     assert max_dev(got, expect) <= TOL
+
+
+def test_factored_cnot_only_program_is_a_permutation():
+    """A program of CNOTs alone (the local CNOTs of a distributed layer between
+    two exchanges) counts as factored and runs on k_perm: bit-identical to the
+    oracle on a state without zeros (a permutation moves the bits unchanged)."""
+    n = 15
+    rng = np.random.default_rng(77)
+    psi0 = ogates.random_state(n, rng)
+    pairs = [(q, n - 1 - q) for q in range(n // 2)] + [(3, 1), (n - 1, 0), (6, 2)]
+    prog = [{"kind": "cu", "qubits": p, "matrix": X} for p in pairs]
+    expect = ocirc.run(n, prog, psi0)
+    st = N.DeviceState(n, n)
+    st.upload(psi0)
+    st.launch_log(True)
+    q = runtime.GateQueue(st, fuse=FACT)
+    for g in prog:
+        q.controlled(*g["qubits"], g["matrix"])
+    q.flush()
+    got = st.download()
+    st.launch_log(False)
+    _, kinds = st.read_launch_log()
+    assert set(int(k) for k in kinds) == {9}, kinds
+    assert bits_equal(got, expect)
