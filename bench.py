@@ -601,13 +601,19 @@ def run_ours(args):
     # numpy-exact pair update: 20 FP64 ops per pair (a CX touches half the pairs);
     # factored: a 4-FMA shear per pair (2 per amplitude; lean passes pad every
     # register round to 4 shears) plus two product diagonals (~13 per amplitude)
-    factored = fuse_mode(args) == "factored" and not cfg3
-    if factored:
+    factored = fuse_mode(args) == "factored"
+    if factored and cfg3:
+        # the three controlled gates of a pair fuse into one controlled matrix
+        fp64_per_amp = 5.0 * 64
+        fp64_note = ("factored: CNOT, CPhase and controlled-Haar of a pair fused into one "
+                     "controlled gate; 10 FP64 instructions per amplitude of the control=1 half")
+    elif factored:
+        # CNOT passes are permutations (k_perm): no arithmetic
         fp64_per_amp = (2.0 * 4 * sum(-(-r // 4) for r in (12, 9, 9)) if n == 30 else 2.0 * n) \
-            + 26.0 + 10.0 * 0.5 * len(cx_pairs)
+            + 26.0
         fp64_note = ("factored: 2 FP64 instructions per amplitude per shear (register rounds "
                      "padded to 4 shears), two product diagonals ~13 each; the pass is not "
-                     "FP64-bound")
+                     "FP64-bound; CNOT passes are permutations")
     else:
         fp64_per_amp = (5.0 + 1.0 + 5.0) * 64 if cfg3 else 10.0 * (n + 0.5 * len(cx_pairs))
         fp64_note = ("10 FP64 instructions per amplitude per gate (numpy-exact complex "
@@ -655,7 +661,10 @@ def run_ours(args):
                             f"2^{m} c128 amplitudes per GPU (n={n}, {p} global qubits)",
                 "qubits": n, "local_qubits": m, "gates_per_step": gates_per_step,
                 "fused": not args.no_fuse,
-                "numerics": ("factored (QS_FUSE_FACTORED: Euler-factored 1q gates as 4-FMA "
+                "numerics": ("factored (QS_FUSE_FACTORED: the controlled gates of a pair fused "
+                             "into one controlled matrix; within 1e-12 of the reference, "
+                             "tests/test_gpu_factored.py)" if factored and cfg3 else
+                             "factored (QS_FUSE_FACTORED: Euler-factored 1q gates as 4-FMA "
                              "shears + merged diagonals; within 1e-12 of the reference, "
                              "tests/test_gpu_factored.py, tests/test_gpu_headline.py)"
                              if factored else

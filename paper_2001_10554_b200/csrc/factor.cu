@@ -362,11 +362,25 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             std::vector<cd> m;            // 4 entries per state (1 state when shared)
         };
         std::vector<Acc> acc(m);
+        // last gate of `prog` that touches each qubit: consecutive controlled
+        // gates on one (control, target) pair fuse like 1q gates do
+        std::vector<int> last_touch(m, -1);
+        auto touch = [&](const qs_gate& g) {
+            const int at = int(prog.size());
+            if (g.kind == QS_KIND_CUTPHASE) {
+                for (int q = 0; q < m; ++q)
+                    if ((phase_support >> q) & 1) last_touch[q] = at;
+                return;
+            }
+            last_touch[g.target] = at;
+            if (g.kind == QS_KIND_CTRL) last_touch[g.control] = at;
+        };
         auto load = [&](const qs_gate& g, std::vector<cd>& dst) {
             const int ns = g.stride ? num_states : 1;
             dst.resize(4 * size_t(ns));
             for (int st = 0; st < ns; ++st) {
-                const double* u = mats + g.offset + uint64_t(st) * g.stride;
+                const uint64_t off = g.offset + uint64_t(st) * g.stride;
+                const double* u = off >= mats_len ? out->extra.data() + (off - mats_len) : mats + off;
                 for (int e = 0; e < 4; ++e) dst[4 * st + e] = cd(u[2 * e], u[2 * e + 1]);
             }
         };
@@ -374,6 +388,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
             Acc& a = acc[q];
             if (a.n == 0) return;
             if (a.n == 1) {
+                touch(a.g);
                 prog.push_back(a.g);
             } else {
                 const int ns = int(a.m.size() / 4);
@@ -382,6 +397,7 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
                 g.offset = mats_len + out->extra.size();
                 g.stride = ns > 1 ? 8 : 0;
                 for (const cd& x : a.m) out->extra.push_back(x.real()), out->extra.push_back(x.imag());
+                touch(g);
                 prog.push_back(g);
                 out->factored += a.n - 1;  // the merged-away gates cost nothing
             }
@@ -426,10 +442,36 @@ void factor_program(const qs_gate* gates, int count, const double* mats, uint64_
                     emit_acc(g.target);
                     emit_acc(g.control);
                 }
+                // the previous gate on both qubits is a controlled gate on the same
+                // pair: one controlled gate with the product matrix (config 3's
+                // CNOT, CPhase, controlled-U on a pair become one gate)
+                const int li = last_touch[g.control];
+                if (li >= 0 && li == last_touch[g.target] && prog[li].kind == QS_KIND_CTRL &&
+                    prog[li].control == g.control && prog[li].target == g.target) {
+                    std::vector<cd> y, x;
+                    load(prog[li], y);  // earlier gate
+                    load(g, x);         // later gate
+                    const int n1 = int(y.size() / 4), n2 = int(x.size() / 4);
+                    const int ns = std::max(n1, n2);
+                    while (out->extra.size() % 2) out->extra.push_back(0.0);
+                    const uint64_t off = mats_len + out->extra.size();
+                    for (int st = 0; st < ns; ++st) {
+                        const cd* b = x.data() + 4 * (n2 > 1 ? st : 0);
+                        const cd* a = y.data() + 4 * (n1 > 1 ? st : 0);
+                        const cd r[4] = {b[0] * a[0] + b[1] * a[2], b[0] * a[1] + b[1] * a[3],
+                                         b[2] * a[0] + b[3] * a[2], b[2] * a[1] + b[3] * a[3]};
+                        for (const cd& v : r) out->extra.push_back(v.real()), out->extra.push_back(v.imag());
+                    }
+                    prog[li].offset = off;
+                    prog[li].stride = ns > 1 ? 8 : 0;
+                    out->factored++;  // the merged-away gate costs nothing
+                    continue;
+                }
             } else {  // cut phase: every vertex of the graph
                 for (int q = 0; q < m; ++q)
                     if ((phase_support >> q) & 1) emit_acc(q);
             }
+            touch(g);
             prog.push_back(g);
         }
         for (int q = 0; q < m; ++q) emit_acc(q);

@@ -581,3 +581,54 @@ def test_factored_cnot_only_program_is_a_permutation():
     _, kinds = st.read_launch_log()
     assert set(int(k) for k in kinds) == {9}, kinds
     assert bits_equal(got, expect)
+
+
+@pytest.mark.parametrize("n", [13, 16])
+def test_factored_controlled_gates_on_one_pair_fuse(n):
+    """Consecutive controlled gates on one (control, target) pair -- config 3's
+    CNOT, CPhase(phi), controlled-Haar per pair -- become one controlled gate
+    with the product matrix in the factored mode; triples, interrupted triples
+    (a gate on the control or the target in between), reversed pairs and
+    per-state matrices in a pool, against the oracle."""
+    from oracle import statevector as osv
+    rng = np.random.default_rng(3100 + n)
+    prog = []
+    for k in range(40):
+        c, t = (int(x) for x in rng.choice(n, 2, replace=False))
+        phi = float(rng.uniform(0, 2 * np.pi))
+        cp = np.diag([1.0, np.exp(1j * phi)]).astype(np.complex128)
+        triple = [X, cp, ogates.random_unitary_2x2(rng)]
+        for j, u in enumerate(triple):
+            prog.append({"kind": "cu", "qubits": (c, t), "matrix": u})
+            r = rng.random()
+            if j < 2 and r < 0.15:    # a 1q gate on the target breaks the run
+                prog.append({"kind": "custom", "qubits": (t,), "matrix": ogates.random_unitary_2x2(rng)})
+            elif j < 2 and r < 0.3:   # ... or one on the control
+                prog.append({"kind": "custom", "qubits": (c,), "matrix": ogates.rz(0.3 + k)})
+            elif j < 2 and r < 0.4:   # ... or the reversed pair
+                prog.append({"kind": "cu", "qubits": (t, c), "matrix": X})
+        if k % 5 == 0:
+            prog.append({"kind": "custom", "qubits": (int(rng.integers(n)),), "matrix": H})
+    psi0 = ogates.random_state(n, rng)
+    expect = ocirc.run(n, prog, psi0)
+    got, passes = run_queue(n, prog, [(0, 1)], psi0, FACT)
+    assert max_dev(got, expect) <= TOL
+    # a pool with per-state controlled matrices in the middle of a triple
+    S = 3
+    states = np.stack([ogates.random_state(n, rng) for _ in range(S)])
+    pool = runtime.PoolState(n, S, fuse=FACT)
+    pool.state.upload(states)
+    expected = states.copy()
+    for k in range(12):
+        c, t = (int(x) for x in rng.choice(n, 2, replace=False))
+        us = [X, np.stack([ogates.random_unitary_2x2(rng) for _ in range(S)]),
+              np.diag([1.0, np.exp(1j * (0.7 + k))]).astype(np.complex128)]
+        for u in us:
+            pool.queue.controlled(c, t, u)
+            for s in range(S):
+                osv.apply_controlled(expected[s], c, t, u[s] if u.ndim == 3 else u)
+        q = int(rng.integers(n))
+        pool.queue.one_qubit(q, H)
+        for s in range(S):
+            osv.apply_1q(expected[s], q, H)
+    assert max_dev(pool.amplitudes(), expected) <= TOL
