@@ -998,9 +998,30 @@ int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const 
     if (const_in)
         g_const_in = {true, make_double2(const_in[0], const_in[1]),
                       st->amps_per_state * uint64_t(st->num_states)};
-    for (const PassPlan& pp : plan) {
+    for (size_t pi = 0; pi < plan.size(); ++pi) {
+        const PassPlan& pp = plan[pi];
         // the internal kinds of a factored program only exist as tile-pass gates
         const bool single = pp.count == 1 && gates[pp.first].kind <= QS_KIND_CUTPHASE;
+        // a CNOT pass right behind a lean pass: offered to the lean launcher,
+        // which folds it into its copy-out when the tile holds every target
+        g_absorb.count = 0;
+        g_absorb.done = false;
+        if (g_factored && !single && pi + 1 < plan.size() && st->num_states == 1 &&
+            gate_class(gates[pp.first], mats) == 0) {
+            const PassPlan& nx = plan[pi + 1];
+            bool all_cnot = nx.count <= kMaxPassGates;
+            for (int i = 0; i < nx.count && all_cnot; ++i)
+                all_cnot = gate_is_cnot(gates[nx.first + i], mats);
+            for (int i = 0; i < pp.count && all_cnot; ++i)
+                all_cnot = kind_is_lean(gates[pp.first + i].kind);
+            if (all_cnot) {
+                g_absorb.count = nx.count;
+                for (int i = 0; i < nx.count; ++i) {
+                    g_absorb.controls[i] = gates[nx.first + i].control;
+                    g_absorb.targets[i] = gates[nx.first + i].target;
+                }
+            }
+        }
         if (single && g_const_in.on) {  // the streaming kernels read their input from HBM
             launch_fill(st->psi, g_const_in.total, g_const_in.v, st->stream);
             g_const_in.on = false;
@@ -1009,9 +1030,13 @@ int apply_program_impl(qs_state* st, const qs_gate* gates, int32_t count, const 
                         : launch_tile(st, gates, pp.first, pp.count, ct, mats);
         if (rc) {
             g_const_in.on = false;
+            g_absorb.count = 0;
             return rc;
         }
         ++passes;
+        if (g_absorb.done) ++pi;  // the CNOT pass ran inside this one
+        g_absorb.count = 0;
+        g_absorb.done = false;
     }
     st->last_passes = passes;
     if (dbg_time) {

@@ -208,6 +208,17 @@ struct ConstIn {
     uint64_t total;
 };
 extern thread_local ConstIn g_const_in;
+// A pass of CNOTs right behind a lean pass whose tile holds all its targets:
+// the lean pass writes its tile back through shared memory and reads the copy-out
+// through the composed permutation (GF(2)-linear smem addressing: no cost per
+// amplitude), so the CNOT pass is never launched.  Set by the program loop
+// (count > 0), `done` by the lean launcher that took it.
+struct AbsorbCnots {
+    int count;
+    int controls[kMaxPassGates], targets[kMaxPassGates];
+    bool done;
+};
+extern thread_local AbsorbCnots g_absorb;
 bool tile_pass_in_params();  // k_tile takes the pass as a kernel parameter
 // returns 0: k_tile, 1: the lean factored kernels (k_fact*), 2: a lean pass that
 // generated a constant input (g_const_in) instead of loading its tiles

@@ -1268,6 +1268,7 @@ void launch_fact(double2* psi, const FactPass& F, const double* mats, const CutT
 // order so that every register round's quarter-warp lanes hit 8 distinct bank
 // groups, and rewrites the rounds' swizzled deposit tables for that layout,
 // so the round bodies are k_fact's.
+constexpr int kMaxAbsorbCtl = 16;
 struct alignas(64) TmaPass {
     CUtensorMap map;             // 128 bytes, 64-byte aligned
     int32_t rank;                // tensor dims (2..5)
@@ -1279,6 +1280,11 @@ struct alignas(64) TmaPass {
     uint64_t coord_mask[5];      // ~0 for the top field
     int32_t sig[kTileLog2];      // smem index of each tile-position basis vector
     int32_t prefetch;            // L2 prefetch distance in tiles of this CTA
+    // absorbed CNOTs (AbsorbCnots): `sig` then holds the permuted copy-out
+    // columns; controls outside the tile flip these smem bits per tile
+    int32_t nctl;
+    int32_t ctl_bit[kMaxAbsorbCtl];
+    int32_t ctl_sig[kMaxAbsorbCtl];
 };
 // host only: the tile pieces above qubits 0..2 in the map's dim order (the
 // pair plan rebuilds a 13-bit map from them)
@@ -1541,7 +1547,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
         if (!direct) {
             double2* gb = gbase + goff(tid);
-            const int s_tid = sig_of(tid);
+            int s_tid = sig_of(tid);
+            for (int j = 0; j < T.nctl; ++j)  // absorbed CNOTs controlled from outside the tile
+                if ((base_local >> T.ctl_bit[j]) & 1) s_tid ^= T.ctl_sig[j];
 #pragma unroll
             for (int i = 0; i < kLoadsPerThread; ++i)
                 gb[goff(i * kTileThreads)] = W[s_tid ^ sig_of(i * kTileThreads)];
@@ -2070,7 +2078,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
         if (!direct) {
             double2* gb = gbase + goff(tid);
-            const int s_tid = sig_of(tid);
+            int s_tid = sig_of(tid);
+            for (int j = 0; j < T.nctl; ++j)  // absorbed CNOTs controlled from outside the tile
+                if ((base_local >> T.ctl_bit[j]) & 1) s_tid ^= T.ctl_sig[j];
 #pragma unroll
             for (int i = 0; i < kLoadsPerThread; ++i)
                 gb[goff(i * kTileThreads)] = W[s_tid ^ sig_of(i * kTileThreads)];
@@ -2497,7 +2507,56 @@ bool launch_fact_tma(double2* psi, FactPass& F, const double* mats, const CutTer
                      bool tables, bool phase, cudaStream_t s) {
     static thread_local TmaPass T;
     static thread_local TmaPieces pieces;
-    if (!tma_plan(F, psi, &T, &pieces)) return false;
+    // a CNOT pass behind this one (g_absorb): composed into the copy-out when all
+    // its targets are tile qubits (out[i] = in[f_1(..f_k(i))], f_j: bit t_j ^= bit c_j)
+    AbsorbCnots& ab = g_absorb;
+    static const bool absorb_ok = getenv("QSB_NO_ABSORB") == nullptr;
+    bool absorb = absorb_ok && ab.count > 0 && !ab.done && F.num_tiles == F.tiles_per_state;
+    uint64_t row[64];
+    int pos_of_qubit[64];
+    if (absorb) {
+        for (int q = 0; q < 64; ++q) row[q] = uint64_t(1) << q, pos_of_qubit[q] = -1;
+        for (int p = 0; p < kTileLog2; ++p) pos_of_qubit[F.tile_bits[p]] = p;
+        for (int j = ab.count - 1; j >= 0 && absorb; --j) {
+            const int t = ab.targets[j], c = ab.controls[j];
+            if (t < 0 || t >= F.m || c < 0 || c >= F.m || pos_of_qubit[t] < 0) absorb = false;
+            else row[t] ^= row[c];
+        }
+        int outside = 0;
+        for (int q = 0; q < F.m && absorb; ++q) {
+            if (pos_of_qubit[q] >= 0) continue;
+            bool used = false;
+            for (int p = 0; p < kTileLog2; ++p) used |= ((row[F.tile_bits[p]] >> q) & 1) != 0;
+            outside += used;
+        }
+        if (outside > kMaxAbsorbCtl) absorb = false;
+    }
+    const int saved_direct = F.direct_store;
+    if (absorb) F.direct_store = 0;  // the tile goes back through shared memory
+    if (!tma_plan(F, psi, &T, &pieces)) {
+        F.direct_store = saved_direct;
+        return false;
+    }
+    T.nctl = 0;
+    if (absorb) {
+        int sig2[kTileLog2];
+        auto column = [&](int q) {
+            int v = 0;
+            for (int p = 0; p < kTileLog2; ++p)
+                if ((row[F.tile_bits[p]] >> q) & 1) v ^= T.sig[p];
+            return v;
+        };
+        for (int b = 0; b < kTileLog2; ++b) sig2[b] = column(F.tile_bits[b]);
+        for (int q = 0; q < F.m; ++q) {
+            if (pos_of_qubit[q] >= 0) continue;
+            const int v = column(q);
+            if (!v) continue;
+            T.ctl_bit[T.nctl] = q;
+            T.ctl_sig[T.nctl++] = v;
+        }
+        for (int b = 0; b < kTileLog2; ++b) T.sig[b] = sig2[b];
+        ab.done = true;
+    }
     bool pre = false;
     for (int r = 0; r < F.num_rounds; ++r) pre |= F.fr[r].pre_any != 0;
     const bool diag = F.has_din || F.has_dout;
@@ -2734,6 +2793,7 @@ int launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_de
 }
 
 thread_local ConstIn g_const_in = {false, {0.0, 0.0}, 0};
+thread_local AbsorbCnots g_absorb = {};
 
 bool launch_perm(double2* psi, int m, const int* controls, const int* targets, int count,
                  cudaStream_t s) {
