@@ -329,6 +329,16 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
     uint64_t need = kLowMask;
     for (int i = 0; i < count; ++i)
         if (kind_has_target(prog[first + i].kind)) need |= uint64_t(1) << prog[first + i].target;
+    static thread_local bool no_absorb_fill = false;
+    bool absorb_fill = false;
+    if (g_absorb.count > 0 && !no_absorb_fill) {
+        // spare tile bits go to the targets of the CNOT pass behind this one, so
+        // that it can be folded into this pass (all of them or none); checked
+        // below: a tile the lean TMA kernel cannot take falls back to the plain fill
+        uint64_t want = need;
+        for (int i = 0; i < g_absorb.count; ++i) want |= uint64_t(1) << g_absorb.targets[i];
+        if (__builtin_popcountll(want) <= kTileLog2 && want != need) need = want, absorb_fill = true;
+    }
     for (int b = 0; __builtin_popcountll(need) < kTileLog2 && b < st->m; ++b) need |= uint64_t(1) << b;
     static thread_local TilePass P;
     memset(&P, 0, sizeof(P));
@@ -513,6 +523,12 @@ int launch_tile(qs_state* st, const qs_gate* prog, int first, int count, const C
         } else {
             ++i;
         }
+    }
+    if (absorb_fill && !absorb_tile_feasible(st->psi, P)) {
+        no_absorb_fill = true;
+        const int rc = launch_tile(st, prog, first, count, ct, mats_host);
+        no_absorb_fill = false;
+        return rc;
     }
     static const bool debug_plan = getenv("QSB_DEBUG_PLAN") != nullptr;
     if (debug_plan) {  // one line per pass: rounds as [gate kind:target ...]

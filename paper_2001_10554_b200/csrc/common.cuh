@@ -219,6 +219,9 @@ struct AbsorbCnots {
     bool done;
 };
 extern thread_local AbsorbCnots g_absorb;
+// the pass can run on the TMA lean kernel with its tile written back through
+// shared memory (what folding a CNOT pass into it needs)
+bool absorb_tile_feasible(double2* psi, const TilePass& pass);
 bool tile_pass_in_params();  // k_tile takes the pass as a kernel parameter
 // returns 0: k_tile, 1: the lean factored kernels (k_fact*), 2: a lean pass that
 // generated a constant input (g_const_in) instead of loading its tiles

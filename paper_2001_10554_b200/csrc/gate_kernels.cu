@@ -2535,7 +2535,9 @@ bool launch_fact_tma(double2* psi, FactPass& F, const double* mats, const CutTer
     if (absorb) F.direct_store = 0;  // the tile goes back through shared memory
     if (!tma_plan(F, psi, &T, &pieces)) {
         F.direct_store = saved_direct;
-        return false;
+        if (!absorb) return false;
+        absorb = false;  // no conflict-free lane order without the direct store: plain pass
+        if (!tma_plan(F, psi, &T, &pieces)) return false;
     }
     T.nctl = 0;
     if (absorb) {
@@ -2794,6 +2796,16 @@ int launch_tile_pass(double2* psi, const TilePass& pass, const TilePass* pass_de
 
 thread_local ConstIn g_const_in = {false, {0.0, 0.0}, 0};
 thread_local AbsorbCnots g_absorb = {};
+
+bool absorb_tile_feasible(double2* psi, const TilePass& pass) {
+    static thread_local FactPass F;
+    static thread_local TmaPass T;
+    static thread_local TmaPieces pieces;
+    bool tb = false, ph = false;
+    if (kGroups != 1 || !fact_pass_from(pass, &F, &tb, &ph)) return false;
+    F.direct_store = 0;
+    return tma_plan(F, psi, &T, &pieces);
+}
 
 bool launch_perm(double2* psi, int m, const int* controls, const int* targets, int count,
                  cudaStream_t s) {
