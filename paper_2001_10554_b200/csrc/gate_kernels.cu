@@ -1679,8 +1679,8 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T, TmaPieces* pieces = nullptr
     if (off || F.low_run < 3 || !encode_fn()) return false;
     const int m = F.m;
     const uint64_t num_states = F.num_tiles / F.tiles_per_state;
-    uint32_t is_tile = 0;  // over local qubits
-    for (int p = 0; p < kTileLog2; ++p) is_tile |= 1u << F.tile_bits[p];
+    uint64_t is_tile = 0;  // over local qubits
+    for (int p = 0; p < kTileLog2; ++p) is_tile |= uint64_t(1) << F.tile_bits[p];
     if (m > 62) return false;
     // position of each qubit among the tile positions (or -1)
     auto pos_of = [&](int q) {
@@ -1692,9 +1692,9 @@ bool tma_plan(FactPass& F, double2* psi, TmaPass* T, TmaPieces* pieces = nullptr
     std::vector<TmaDim> tile_runs, nontile;
     int below = 0;
     for (int q = 3; q < m;) {
-        const bool t = q < 32 && ((is_tile >> q) & 1);
+        const bool t = ((is_tile >> q) & 1) != 0;
         int e = q;
-        while (e + 1 < m && ((e + 1 < 32 && ((is_tile >> (e + 1)) & 1)) == t)) ++e;
+        while (e + 1 < m && (((is_tile >> (e + 1)) & 1) != 0) == t) ++e;
         TmaDim d{q, e - q + 1, t, false, 0};
         if (t) {
             tile_runs.push_back(d);
@@ -2107,8 +2107,8 @@ bool pair_plan(const FactPass& F, const TmaPieces& T, double2* psi, PairPass* X)
     static const bool off = getenv("QSB_NO_PAIR") != nullptr;
     if (off || F.low_run < 3 || (F.num_tiles & 1)) return false;
     const int m = F.m;
-    uint32_t is_tile = 0;
-    for (int q = 0; q < kTileLog2; ++q) is_tile |= 1u << F.tile_bits[q];
+    uint64_t is_tile = 0;
+    for (int q = 0; q < kTileLog2; ++q) is_tile |= uint64_t(1) << F.tile_bits[q];
     int p = 0;
     while (p < m && ((is_tile >> p) & 1)) ++p;
     if (p >= m || p >= 31) return false;
@@ -2127,7 +2127,7 @@ bool pair_plan(const FactPass& F, const TmaPieces& T, double2* psi, PairPass* X)
     if (!pair_row) dims.push_back({p, 1});
     if (1 + dims.size() > 5) return false;
     // non-tile runs of the 13-bit set, each on the dim below it
-    const uint32_t set13 = is_tile | (1u << p);
+    const uint64_t set13 = is_tile | (uint64_t(1) << p);
     struct N { int lo, len, field_shift; bool states; };
     std::vector<N> nontile;
     int below = 0;

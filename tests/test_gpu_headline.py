@@ -90,3 +90,53 @@ def test_config2_sweep_n30_exact_and_factored_vs_oracle():
     assert report["exact"]["bit_equal"], report
     assert report["factored"]["max_abs"] <= TOL, report
     assert not report["factored"]["bit_equal"]  # the factored rewrite really ran
+
+
+@pytest.mark.timeout(900)
+def test_config4_layer_n33_product_state():
+    """Config 4's N=1 point (n=33, 128 GiB): the lean passes whose tiles hold
+    qubit 32, the CNOT pass folded into the last of them and the k_perm pass,
+    checked through a size-independent property -- a Haar layer takes the
+    uniform product state to the product state of the gates' first-column
+    sums, and the CNOT layer permutes its indices -- on sampled index ranges,
+    factored mode (1e-12 absolute; the amplitudes are ~1e-5)."""
+    n = 33
+    try:
+        st = N.DeviceState(n, n)
+    except MemoryError as exc:
+        pytest.skip(f"no room for a 2^{n} state: {exc}")
+    rng = np.random.default_rng(3333)
+    us = [og.random_unitary_2x2(rng) for _ in range(n)]
+    pairs = [(q, n - 1 - q) for q in range(n // 2)]
+    X = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+    N.call("qs_init_constant", st.handle, 2.0 ** (-n / 2.0), 0.0)
+    q = runtime.GateQueue(st, fuse="factored")
+    for k in range(n):
+        q.one_qubit(k, us[k])
+    for c, t in pairs:
+        q.controlled(c, t, X)
+    passes = q.flush()
+    assert passes <= 6
+    # per-qubit factors of the product state after the Haar layer
+    f = np.array([(u @ np.array([1.0, 1.0])) / np.sqrt(2.0) for u in us])  # f[q][bit]
+
+    def expect(idx):
+        idx = np.asarray(idx, dtype=np.uint64)
+        src = idx.copy()
+        for c, t in reversed(pairs):  # out[i] = in[f_1(f_2(..f_k(i)))]
+            src ^= ((src >> np.uint64(c)) & np.uint64(1)) << np.uint64(t)
+        out = np.ones(idx.shape, dtype=np.complex128)
+        for k in range(n):
+            out *= f[k][((src >> np.uint64(k)) & np.uint64(1)).astype(np.int64)]
+        return out
+
+    worst = 0.0
+    for off in (0, 12345 * 4096, (1 << 32) + 777 * 512, (1 << 33) - 8192,
+                int(rng.integers(0, (1 << 33) - 8192)) & ~511):
+        got = st.download(offset=off, count=8192)
+        want = expect(np.arange(off, off + 8192, dtype=np.uint64))
+        worst = max(worst, float(np.max(np.abs(got - want))))
+    assert worst <= 1e-12, worst
+    assert worst <= 1e-9 * 2.0 ** (-n / 2.0) * 1e3  # ~1e-11 relative to the amplitude scale
+    norm = float(st.observable(N.QS_OBS_NORM)[0])
+    assert abs(norm - 1.0) <= 1e-10
